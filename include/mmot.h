@@ -1,0 +1,163 @@
+/* mmot.h -- C ABI of the B200-native fast tensor-vector product / multi-marginal Sinkhorn
+ * for the L1 pairwise cost on a uniform 1-D grid (arXiv 2405.19246).
+ *
+ * Citations: P:n = line n of the paper's LaTeX, with section / equation /
+ * algorithm.  Notation follows the paper and DESIGN.md:
+ *   l marginals, N grid points x_i = x_min + i h, h = (x_max - x_min)/(N-1)
+ *   cost c(i) = h sum_{p<q} |i_p - i_q|
+ *   kernel K = exp(-C/eta) = lambda^{E(i)}, lambda = e^{-h/eta}
+ *   scalings phi_1..phi_l, plan t_i = K_i prod_q phi_q[i_q]
+ *   J_k = K x_{q != k} phi_q  (tensor-vector product, mode k free)
+ *   k-th marginal of the plan m_k = phi_k * J_k
+ *   Sinkhorn update phi_k <- mu_k / J_k, k = 1..l, freshest peers
+ *   W = sum_i c(i) t(i) = <phi_l, (C.K) x_{q<l} phi_q>
+ *
+ * Conventions for every entry point:
+ *   - Array arguments of the compute calls are DEVICE pointers owned by the caller,
+ *     16-byte aligned, contiguous, element type given by the context dtype (MMOT_F64:
+ *     double; MMOT_F32: float) except where stated.  Marginal index k is 0-based.
+ *   - All work is enqueued on the context's CUDA stream; calls return without waiting
+ *     unless they fill a HOST output (mmot_sinkhorn's report, mmot_cost's W), in which
+ *     case they synchronise that stream once at the end.
+ *   - Argument errors are detected on the host before any launch.  Data errors (NaN/Inf,
+ *     negative or zero mass) are detected on device and reported through mmot_report /
+ *     the return value of the synchronising calls.
+ *   - A context is not reentrant: one host thread per context at a time.
+ *   - No call allocates device memory after mmot_create* except mmot_sinkhorn_host
+ *     (staging buffers, allocated once on first use).
+ */
+#ifndef MMOT_H_
+#define MMOT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MMOT_VERSION_MAJOR 0
+#define MMOT_VERSION_MINOR 1
+#define MMOT_MAX_L 6          /* supported marginal counts: 2..MMOT_MAX_L */
+
+#if defined(__GNUC__)
+#define MMOT_API __attribute__((visibility("default")))
+#else
+#define MMOT_API
+#endif
+
+typedef struct mmot_ctx mmot_ctx;  /* opaque; owns device workspace only */
+
+typedef enum { MMOT_F64 = 0, MMOT_F32 = 1 } mmot_dtype;
+
+/* Representation of the scaling vectors u[] passed to mmot_marginal / mmot_sinkhorn /
+ * mmot_cost / mmot_init_uniform.  MMOT_LOG (default): u[q] holds g_q = log phi_q (the
+ * paper's potentials up to sign/scale, Remark 1 P:138-151), -inf allowed.
+ * MMOT_LINEAR: u[q] holds phi_q itself.  u[] is always float64 (both dtypes). */
+typedef enum { MMOT_LOG = 0, MMOT_LINEAR = 1 } mmot_repr;
+
+typedef enum {
+    MMOT_OK = 0,
+    MMOT_EINVAL = 1,       /* invalid scalar argument (l, N, eta, grid, k, iters, NULL) */
+    MMOT_ESHAPE = 2,       /* pointer / batch / shard layout mismatch                     */
+    MMOT_ENONFINITE = 3,   /* NaN or Inf in a marginal or scaling vector                  */
+    MMOT_ENEGMASS = 4,     /* negative entry in a marginal                                */
+    MMOT_EZEROMASS = 5,    /* a marginal with zero total mass                              */
+    MMOT_EOVERFLOW = 6,    /* a product J_k left the representable range (P:1184 analogue) */
+    MMOT_ECUDA = 7,        /* CUDA runtime error (see mmot_last_error)                    */
+    MMOT_ENCCL = 8,        /* NCCL error (sharded contexts)                               */
+    MMOT_ENOMEM = 9,       /* device allocation failed                                    */
+    MMOT_EUNSUPPORTED = 10 /* valid request this build does not implement                */
+} mmot_status;
+
+/* Uniform grid x_i = x_min + i h, i = 0..N-1 (endpoints included, A1). */
+typedef struct { double x_min, x_max; } mmot_grid;
+
+typedef struct {
+    int check_every;    /* residual cadence in sweeps; 0 = only when tol > 0, every sweep (default) */
+    int residual_mode;  /* 0 = paper: sum_{k<l} ||m_k - mu_k||_1 (Alg. 1 line 7, generalised) */
+    mmot_repr repr;     /* representation of u[] (default MMOT_LOG) */
+    int chunk;          /* grid points per chunk; 0 = automatic */
+} mmot_opts;
+
+typedef struct {
+    int iters_done;     /* sweeps completed (each sweep = l updates) */
+    double residual;    /* last computed residual (NaN if never computed) */
+    int converged;      /* 1 if residual <= tol stopped the loop */
+    int status;         /* mmot_status of the run */
+    int fail_iter;      /* sweep index at which EOVERFLOW/ENONFINITE was detected, else -1 */
+} mmot_report;
+
+/* Create a context for single instances of (l, N, eta) on `grid`.
+ *   l in [2, MMOT_MAX_L], N >= 1, eta > 0 finite, x_max > x_min when N > 1.
+ *   dt: arithmetic of the scans (MMOT_F64 implemented; MMOT_F32 -> EUNSUPPORTED in v0.1).
+ *   opts may be NULL (defaults).  cuda_stream: cudaStream_t (NULL = legacy default stream).
+ * The per-edge weights w_a = lambda^{a(l-a)} = exp(-a(l-a) h/eta), a = 0..l, are computed
+ * once in fp64 on the host (A15).  Allocates all workspace.
+ * On error *out is set to NULL. */
+MMOT_API mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype dt,
+                        const mmot_opts *opts, void *cuda_stream, mmot_ctx **out);
+
+/* m_k = phi_k * J_k(phi_{-k}) -- the k-th marginal of K . (phi_1 x ... x phi_l)
+ * (P:1021), computed by the O(N) separated-summation scans.
+ *   k in [0, l); u: host array of l device pointers (repr per opts, float64, length N each);
+ *   out: device pointer, N elements of the context dtype (linear units).  Asynchronous. */
+MMOT_API mmot_status mmot_marginal(mmot_ctx *ctx, int k, const void *const *u, void *out);
+
+/* Generalized Sinkhorn (Algorithm 4): at most `iters` sweeps of the
+ * l Gauss-Seidel updates phi_k <- mu_k / J_k; after each sweep whose index is a multiple of
+ * check_every, Res = sum_{k<l-1} ||phi_k J_k - mu_k||_1 on the end-of-sweep vectors (P:168
+ * generalised, A6); stops after the first sweep with Res <= tol (tol <= 0: run
+ * exactly `iters` sweeps, no residual).  The loop, residual and stop flag stay on device.
+ *   marginals: host array of l device pointers to mu_q (context dtype, >= 0, sum > 0; the
+ *              library does not renormalise);
+ *   u: host array of l device pointers, in = initial scalings, out = final (repr per opts);
+ *   rep: host pointer, may be NULL.  Synchronises the context stream once at the end. */
+MMOT_API mmot_status mmot_sinkhorn(mmot_ctx *ctx, const void *const *marginals, int iters, double tol,
+                          void *const *u, mmot_report *rep);
+
+/* Same as mmot_sinkhorn with HOST buffers: marginals_host[q] (context dtype) and u_host[q]
+ * (float64, repr per opts) are copied to device staging buffers owned by the context, the
+ * solve runs, u is copied back.  Pinned host memory gives asynchronous copies.
+ * Synchronises once at the end. */
+MMOT_API mmot_status mmot_sinkhorn_host(mmot_ctx *ctx, const void *const *marginals_host, int iters,
+                               double tol, void *const *u_host, mmot_report *rep);
+
+/* W = sum_i c(i) t(i), the linear transport cost of the plan t = K . (phi_1 x .. x phi_l)
+ * (P:1037-1040), with a single factor h (Algorithm 4's return line P:652 applies h twice,
+ * DESIGN.md A8).  Computed as h <phi_l, hatJ_l> with hatJ = sum E lambda^E prod phi carried
+ * as the tangent of the same scans.  W: host pointer.  Synchronises. */
+MMOT_API mmot_status mmot_cost(mmot_ctx *ctx, const void *const *u, double *W);
+
+/* u_q <- the paper's initial scalings phi_q = 1/N: log phi = -log N (MMOT_LOG)
+ * or 1/N (MMOT_LINEAR).  u: host array of l device pointers.  Asynchronous. */
+MMOT_API mmot_status mmot_init_uniform(mmot_ctx *ctx, void *const *u);
+
+/* Release all workspace.  NULL is a no-op. */
+MMOT_API void mmot_destroy(mmot_ctx *ctx);
+
+/* Static description of a status code. */
+MMOT_API const char *mmot_strerror(mmot_status s);
+
+/* Last detailed error message of the context ("" if none).  ctx may be NULL (global). */
+MMOT_API const char *mmot_last_error(const mmot_ctx *ctx);
+
+/* Library version as (major << 16 | minor). */
+MMOT_API int mmot_version(void);
+
+/* Kernel-launch counter: number of CUDA kernels this context has launched so far. */
+MMOT_API int64_t mmot_launch_count(const mmot_ctx *ctx);
+
+/* Benchmark instrumentation.  While enabled, every tensor-vector product records CUDA events
+ * on the context stream around its phases.  mmot_profile_read synchronises the stream and
+ * returns, accumulated since the last read, the device milliseconds and product counts of
+ *   ms[0] operator phase, ms[1] scan phase, ms[2] apply phase, ms[3] whole product,
+ * and per mode in ms_mode[0..3] (marginal, update, residual, cost) with counts n_mode[0..3].
+ * Either output pointer may be NULL. */
+MMOT_API mmot_status mmot_profile_enable(mmot_ctx *ctx, int enable);
+MMOT_API mmot_status mmot_profile_read(mmot_ctx *ctx, double *ms /*[4]*/, double *ms_mode /*[4]*/,
+                                       int64_t *n_mode /*[4]*/);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMOT_H_ */

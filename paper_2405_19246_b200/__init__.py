@@ -1,0 +1,224 @@
+"""B200-native fast tensor-vector product / multi-marginal Sinkhorn, L1 cost (arXiv 2405.19246).
+
+Thin Python binding of ``libmmot.so`` (C ABI in ``include/mmot.h``).  Argument
+marshalling only: every step of the path runs in the library's CUDA kernels.
+PyTorch is used for device memory and streams.  There is no CPU fallback: if
+the shared library is missing or no CUDA device is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from typing import List, Optional, Sequence
+
+__all__ = ["Context", "MMOTError", "lib_path", "load_library", "STATUS", "exported_symbols"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libmmot.so")
+_lib = None
+
+STATUS = {
+    0: "MMOT_OK", 1: "MMOT_EINVAL", 2: "MMOT_ESHAPE", 3: "MMOT_ENONFINITE", 4: "MMOT_ENEGMASS",
+    5: "MMOT_EZEROMASS", 6: "MMOT_EOVERFLOW", 7: "MMOT_ECUDA", 8: "MMOT_ENCCL", 9: "MMOT_ENOMEM",
+    10: "MMOT_EUNSUPPORTED",
+}
+
+F64, F32 = 0, 1
+LOG, LINEAR = 0, 1
+
+
+class MMOTError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class _Grid(ctypes.Structure):
+    _fields_ = [("x_min", ctypes.c_double), ("x_max", ctypes.c_double)]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("check_every", ctypes.c_int), ("residual_mode", ctypes.c_int),
+                ("repr", ctypes.c_int), ("chunk", ctypes.c_int)]
+
+
+class _Report(ctypes.Structure):
+    _fields_ = [("iters_done", ctypes.c_int), ("residual", ctypes.c_double), ("converged", ctypes.c_int),
+                ("status", ctypes.c_int), ("fail_iter", ctypes.c_int)]
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libmmot.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} not built; run `python -m paper_2405_19246_b200._build` "
+                          "or __graft_entry__.build()")
+    lib = ctypes.CDLL(_LIB_PATH)
+    vp = ctypes.c_void_p
+    vpp = ctypes.POINTER(ctypes.c_void_p)
+    lib.mmot_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_double, _Grid, ctypes.c_int,
+                                ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
+    lib.mmot_create.restype = ctypes.c_int
+    lib.mmot_marginal.argtypes = [vp, ctypes.c_int, vpp, vp]
+    lib.mmot_marginal.restype = ctypes.c_int
+    lib.mmot_sinkhorn.argtypes = [vp, vpp, ctypes.c_int, ctypes.c_double, vpp, ctypes.POINTER(_Report)]
+    lib.mmot_sinkhorn.restype = ctypes.c_int
+    lib.mmot_sinkhorn_host.argtypes = [vp, vpp, ctypes.c_int, ctypes.c_double, vpp, ctypes.POINTER(_Report)]
+    lib.mmot_sinkhorn_host.restype = ctypes.c_int
+    lib.mmot_cost.argtypes = [vp, vpp, ctypes.POINTER(ctypes.c_double)]
+    lib.mmot_cost.restype = ctypes.c_int
+    lib.mmot_init_uniform.argtypes = [vp, vpp]
+    lib.mmot_init_uniform.restype = ctypes.c_int
+    lib.mmot_destroy.argtypes = [vp]
+    lib.mmot_destroy.restype = None
+    lib.mmot_strerror.argtypes = [ctypes.c_int]
+    lib.mmot_strerror.restype = ctypes.c_char_p
+    lib.mmot_last_error.argtypes = [vp]
+    lib.mmot_last_error.restype = ctypes.c_char_p
+    lib.mmot_version.argtypes = []
+    lib.mmot_version.restype = ctypes.c_int
+    lib.mmot_launch_count.argtypes = [vp]
+    lib.mmot_launch_count.restype = ctypes.c_int64
+    lib.mmot_profile_enable.argtypes = [vp, ctypes.c_int]
+    lib.mmot_profile_enable.restype = ctypes.c_int
+    dp = ctypes.POINTER(ctypes.c_double)
+    lib.mmot_profile_read.argtypes = [vp, dp, dp, ctypes.POINTER(ctypes.c_int64)]
+    lib.mmot_profile_read.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def exported_symbols() -> List[str]:
+    """Dynamic symbols of libmmot.so starting with ``mmot_`` (no GPU needed)."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", _LIB_PATH], capture_output=True, text=True, check=True).stdout
+    return sorted({ln.split()[-1] for ln in out.splitlines() if ln.split() and ln.split()[-1].startswith("mmot_")})
+
+
+def _ptr_array(ptrs: Sequence[int]):
+    arr = (ctypes.c_void_p * len(ptrs))()
+    for i, p in enumerate(ptrs):
+        arr[i] = p
+    return arr
+
+
+class Context:
+    """One MMOT problem shape (l, N, eta, grid) with its device workspace.
+
+    Tensors passed in are torch CUDA tensors (float64, contiguous); the binding only
+    forwards their data pointers and the current CUDA stream to the C ABI.
+    """
+
+    def __init__(self, l: int, N: int, eta: float, grid=(0.0, 1.0), dtype: str = "f64",
+                 repr: str = "log", check_every: int = 0, chunk: int = 0, stream=None):
+        import torch
+        self._lib = load_library()
+        if not torch.cuda.is_available():
+            raise MMOTError(7, "no CUDA device: the library has no CPU path")
+        self.l, self.N, self.eta = int(l), int(N), float(eta)
+        self.grid = (float(grid[0]), float(grid[1]))
+        self.repr = repr
+        self.h = (self.grid[1] - self.grid[0]) / (self.N - 1) if self.N > 1 else 1.0
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        opts = _Opts(int(check_every), 0, LOG if repr == "log" else LINEAR, int(chunk))
+        ctx = ctypes.c_void_p()
+        st = self._lib.mmot_create(self.l, self.N, self.eta, _Grid(*self.grid), F64 if dtype == "f64" else F32,
+                                   ctypes.byref(opts), ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx))
+        if st != 0:
+            raise MMOTError(st, self._lib.mmot_last_error(None).decode())
+        self._ctx = ctx
+
+    # -- helpers ------------------------------------------------------------------------
+    def _check(self, st: int):
+        if st != 0:
+            raise MMOTError(st, self._lib.mmot_last_error(self._ctx).decode())
+
+    def _ptrs(self, ts) -> ctypes.Array:
+        if len(ts) != self.l:
+            raise MMOTError(2, f"expected {self.l} vectors, got {len(ts)}")
+        for t in ts:
+            if not t.is_cuda or not t.is_contiguous() or t.numel() != self.N:
+                raise MMOTError(2, "vectors must be contiguous CUDA tensors of length N")
+        return _ptr_array([t.data_ptr() for t in ts])
+
+    @property
+    def launches(self) -> int:
+        return int(self._lib.mmot_launch_count(self._ctx))
+
+    # -- ABI calls ------------------------------------------------------------------------
+    def init_uniform(self, u) -> None:
+        self._check(self._lib.mmot_init_uniform(self._ctx, self._ptrs(u)))
+
+    def marginal(self, k: int, u, out=None):
+        import torch
+        if out is None:
+            out = torch.empty(self.N, dtype=torch.float64, device=u[0].device)
+        self._check(self._lib.mmot_marginal(self._ctx, int(k), self._ptrs(u), ctypes.c_void_p(out.data_ptr())))
+        return out
+
+    def sinkhorn(self, marginals, iters: int, tol: float, u) -> dict:
+        rep = _Report()
+        st = self._lib.mmot_sinkhorn(self._ctx, self._ptrs(marginals), int(iters), float(tol), self._ptrs(u),
+                                     ctypes.byref(rep))
+        out = dict(iters_done=rep.iters_done, residual=rep.residual, converged=bool(rep.converged),
+                   status=rep.status, fail_iter=rep.fail_iter)
+        if st != 0:
+            err = MMOTError(st, self._lib.mmot_last_error(self._ctx).decode())
+            err.report = out
+            raise err
+        return out
+
+    def sinkhorn_host(self, marginals_host, iters: int, tol: float, u_host) -> dict:
+        """Host (pinned torch CPU or numpy) buffers; copies happen inside the call."""
+        def hp(a):
+            return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+        rep = _Report()
+        st = self._lib.mmot_sinkhorn_host(self._ctx, _ptr_array([hp(a) for a in marginals_host]), int(iters),
+                                          float(tol), _ptr_array([hp(a) for a in u_host]), ctypes.byref(rep))
+        self._check(st)
+        return dict(iters_done=rep.iters_done, residual=rep.residual, converged=bool(rep.converged),
+                    status=rep.status, fail_iter=rep.fail_iter)
+
+    def cost(self, u) -> float:
+        W = ctypes.c_double()
+        self._check(self._lib.mmot_cost(self._ctx, self._ptrs(u), ctypes.byref(W)))
+        return W.value
+
+    def profile(self, enable: bool = True) -> None:
+        self._check(self._lib.mmot_profile_enable(self._ctx, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        """Device ms per product phase (ops, scan, apply, total) and per mode since the last read."""
+        ms = (ctypes.c_double * 4)()
+        msm = (ctypes.c_double * 4)()
+        nm = (ctypes.c_int64 * 4)()
+        self._check(self._lib.mmot_profile_read(self._ctx, ms, msm, nm))
+        modes = ["marginal", "update", "residual", "cost"]
+        return dict(phase_ms=dict(ops=ms[0], scan=ms[1], apply=ms[2], total=ms[3]),
+                    mode_ms={m: msm[i] for i, m in enumerate(modes)},
+                    mode_n={m: int(nm[i]) for i, m in enumerate(modes)})
+
+    def close(self) -> None:
+        if getattr(self, "_ctx", None):
+            self._lib.mmot_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,514 @@
+// api.cu -- the C ABI declared in include/mmot.h: argument validation, context workspace,
+// and the device-resident Sinkhorn driver (Algorithm 4).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/mmot.h"
+#include "internal.h"
+
+using mmot::Plan;
+
+namespace {
+
+struct DevScalars {
+    int stop;
+    int status;
+    int fail_iter;
+    int iters_done;
+    int converged;
+    int flags[2 * mmot::kMaxL];
+    int pad;
+    double resid;
+    double res_acc;
+    double W;
+    double mass[mmot::kMaxL];
+};
+
+char g_err[256] = "";
+
+}  // namespace
+
+struct mmot_ctx {
+    int l = 0;
+    int64_t N = 0;
+    double eta = 0, h = 0;
+    mmot_grid grid{0, 1};
+    mmot_dtype dt = MMOT_F64;
+    mmot_opts opts{0, 0, MMOT_LOG, 0};
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    mmot::Weights W{};
+    int64_t P = 0, nchunks = 0;
+    int nlev = 0;
+    int64_t nlev_n[mmot::kMaxLevels] = {0};
+    void *ws = nullptr;
+    void *ops_f[mmot::kMaxLevels] = {nullptr}, *ops_b[mmot::kMaxLevels] = {nullptr};
+    void *car_f[mmot::kMaxLevels] = {nullptr}, *car_b[mmot::kMaxLevels] = {nullptr};
+    double *partial = nullptr;
+    DevScalars *dsc = nullptr;
+    DevScalars *hsc = nullptr;  // pinned host mirror
+    double *lin[mmot::kMaxL] = {nullptr};  // internal linear scalings (MMOT_LOG repr)
+    double *stage_mu[mmot::kMaxL] = {nullptr};
+    double *stage_u[mmot::kMaxL] = {nullptr};
+    int *hstop = nullptr;       // pinned, async stop polling
+    cudaEvent_t poll_ev = nullptr;
+    int64_t launches = 0;
+    char err[256] = "";
+    // profiling (mmot_profile_enable)
+    bool prof = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<int> pool_mode;
+    size_t used = 0;
+};
+
+static cudaEvent_t *prof_events(mmot_ctx *c, int mode) {
+    if (!c->prof) return nullptr;
+    if (c->used + 4 > c->pool.size()) {
+        for (int i = 0; i < 4; ++i) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+            c->pool.push_back(e);
+        }
+    }
+    cudaEvent_t *ev = &c->pool[c->used];
+    c->pool_mode.push_back(mode);
+    c->used += 4;
+    return ev;
+}
+
+static void set_err(mmot_ctx *c, const char *fmt, ...) {
+    char buf[256];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) snprintf(c->err, sizeof c->err, "%s", buf);
+    snprintf(g_err, sizeof g_err, "%s", buf);
+}
+
+#define CK(ctx, call)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            set_err(ctx, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+            return e_ == cudaErrorMemoryAllocation ? MMOT_ENOMEM : MMOT_ECUDA;          \
+        }                                                                               \
+    } while (0)
+
+extern "C" {
+
+const char *mmot_strerror(mmot_status s) {
+    switch (s) {
+        case MMOT_OK: return "ok";
+        case MMOT_EINVAL: return "invalid argument";
+        case MMOT_ESHAPE: return "shape / pointer layout mismatch";
+        case MMOT_ENONFINITE: return "non-finite input";
+        case MMOT_ENEGMASS: return "negative mass in a marginal";
+        case MMOT_EZEROMASS: return "marginal with zero total mass";
+        case MMOT_EOVERFLOW: return "tensor-vector product left the representable range";
+        case MMOT_ECUDA: return "CUDA error";
+        case MMOT_ENCCL: return "NCCL error";
+        case MMOT_ENOMEM: return "device allocation failed";
+        case MMOT_EUNSUPPORTED: return "unsupported in this build";
+    }
+    return "unknown status";
+}
+
+const char *mmot_last_error(const mmot_ctx *ctx) { return ctx ? ctx->err : g_err; }
+
+int mmot_version(void) { return (MMOT_VERSION_MAJOR << 16) | MMOT_VERSION_MINOR; }
+
+int64_t mmot_launch_count(const mmot_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+void mmot_destroy(mmot_ctx *ctx) {
+    if (!ctx) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    else cudaDeviceSynchronize();
+    cudaFree(ctx->ws);
+    for (int q = 0; q < mmot::kMaxL; ++q) {
+        cudaFree(ctx->lin[q]);
+        cudaFree(ctx->stage_mu[q]);
+        cudaFree(ctx->stage_u[q]);
+    }
+    if (ctx->hsc) cudaFreeHost(ctx->hsc);
+    if (ctx->hstop) cudaFreeHost(ctx->hstop);
+    if (ctx->poll_ev) cudaEventDestroy(ctx->poll_ev);
+    for (cudaEvent_t e : ctx->pool) cudaEventDestroy(e);
+    cudaSetDevice(cur);
+    delete ctx;
+}
+
+mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype dt, const mmot_opts *opts,
+                        void *cuda_stream, mmot_ctx **out) {
+    if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
+    *out = nullptr;
+    if (l < 2 || l > 8) { set_err(nullptr, "l=%d outside [2,8]", l); return MMOT_EINVAL; }
+    if (N < 1) { set_err(nullptr, "N=%lld < 1", (long long)N); return MMOT_EINVAL; }
+    if (!(eta > 0) || !isfinite(eta)) { set_err(nullptr, "eta must be finite and > 0"); return MMOT_EINVAL; }
+    if (!isfinite(grid.x_min) || !isfinite(grid.x_max) || (N > 1 && !(grid.x_max > grid.x_min))) {
+        set_err(nullptr, "grid must satisfy x_max > x_min");
+        return MMOT_EINVAL;
+    }
+    if (dt != MMOT_F64 && dt != MMOT_F32) { set_err(nullptr, "bad dtype"); return MMOT_EINVAL; }
+    if (opts && (opts->check_every < 0 || opts->chunk < 0 || (opts->repr != MMOT_LOG && opts->repr != MMOT_LINEAR))) {
+        set_err(nullptr, "bad opts");
+        return MMOT_EINVAL;
+    }
+    if (l > MMOT_MAX_L) { set_err(nullptr, "l=%d > MMOT_MAX_L=%d in this build", l, MMOT_MAX_L); return MMOT_EUNSUPPORTED; }
+    if (dt == MMOT_F32) { set_err(nullptr, "MMOT_F32 single-instance contexts are not implemented yet"); return MMOT_EUNSUPPORTED; }
+
+    mmot_ctx *c = new mmot_ctx();
+    c->l = l;
+    c->N = N;
+    c->eta = eta;
+    c->grid = grid;
+    c->dt = dt;
+    if (opts) c->opts = *opts;
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    cudaGetDevice(&c->device);
+    c->h = N > 1 ? (grid.x_max - grid.x_min) / (double)(N - 1) : 1.0;
+    // w_a = lambda^{a(l-a)} = exp(-a(l-a) h/eta) in fp64 (A15)
+    for (int a = 0; a <= mmot::kMaxL; ++a) {
+        const int e = a <= l ? a * (l - a) : 0;
+        c->W.e[a] = (double)e;
+        c->W.w[a] = a <= l ? exp(-(double)e * c->h / eta) : 0.0;
+    }
+    const int NB = l - 1;
+    const int64_t pmax = mmot::chunk_max(NB);
+    const int q = mmot::sub_q(NB);
+    int64_t P;
+    if (c->opts.chunk > 0) {
+        P = std::min<int64_t>(c->opts.chunk, pmax);
+    } else {
+        const int64_t target = 148 * 256;
+        P = (N + target - 1) / target;
+        P = ((P + q - 1) / q) * q;
+        P = std::max<int64_t>(q, std::min<int64_t>(P, pmax));
+    }
+    c->P = P;
+    c->nchunks = (N + P - 1) / P;
+    // levels of the hierarchical operator scan
+    int64_t n = c->nchunks;
+    c->nlev = 0;
+    while (true) {
+        c->nlev_n[c->nlev++] = n;
+        if (n <= mmot::kGroup || c->nlev == mmot::kMaxLevels) break;
+        n = (n + mmot::kGroup - 1) / mmot::kGroup;
+    }
+    // workspace, sized for dual numbers (the cost) so every mode fits
+    const int M = 1 << NB;
+    const size_t opsz = (size_t)(NB + 1) * M * sizeof(mmot::Dual);
+    const size_t carsz = (size_t)M * sizeof(mmot::Dual);
+    size_t total = 0;
+    size_t off_ops[mmot::kMaxLevels], off_car[mmot::kMaxLevels];
+    for (int i = 0; i < c->nlev; ++i) {
+        off_ops[i] = total;
+        total += 2 * (size_t)c->nlev_n[i] * opsz;
+        total = (total + 255) & ~(size_t)255;
+        off_car[i] = total;
+        total += 2 * (size_t)c->nlev_n[i] * carsz;
+        total = (total + 255) & ~(size_t)255;
+    }
+    const size_t off_part = total;
+    total += (size_t)c->nchunks * sizeof(double);
+    total = (total + 255) & ~(size_t)255;
+    const size_t off_sc = total;
+    total += sizeof(DevScalars);
+    cudaError_t e = cudaMalloc(&c->ws, total);
+    if (e != cudaSuccess) {
+        set_err(c, "cudaMalloc(%zu): %s", total, cudaGetErrorString(e));
+        snprintf(g_err, sizeof g_err, "%s", c->err);
+        delete c;
+        return MMOT_ENOMEM;
+    }
+    char *base = static_cast<char *>(c->ws);
+    for (int i = 0; i < c->nlev; ++i) {
+        c->ops_f[i] = base + off_ops[i];
+        c->ops_b[i] = base + off_ops[i] + (size_t)c->nlev_n[i] * opsz;
+        c->car_f[i] = base + off_car[i];
+        c->car_b[i] = base + off_car[i] + (size_t)c->nlev_n[i] * carsz;
+    }
+    c->partial = reinterpret_cast<double *>(base + off_part);
+    c->dsc = reinterpret_cast<DevScalars *>(base + off_sc);
+    if (c->opts.repr == MMOT_LOG) {
+        for (int qq = 0; qq < l; ++qq) {
+            e = cudaMalloc(&c->lin[qq], (size_t)N * sizeof(double));
+            if (e != cudaSuccess) {
+                set_err(c, "cudaMalloc scalings: %s", cudaGetErrorString(e));
+                snprintf(g_err, sizeof g_err, "%s", c->err);
+                mmot_destroy(c);
+                return MMOT_ENOMEM;
+            }
+        }
+    }
+    if (cudaMallocHost(&c->hsc, sizeof(DevScalars)) != cudaSuccess ||
+        cudaMallocHost(&c->hstop, sizeof(int)) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->poll_ev, cudaEventDisableTiming) != cudaSuccess) {
+        set_err(c, "host allocation failed");
+        snprintf(g_err, sizeof g_err, "%s", c->err);
+        mmot_destroy(c);
+        return MMOT_ENOMEM;
+    }
+    if (cudaMemsetAsync(c->dsc, 0, sizeof(DevScalars), c->stream) != cudaSuccess) {
+        set_err(c, "memset failed");
+        mmot_destroy(c);
+        return MMOT_ECUDA;
+    }
+    *out = c;
+    return MMOT_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double *mu, double *out, int iter) {
+    Plan p{};
+    p.NB = c->l - 1;
+    p.N = c->N;
+    p.P = c->P;
+    p.nchunks = c->nchunks;
+    int b = 0;
+    for (int q = 0; q < c->l; ++q)
+        if (q != k) p.bound[b++] = lin[q];
+    p.phik = lin[k];
+    p.muk = mu;
+    p.outk = out;
+    p.W = c->W;
+    p.nlev = c->nlev;
+    for (int i = 0; i < c->nlev; ++i) {
+        p.nlev_n[i] = c->nlev_n[i];
+        p.ops_f[i] = c->ops_f[i];
+        p.ops_b[i] = c->ops_b[i];
+        p.car_f[i] = c->car_f[i];
+        p.car_b[i] = c->car_b[i];
+    }
+    p.partial = c->partial;
+    p.stop = &c->dsc->stop;
+    p.status = &c->dsc->status;
+    p.fail_iter = &c->dsc->fail_iter;
+    p.iter = iter;
+    return p;
+}
+
+static mmot_status reset_scalars(mmot_ctx *c) {
+    CK(c, cudaMemsetAsync(c->dsc, 0, sizeof(DevScalars), c->stream));
+    return MMOT_OK;
+}
+
+// Resolve the linear scalings used by the kernels (convert from log if needed).
+static mmot_status to_linear(mmot_ctx *c, const void *const *u, const double **lin) {
+    for (int q = 0; q < c->l; ++q) {
+        if (!u[q]) { set_err(c, "u[%d] is NULL", q); return MMOT_EINVAL; }
+        if (c->opts.repr == MMOT_LOG) {
+            CK(c, mmot::launch_exp(static_cast<const double *>(u[q]), c->lin[q], c->N, c->stream, &c->launches));
+            lin[q] = c->lin[q];
+        } else {
+            lin[q] = static_cast<const double *>(u[q]);
+        }
+    }
+    return MMOT_OK;
+}
+
+static mmot_status sync_report(mmot_ctx *c) {
+    CK(c, cudaMemcpyAsync(c->hsc, c->dsc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return MMOT_OK;
+}
+
+static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters, double tol, void *const *u,
+                                 mmot_report *rep) {
+    const int l = c->l;
+    mmot_status st = reset_scalars(c);
+    if (st) return st;
+    // data checks (P:75 marginals are probability vectors; SPEC S:77 error vocabulary)
+    for (int q = 0; q < l; ++q) {
+        CK(c, mmot::launch_check(mu[q], c->N, 0, &c->dsc->flags[q], &c->dsc->mass[q], c->stream, &c->launches));
+        CK(c, mmot::launch_check(static_cast<const double *>(u[q]), c->N, c->opts.repr == MMOT_LOG ? 1 : 0,
+                                 &c->dsc->flags[l + q], nullptr, c->stream, &c->launches));
+    }
+    CK(c, mmot::launch_check_finish(c->dsc->flags, c->dsc->mass, 2 * l, l, &c->dsc->status, &c->dsc->stop,
+                                    &c->dsc->fail_iter, c->stream, &c->launches));
+    // working scalings
+    double *lin[mmot::kMaxL];
+    for (int q = 0; q < l; ++q) {
+        if (c->opts.repr == MMOT_LOG) {
+            CK(c, mmot::launch_exp(static_cast<const double *>(u[q]), c->lin[q], c->N, c->stream, &c->launches));
+            lin[q] = c->lin[q];
+        } else {
+            lin[q] = static_cast<double *>(u[q]);
+        }
+    }
+    const int check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
+    bool poll_pending = false;
+    for (int t = 1; t <= iters; ++t) {
+        // asynchronous early exit: the device stop flag is polled without blocking
+        if (poll_pending && cudaEventQuery(c->poll_ev) == cudaSuccess) {
+            poll_pending = false;
+            if (*c->hstop) break;
+        }
+        for (int k = 0; k < l; ++k) {
+            Plan p = make_plan(c, k, lin, mu[k], lin[k], t);
+            CK(c, mmot::launch_product(p, mmot::MODE_UPD, c->stream, &c->launches, prof_events(c, mmot::MODE_UPD)));
+        }
+        if (tol > 0 && (t % check_every == 0 || t == iters)) {
+            for (int k = 0; k + 1 < l; ++k) {
+                Plan p = make_plan(c, k, lin, mu[k], nullptr, t);
+                CK(c, mmot::launch_product(p, mmot::MODE_RES, c->stream, &c->launches, prof_events(c, mmot::MODE_RES)));
+                CK(c, mmot::launch_sum(c->partial, c->nchunks, &c->dsc->res_acc, 1.0, k > 0, &c->dsc->stop, c->stream,
+                                       &c->launches));
+            }
+            CK(c, mmot::launch_resid_finish(&c->dsc->res_acc, tol, t, &c->dsc->resid, &c->dsc->iters_done,
+                                            &c->dsc->converged, &c->dsc->stop, c->stream, &c->launches));
+        } else {
+            CK(c, mmot::launch_sweep_done(t, &c->dsc->iters_done, &c->dsc->stop, c->stream, &c->launches));
+        }
+        if (tol > 0 && !poll_pending && (t % 8 == 0)) {
+            CK(c, cudaMemcpyAsync(c->hstop, &c->dsc->stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+            CK(c, cudaEventRecord(c->poll_ev, c->stream));
+            poll_pending = true;
+        }
+    }
+    if (c->opts.repr == MMOT_LOG)
+        for (int q = 0; q < l; ++q)
+            CK(c, mmot::launch_log(c->lin[q], static_cast<double *>(u[q]), c->N, c->stream, &c->launches));
+    st = sync_report(c);
+    if (st) return st;
+    const DevScalars &h = *c->hsc;
+    if (rep) {
+        rep->iters_done = h.iters_done;
+        rep->residual = tol > 0 && h.iters_done > 0 ? h.resid : NAN;
+        rep->converged = h.converged;
+        rep->status = h.status;
+        rep->fail_iter = h.status ? h.fail_iter : -1;
+    }
+    if (h.status) set_err(c, "%s (sweep %d)", mmot_strerror((mmot_status)h.status), h.fail_iter);
+    return (mmot_status)h.status;
+}
+
+extern "C" {
+
+mmot_status mmot_marginal(mmot_ctx *c, int k, const void *const *u, void *out) {
+    if (!c || !u || !out) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
+    if (k < 0 || k >= c->l) { set_err(c, "k=%d outside [0,%d)", k, c->l); return MMOT_EINVAL; }
+    cudaSetDevice(c->device);
+    mmot_status st = reset_scalars(c);
+    if (st) return st;
+    const double *lin[mmot::kMaxL];
+    st = to_linear(c, u, lin);
+    if (st) return st;
+    Plan p = make_plan(c, k, lin, nullptr, static_cast<double *>(out), 0);
+    CK(c, mmot::launch_product(p, mmot::MODE_MARG, c->stream, &c->launches, prof_events(c, mmot::MODE_MARG)));
+    return MMOT_OK;
+}
+
+mmot_status mmot_sinkhorn(mmot_ctx *c, const void *const *marginals, int iters, double tol, void *const *u,
+                          mmot_report *rep) {
+    if (rep) { rep->iters_done = 0; rep->residual = NAN; rep->converged = 0; rep->status = 0; rep->fail_iter = -1; }
+    if (!c || !marginals || !u) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
+    if (iters < 0 || isnan(tol)) { set_err(c, "iters must be >= 0"); return MMOT_EINVAL; }
+    const double *mu[mmot::kMaxL];
+    for (int q = 0; q < c->l; ++q) {
+        if (!marginals[q] || !u[q]) { set_err(c, "marginals[%d] or u[%d] is NULL", q, q); return MMOT_EINVAL; }
+        mu[q] = static_cast<const double *>(marginals[q]);
+    }
+    cudaSetDevice(c->device);
+    return sinkhorn_impl(c, mu, iters, tol, u, rep);
+}
+
+mmot_status mmot_sinkhorn_host(mmot_ctx *c, const void *const *marginals_host, int iters, double tol,
+                               void *const *u_host, mmot_report *rep) {
+    if (rep) { rep->iters_done = 0; rep->residual = NAN; rep->converged = 0; rep->status = 0; rep->fail_iter = -1; }
+    if (!c || !marginals_host || !u_host) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
+    if (iters < 0 || isnan(tol)) { set_err(c, "iters must be >= 0"); return MMOT_EINVAL; }
+    cudaSetDevice(c->device);
+    const size_t bytes = (size_t)c->N * sizeof(double);
+    for (int q = 0; q < c->l; ++q) {
+        if (!marginals_host[q] || !u_host[q]) { set_err(c, "NULL host pointer"); return MMOT_EINVAL; }
+        if (!c->stage_mu[q]) CK(c, cudaMalloc(&c->stage_mu[q], bytes));
+        if (!c->stage_u[q]) CK(c, cudaMalloc(&c->stage_u[q], bytes));
+        CK(c, cudaMemcpyAsync(c->stage_mu[q], marginals_host[q], bytes, cudaMemcpyHostToDevice, c->stream));
+        CK(c, cudaMemcpyAsync(c->stage_u[q], u_host[q], bytes, cudaMemcpyHostToDevice, c->stream));
+    }
+    const double *mu[mmot::kMaxL];
+    void *ud[mmot::kMaxL];
+    for (int q = 0; q < c->l; ++q) {
+        mu[q] = c->stage_mu[q];
+        ud[q] = c->stage_u[q];
+    }
+    mmot_status st = sinkhorn_impl(c, mu, iters, tol, ud, rep);
+    for (int q = 0; q < c->l; ++q)
+        CK(c, cudaMemcpyAsync(u_host[q], c->stage_u[q], bytes, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return st;
+}
+
+mmot_status mmot_cost(mmot_ctx *c, const void *const *u, double *W) {
+    if (!c || !u || !W) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
+    cudaSetDevice(c->device);
+    mmot_status st = reset_scalars(c);
+    if (st) return st;
+    const double *lin[mmot::kMaxL];
+    st = to_linear(c, u, lin);
+    if (st) return st;
+    const int k = c->l - 1;
+    Plan p = make_plan(c, k, lin, nullptr, nullptr, 0);
+    CK(c, mmot::launch_product(p, mmot::MODE_COST, c->stream, &c->launches, prof_events(c, mmot::MODE_COST)));
+    CK(c, mmot::launch_sum(c->partial, c->nchunks, &c->dsc->W, c->h, 0, &c->dsc->stop, c->stream, &c->launches));
+    st = sync_report(c);
+    if (st) return st;
+    *W = c->hsc->W;
+    return (mmot_status)c->hsc->status;
+}
+
+mmot_status mmot_profile_enable(mmot_ctx *c, int enable) {
+    if (!c) { set_err(c, "NULL context"); return MMOT_EINVAL; }
+    c->prof = enable != 0;
+    return MMOT_OK;
+}
+
+mmot_status mmot_profile_read(mmot_ctx *c, double *ms, double *ms_mode, int64_t *n_mode) {
+    if (!c) { set_err(c, "NULL context"); return MMOT_EINVAL; }
+    CK(c, cudaStreamSynchronize(c->stream));
+    double acc[4] = {0, 0, 0, 0}, accm[4] = {0, 0, 0, 0};
+    int64_t nm[4] = {0, 0, 0, 0};
+    for (size_t i = 0; i + 4 <= c->used; i += 4) {
+        float t01 = 0, t12 = 0, t23 = 0, t03 = 0;
+        CK(c, cudaEventElapsedTime(&t01, c->pool[i], c->pool[i + 1]));
+        CK(c, cudaEventElapsedTime(&t12, c->pool[i + 1], c->pool[i + 2]));
+        CK(c, cudaEventElapsedTime(&t23, c->pool[i + 2], c->pool[i + 3]));
+        CK(c, cudaEventElapsedTime(&t03, c->pool[i], c->pool[i + 3]));
+        acc[0] += t01; acc[1] += t12; acc[2] += t23; acc[3] += t03;
+        const int m = c->pool_mode[i / 4];
+        accm[m] += t03;
+        nm[m] += 1;
+    }
+    c->used = 0;
+    c->pool_mode.clear();
+    if (ms) for (int i = 0; i < 4; ++i) ms[i] = acc[i];
+    if (ms_mode) for (int i = 0; i < 4; ++i) ms_mode[i] = accm[i];
+    if (n_mode) for (int i = 0; i < 4; ++i) n_mode[i] = nm[i];
+    return MMOT_OK;
+}
+
+mmot_status mmot_init_uniform(mmot_ctx *c, void *const *u) {
+    if (!c || !u) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
+    cudaSetDevice(c->device);
+    const double v = c->opts.repr == MMOT_LOG ? -log((double)c->N) : 1.0 / (double)c->N;
+    for (int q = 0; q < c->l; ++q) {
+        if (!u[q]) { set_err(c, "u[%d] is NULL", q); return MMOT_EINVAL; }
+        CK(c, mmot::launch_fill(static_cast<double *>(u[q]), v, c->N, c->stream, &c->launches));
+    }
+    return MMOT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,191 @@
+// dp.cuh -- device building blocks of the O(N) tensor-vector product (arXiv 2405.19246).
+//
+// The paper splits the index set into the l! order regions D_p,
+// makes the exponent linear inside each region and evaluates every region by
+// nested prefix/suffix sums computed with first-order recurrences ("separated summations
+// and dynamic programming").  On the GPU we use the equivalent
+// edge form of the same exponent:
+//
+//     E(i) = sum_{p<q} |i_p - i_q| = sum_{x=0}^{N-2} a_x (l - a_x),
+//     a_x  = #{ indices at or left of grid point x }.
+//
+// Every grid edge with a indices on its left contributes w_a = lambda^{a(l-a)}, so the l!
+// region chains collapse into one left-to-right recurrence over the 2^{l-1} subsets S of
+// the bound marginals B = {1..l}\{k} ("which bound marginals are already placed"):
+//
+//     F_x[S] = sum_{T subset S} w_{|S\T|} F_{x-1}[S\T] prod_{q in T} phi_q[x]     (prefix)
+//     B_x[R] = sum_{T subset R} w_{|R\T|} B_{x+1}[R\T] prod_{q in T} phi_q[x]     (suffix)
+//     J_k[m] = sum_{S subset B} F_m[S] * w_{|S|+1} * B_{m+1}[B\S]                 (combine)
+//
+// Each state is a first-order constant-decay recurrence s[x] = w s[x-1] + v[x] (north_star)
+// whose input v comes from lower subset levels.  A step is "diag" (multiply by w_{|S|},
+// the edge crossed) followed by "place" (in-place rank-1 updates, one per bound marginal,
+// which also realises ties i_p = i_q).
+//
+// Chunk operators.  The state after a chunk is linear in the state before it.  Because
+// the edge weight only depends on the COUNT of indices already placed, the operator has
+// the form  Op(F)[S] = sum_{U subset S} F[U] * G_{|U|}[S\U],  where G_c is the chunk DP
+// started from the empty set with weights shifted by c (w_{c+|V|}).  Only entries with
+// |V| <= NB - c are ever used.  Operators compose in the same form, which gives the
+// parallel (hierarchical) scan over chunks.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mmot {
+
+constexpr int kMaxL = 6;
+
+__host__ __device__ constexpr int pc(int x) { return x ? (x & 1) + pc(x >> 1) : 0; }
+
+// ---------------------------------------------------------------------------------------
+// Scalar types: plain double, and a dual number (value, d/dlog(lambda)) for the cost.
+// With w_a = lambda^{e_a}, dw_a/dlog(lambda) = e_a w_a, so carrying duals through the
+// same scans yields hatJ = sum_i E(i) lambda^{E(i)} prod phi.
+// ---------------------------------------------------------------------------------------
+struct Dual {
+    double v, d;
+};
+
+__device__ __forceinline__ double zero_of(double) { return 0.0; }
+__device__ __forceinline__ Dual zero_of(Dual) { return Dual{0.0, 0.0}; }
+__device__ __forceinline__ double one_of(double) { return 1.0; }
+__device__ __forceinline__ Dual one_of(Dual) { return Dual{1.0, 0.0}; }
+
+// a * b
+__device__ __forceinline__ double mul(double a, double b) { return a * b; }
+__device__ __forceinline__ Dual mul(Dual a, Dual b) { return Dual{a.v * b.v, fma(a.d, b.v, a.v * b.d)}; }
+// acc + a * b
+__device__ __forceinline__ double mad(double a, double b, double acc) { return fma(a, b, acc); }
+__device__ __forceinline__ Dual mad(Dual a, Dual b, Dual acc) {
+    return Dual{fma(a.v, b.v, acc.v), fma(a.d, b.v, fma(a.v, b.d, acc.d))};
+}
+// acc + f * b  with a plain scalar f (scaling vector entry)
+__device__ __forceinline__ double mads(double f, double b, double acc) { return fma(f, b, acc); }
+__device__ __forceinline__ Dual mads(double f, Dual b, Dual acc) { return Dual{fma(f, b.v, acc.v), fma(f, b.d, acc.d)}; }
+
+__device__ __forceinline__ double value_of(double a) { return a; }
+__device__ __forceinline__ double value_of(Dual a) { return a.v; }
+
+// Edge weight w_a as scalar type T (dual part e_a w_a).
+struct Weights {
+    double w[kMaxL + 1];  // w_a = exp(-a(l-a) h / eta), a = 0..l
+    double e[kMaxL + 1];  // e_a = a(l-a)
+};
+__device__ __forceinline__ void load_weight(double &o, const Weights &W, int a) { o = W.w[a]; }
+__device__ __forceinline__ void load_weight(Dual &o, const Weights &W, int a) { o = Dual{W.w[a], W.e[a] * W.w[a]}; }
+
+// ---------------------------------------------------------------------------------------
+// One grid point of the recurrence.  `wc[a]` = w_{c+a}; states S with popcount > LIMIT are
+// not needed (operators) and are skipped at compile time.
+// ---------------------------------------------------------------------------------------
+template <int NB, typename T>
+__device__ __forceinline__ void dp_diag(T (&st)[1 << NB], const T *wc, int limit = NB) {
+#pragma unroll
+    for (int S = 0; S < (1 << NB); ++S)
+        if (pc(S) <= limit) st[S] = mul(wc[pc(S)], st[S]);
+}
+
+template <int NB, typename T>
+__device__ __forceinline__ void dp_place(T (&st)[1 << NB], const double (&f)[NB > 0 ? NB : 1], int limit = NB) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+#pragma unroll
+        for (int S = (1 << NB) - 1; S >= 0; --S)
+            if ((S >> b) & 1)
+                if (pc(S) <= limit) st[S] = mads(f[b], st[S ^ (1 << b)], st[S]);
+    }
+}
+
+// Operator storage: G[c][S], c = 0..NB, S = 0..2^NB-1 (entries with pc(S) > NB-c unused).
+template <int NB>
+struct OpShape {
+    static constexpr int M = 1 << NB;
+    static constexpr int SZ = (NB + 1) * M;
+};
+
+template <int NB, typename T>
+__device__ __forceinline__ void op_identity(T (&G)[NB + 1][1 << NB]) {
+#pragma unroll
+    for (int c = 0; c <= NB; ++c)
+#pragma unroll
+        for (int S = 0; S < (1 << NB); ++S) G[c][S] = (S == 0) ? one_of(T{}) : zero_of(T{});
+}
+
+// Advance all shifted DPs G_c by one grid point (weights wt[a] = w_a, a = 0..NB+1).
+template <int NB, typename T>
+__device__ __forceinline__ void op_step(T (&G)[NB + 1][1 << NB], const T *wt, const double (&f)[NB > 0 ? NB : 1]) {
+#pragma unroll
+    for (int c = 0; c <= NB; ++c) {
+        dp_diag<NB, T>(G[c], wt + c, NB - c);
+        dp_place<NB, T>(G[c], f, NB - c);
+    }
+}
+
+// out = Op(in):  out[S] = sum_{U subset S} in[U] * G[|U|][S\U]
+template <int NB, typename T>
+__device__ __forceinline__ void op_apply(const T (&G)[NB + 1][1 << NB], const T (&in)[1 << NB], T (&out)[1 << NB]) {
+#pragma unroll
+    for (int S = 0; S < (1 << NB); ++S) {
+        T acc = zero_of(T{});
+#pragma unroll
+        for (int U = 0; U < (1 << NB); ++U)
+            if ((U & S) == U) acc = mad(in[U], G[pc(U)][S ^ U], acc);
+        out[S] = acc;
+    }
+}
+
+// C = B o A (A applied first):  C_c[V] = sum_{U subset V} A_c[U] * B_{c+|U|}[V\U]
+template <int NB, typename T>
+__device__ __forceinline__ void op_compose(const T (&A)[NB + 1][1 << NB], const T (&B)[NB + 1][1 << NB],
+                                           T (&C)[NB + 1][1 << NB]) {
+#pragma unroll
+    for (int c = 0; c <= NB; ++c) {
+#pragma unroll
+        for (int V = 0; V < (1 << NB); ++V) {
+            if (pc(V) > NB - c) { C[c][V] = zero_of(T{}); continue; }
+            T acc = zero_of(T{});
+#pragma unroll
+            for (int U = 0; U < (1 << NB); ++U)
+                if ((U & V) == U) acc = mad(A[c][U], B[c + pc(U)][V ^ U], acc);
+            C[c][V] = acc;
+        }
+    }
+}
+
+template <int NB, typename T>
+__device__ __forceinline__ void op_load(T (&G)[NB + 1][1 << NB], const T *p) {
+#pragma unroll
+    for (int c = 0; c <= NB; ++c)
+#pragma unroll
+        for (int S = 0; S < (1 << NB); ++S)
+            if (pc(S) <= NB - c) G[c][S] = p[c * (1 << NB) + S];
+            else G[c][S] = zero_of(T{});
+}
+
+template <int NB, typename T>
+__device__ __forceinline__ void op_store(const T (&G)[NB + 1][1 << NB], T *p) {
+#pragma unroll
+    for (int c = 0; c <= NB; ++c)
+#pragma unroll
+        for (int S = 0; S < (1 << NB); ++S)
+            if (pc(S) <= NB - c) p[c * (1 << NB) + S] = G[c][S];
+}
+
+template <int NB, typename T>
+__device__ __forceinline__ void vec_load(T (&v)[1 << NB], const T *p) {
+#pragma unroll
+    for (int S = 0; S < (1 << NB); ++S) v[S] = p[S];
+}
+template <int NB, typename T>
+__device__ __forceinline__ void vec_store(const T (&v)[1 << NB], T *p) {
+#pragma unroll
+    for (int S = 0; S < (1 << NB); ++S) p[S] = v[S];
+}
+template <int NB, typename T>
+__device__ __forceinline__ void vec_unit(T (&v)[1 << NB]) {
+#pragma unroll
+    for (int S = 0; S < (1 << NB); ++S) v[S] = (S == 0) ? one_of(T{}) : zero_of(T{});
+}
+
+}  // namespace mmot

@@ -1,0 +1,70 @@
+// internal.h -- host-side plan of one tensor-vector product and the kernel launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dp.cuh"
+
+namespace mmot {
+
+enum Mode : int {
+    MODE_MARG = 0,  // out = phi_k * J_k                         (mmot_marginal)
+    MODE_UPD = 1,   // phi_k = mu_k / J_k                        (Sinkhorn update)
+    MODE_RES = 2,   // partial[c] = sum |phi_k J_k - mu_k|       (residual)
+    MODE_COST = 3,  // partial[c] = sum phi_k * hatJ_k (duals)   (W)
+};
+
+constexpr int kGroup = 32;      // operators composed per thread in the hierarchical scan
+constexpr int kMaxLevels = 8;
+
+// Sub-block length Q (registers hold Q suffix states) and max sub-blocks per chunk
+// (local-memory checkpoints) for NB = l-1 bound marginals.
+__host__ __device__ constexpr int sub_q(int NB) { return NB <= 2 ? 8 : (NB == 3 ? 4 : (NB == 4 ? 2 : 1)); }
+__host__ __device__ constexpr int nsub_max(int NB) { return 256 >> NB; }
+__host__ __device__ constexpr int chunk_max(int NB) { return sub_q(NB) * nsub_max(NB); }
+
+struct Plan {
+    int NB;                          // l - 1
+    int64_t N, P, nchunks;
+    const double *bound[kMaxL];      // the NB bound scaling vectors, increasing marginal index
+    const double *phik;              // phi_k (marg / res / cost)
+    const double *muk;               // mu_k (upd / res)
+    double *outk;                    // out (marg) or phi_k (upd); may alias phik for upd
+    Weights W;
+    int nlev;
+    int64_t nlev_n[kMaxLevels];      // entries per level (level 0 = chunks)
+    void *ops_f[kMaxLevels], *ops_b[kMaxLevels];
+    void *car_f[kMaxLevels], *car_b[kMaxLevels];
+    double *partial;                 // nchunks partial sums
+    int *stop;                       // device flag: nonzero -> every kernel returns at once
+    int *status;                     // device status (mmot_status) of the run
+    int *fail_iter;                  // device: sweep index of the first failure
+    int iter;                        // current sweep index (for fail_iter)
+};
+
+// Enqueue one product (ops -> scan -> apply) of `mode` on `s`.  Returns the number of
+// kernels launched through *launches (accumulated).
+cudaError_t launch_product(const Plan &p, int mode, cudaStream_t s, int64_t *launches,
+                           cudaEvent_t *ev = nullptr /* 4 events: before ops, after ops, after scan, after apply */);
+
+// Deterministic single-block sum of partial[0..n) -> *out = scale * sum (+ *out if accumulate).
+cudaError_t launch_sum(const double *partial, int64_t n, double *out, double scale, int accumulate,
+                       const int *stop, cudaStream_t s, int64_t *launches);
+
+// Elementwise helpers.
+cudaError_t launch_exp(const double *in, double *out, int64_t n, cudaStream_t s, int64_t *launches);
+cudaError_t launch_log(const double *in, double *out, int64_t n, cudaStream_t s, int64_t *launches);
+cudaError_t launch_fill(double *out, double v, int64_t n, cudaStream_t s, int64_t *launches);
+// Validate marginals / scalings.  flags: bit0 non-finite, bit1 negative; mass[q] += sum.
+cudaError_t launch_check(const double *v, int64_t n, int allow_neg_inf, int *flags, double *mass,
+                         cudaStream_t s, int64_t *launches);
+// After checks: turn flags/mass into a status and stop flag.
+cudaError_t launch_check_finish(const int *flags, const double *mass, int nvec, int nmarg, int *status,
+                                int *stop, int *fail_iter, cudaStream_t s, int64_t *launches);
+// End of a residual evaluation: res = *acc; if res <= tol stop (converged).
+cudaError_t launch_resid_finish(double *acc, double tol, int iter, double *res_out, int *iters_done,
+                                int *converged, int *stop, cudaStream_t s, int64_t *launches);
+// End of a sweep without residual: iters_done = iter unless stopped.
+cudaError_t launch_sweep_done(int iter, int *iters_done, const int *stop, cudaStream_t s, int64_t *launches);
+
+}  // namespace mmot

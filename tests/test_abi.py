@@ -1,0 +1,59 @@
+"""CPU checks of the C ABI: the library builds for sm_100a, loads without a GPU, and exports
+every entry point declared in include/mmot.h (no compute calls)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2405_19246_b200 as mm
+from paper_2405_19246_b200 import _build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "mmot.h")).read()
+    return sorted(set(re.findall(r"MMOT_API\s+[\w\s\*]+?\b(mmot_\w+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return mm.load_library()
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    for n in ("mmot_create", "mmot_marginal", "mmot_sinkhorn", "mmot_cost", "mmot_destroy",
+              "mmot_strerror", "mmot_init_uniform", "mmot_sinkhorn_host", "mmot_last_error"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    exported = set(mm.exported_symbols())
+    missing = [n for n in _declared() if n not in exported]
+    assert not missing, missing
+    # no internal symbols leak (visibility hidden)
+    assert all(s.startswith("mmot_") for s in exported)
+
+
+def test_host_only_calls(lib):
+    assert lib.mmot_version() == (0 << 16) | 1
+    assert lib.mmot_strerror(0) == b"ok"
+    assert b"overflow" in lib.mmot_strerror(6) or b"range" in lib.mmot_strerror(6)
+
+
+def test_argument_errors_before_any_launch(lib):
+    """mmot_create validates on the host (EINVAL / EUNSUPPORTED) without touching the device."""
+    ctx = ctypes.c_void_p()
+    g = mm._Grid(0.0, 1.0)
+    assert lib.mmot_create(1, 10, 0.1, g, 0, None, None, ctypes.byref(ctx)) == 1       # l < 2
+    assert lib.mmot_create(3, 0, 0.1, g, 0, None, None, ctypes.byref(ctx)) == 1        # N < 1
+    assert lib.mmot_create(3, 10, -1.0, g, 0, None, None, ctypes.byref(ctx)) == 1      # eta <= 0
+    assert lib.mmot_create(3, 10, float("nan"), g, 0, None, None, ctypes.byref(ctx)) == 1
+    assert lib.mmot_create(3, 10, 0.1, mm._Grid(1.0, 0.0), 0, None, None, ctypes.byref(ctx)) == 1
+    assert lib.mmot_create(7, 10, 0.1, g, 0, None, None, ctypes.byref(ctx)) == 10      # l > MMOT_MAX_L
+    assert ctx.value is None
+    assert lib.mmot_marginal(None, 0, None, None) == 1
+    assert lib.mmot_sinkhorn(None, None, 1, 0.0, None, None) == 1
