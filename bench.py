@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""bench.py -- B200 benchmark of the fast tensor-vector product inside multi-marginal Sinkhorn.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl mmot|reference]
+
+A *step* is one pass of the whole hot path over the config's synthetic batch: the paper's
+initialisation, ``mmot_sinkhorn`` for the config's T sweeps of l fused updates
+(residual + tolerance when the config has one) and ``mmot_cost``
+(P:1037-1040).  Metric (BASELINE.json): fast marginal evaluations, reported as l*N elements
+per second (one eval = one J_k, T*l evals per step), plus Sinkhorn iters/s and the HBM
+roofline fraction of the update.
+
+Prints ONE JSON line on rank 0.  See DESIGN.md §5 for every field's definition.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import mmot_inputs  # noqa: E402
+
+METRIC = "fast marginal evals throughput (l*N elements/s)"
+UNIT = "elem/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--impl", default="mmot", choices=["mmot", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _workload(cfg):
+    return (f"{cfg.name}: l={cfg.l} N={cfg.N} eta={cfg.eta} {cfg.dtype} T={cfg.iters}"
+            + (f" tol={cfg.tol}" if cfg.tol > 0 else ""))
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(dev_index)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for ln in open(self.f.name):
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------------------
+def oracle_update_rate(cfg, mus, n_sample: int):
+    """The CPU oracle as it stands (oracle/regions.c, single thread): one Sinkhorn update
+    phi_0 <- mu_0 / J_0 on the first n_sample grid points of the config's marginals."""
+    from oracle import regions
+    l = cfg.l
+    N = n_sample
+    h = mmot_inputs.grid_h(cfg.N)  # keep the config's grid spacing (lambda)
+    w = regions.edge_weights(l, h, cfg.eta)
+    phis = [np.full(N, 1.0 / cfg.N) for _ in range(l)]
+    t0 = time.perf_counter()
+    J = regions.marginal_product(phis, 0, w)
+    phi0 = mus[0][:N] / J
+    dt = time.perf_counter() - t0
+    assert np.all(np.isfinite(phi0))
+    return l * N / dt, dt
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    n_sample = min(cfg.N, 10_000_000)
+    mus = mmot_inputs.make_marginals(cfg.name, 0, None if cfg.N <= 2_000_000 else n_sample)
+    rates = []
+    for i in range(args.warmup + args.steps):
+        r, dt = oracle_update_rate(cfg, mus, n_sample)
+        if i >= args.warmup:
+            rates.append((r, dt))
+    value = statistics.median(r for r, _ in rates)
+    ms = statistics.median(dt for _, dt in rates) * 1e3
+    sample = (f"one Sinkhorn update (J_0 by the oracle's region chains + division) on the first {n_sample} "
+              f"grid points of {cfg.name}'s marginals, config lambda")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": _workload(cfg), "parallelism": "oracle, 1 host thread"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def run_mmot(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_19246_b200 as mm
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    l, N, T, tol = cfg.l, cfg.N, cfg.iters, cfg.tol
+
+    mus_h = mmot_inputs.make_marginals(cfg.name, rank if ws > 1 else 0)  # fp64 host, seeded
+    mus_d = [torch.from_numpy(m).to(dev) for m in mus_h]
+    ctx = mm.Context(l, N, cfg.eta, repr="log", check_every=1 if tol > 0 else 0)
+    u = [torch.empty(N, dtype=torch.float64, device=dev) for _ in range(l)]
+    state = {}
+
+    def step():
+        ctx.init_uniform(u)
+        rep = ctx.sinkhorn(mus_d, T, tol, u)
+        state["rep"] = rep
+        state["W"] = ctx.cost(u)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = ctx.stream
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    ctx.profile(True)
+    ctx.profile_read()
+    launches0 = ctx.launches
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    launches = (ctx.launches - launches0) // args.steps
+    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    iters_done = state["rep"]["iters_done"]
+    evals = iters_done * l
+    value = ws * evals * l * N / (ms / 1e3)
+
+    # roofline of the dominant kernel group: the fused Sinkhorn update (one product of mode
+    # "update" = operator pass + scan + apply).  Algorithmic bytes per update = (l+1) N 8.
+    n_upd = prof["mode_n"]["update"]
+    upd_ms = prof["mode_ms"]["update"] / max(n_upd, 1)
+    alg_bytes = (l + 1) * N * 8
+    peak, peak_src = _peaks()
+    achieved = alg_bytes / (upd_ms / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(cfg.name)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "fused update (ops + scan + apply of one J_k)",
+                "alg_bytes_per_launch": alg_bytes, "ms_per_launch": upd_ms, "peak_source": peak_src,
+                "phase_ms_per_update": {k: v / max(sum(prof["mode_n"].values()), 1) for k, v in prof["phase_ms"].items()}}
+
+    # end-to-end through the C ABI with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        mh = [torch.from_numpy(m).pin_memory() for m in mus_h]
+        uh = [torch.empty(N, dtype=torch.float64).pin_memory() for _ in range(l)]
+        for x in uh:
+            x.fill_(-math.log(N))
+        ctx.sinkhorn_host(mh, T, tol, uh)  # warm (allocates staging once)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for x in uh:
+                x.fill_(-math.log(N))
+            ctx.sinkhorn_host(mh, T, tol, uh)
+        torch.cuda.synchronize()
+        barrier()
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = float(te.item())
+        e2e = {"value": ws * evals * l * N / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": 2 * l * N * 8, "d2h_bytes_per_step": l * N * 8}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        n_sample = min(N, 100_000_000)
+        r, dt = oracle_update_rate(cfg, mus_h, n_sample)
+        cpu = {"value": r, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"one update (region-chain J_0 + division) over {n_sample} grid points of {cfg.name}, "
+                         f"{dt:.1f} s single-thread of {os.cpu_count()} host cores"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": _workload(cfg), "l": l, "N": N, "eta": cfg.eta, "iters": T, "tol": tol,
+                       "global_batch": ws, "parallelism": "replicas" if ws > 1 else "single",
+                       "l2": "inputs (l*N*8*2 B) exceed the 126 MB L2; no flush needed" if N >= 5_000_000 else
+                             "working set L2-resident (latency-bound config)"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk,
+            "gpu_launches": int(launches),
+            "iters_per_s": ws * iters_done / (ms / 1e3),
+            "iters_done": iters_done,
+            "W": state["W"],
+            "impl": "mmot",
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    cfg = mmot_inputs.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_mmot(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -36,7 +36,14 @@ namespace mmot {
 
 constexpr int kMaxL = 6;
 
-__host__ __device__ constexpr int pc(int x) { return x ? (x & 1) + pc(x >> 1) : 0; }
+// popcount; non-recursive and force-inlined so that it folds to a constant inside the
+// fully unrolled subset loops (a recursive constexpr is emitted as a real CALL otherwise).
+__host__ __device__ __forceinline__ constexpr int pc(int x) {
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c += (x >> i) & 1;
+    return c;
+}
 
 // ---------------------------------------------------------------------------------------
 // Scalar types: plain double, and a dual number (value, d/dlog(lambda)) for the cost.

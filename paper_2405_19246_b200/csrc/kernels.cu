@@ -35,31 +35,127 @@ __device__ __forceinline__ void load_f(double (&f)[NB > 0 ? NB : 1], const Plan 
 }
 
 // ---------------------------------------------------------------------------------------
-// Phase 1: chunk operators.
+// Warp-cooperative slab staging.  A warp owns 32 consecutive chains (chunks of P points,
+// lane r <-> chain r).  The chains' data are moved through shared memory in slabs of S
+// points per chain: each warp-wide cp.async instruction copies 32/S chains' contiguous
+// S-point segments (full 32-byte sectors), lanes then read their own chain's values from
+// the [32][S+1] tile (odd row pitch: conflict-free 8-byte reads).  Two buffers: the next
+// slab is in flight while the current one is consumed.
 // ---------------------------------------------------------------------------------------
+__host__ __device__ constexpr int slab_s(int NB) { return NB <= 2 ? 16 : 8; }
+
+__device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool valid) {
+    const unsigned saddr = (unsigned)__cvta_generic_to_shared(sdst);
+    const int sz = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
+
+// Issue the copies of slab s of NV vectors into buf[NV][32][S+1].
+template <int S, int NV>
+__device__ __forceinline__ void slab_issue(double *buf, const double *const *vec, int64_t chain0, int64_t P,
+                                           int64_t N, int s, int lane) {
+#pragma unroll
+    for (int it = 0; it < S; ++it) {
+        const int e = it * 32 + lane;
+        const int r = e / S, j = e % S;
+        const int64_t off = (int64_t)s * S + j;
+        const int64_t x = (chain0 + r) * P + off;
+        const bool valid = off < P && x < N;
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+            cp_async8(buf + (v * 32 + r) * (S + 1) + j, vec[v] + (valid ? x : 0), valid);
+    }
+}
+
+// Store an output slab obuf[32][S+1] to global (coalesced, like slab_issue).
+template <int S>
+__device__ __forceinline__ void slab_store(const double *obuf, double *out, int64_t chain0, int64_t P, int64_t N,
+                                           int s, int lane) {
+#pragma unroll
+    for (int it = 0; it < S; ++it) {
+        const int e = it * 32 + lane;
+        const int r = e / S, j = e % S;
+        const int64_t off = (int64_t)s * S + j;
+        const int64_t x = (chain0 + r) * P + off;
+        if (off < P && x < N) out[x] = obuf[r * (S + 1) + j];
+    }
+}
+
+template <int NB, int S>
+__device__ __forceinline__ void slab_f(double (&f)[NB > 0 ? NB : 1], const double *buf, int lane, int j) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) f[b] = buf[(b * 32 + lane) * (S + 1) + j];
+}
+
+// ---------------------------------------------------------------------------------------
+// Phase 1: chain operators (prefix walk and suffix walk of every chain).
+// ---------------------------------------------------------------------------------------
+constexpr int kWarpsPerCta = 4;
+
 template <int NB, typename T>
-__global__ void __launch_bounds__(128) k_chunk_ops(Plan p) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_ops(Plan p) {
     constexpr int M = 1 << NB;
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= p.nchunks || *p.stop) return;
+    constexpr int S = slab_s(NB);
+    constexpr int TILE = 32 * (S + 1);
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t chain0 = ((int64_t)blockIdx.x * kWarpsPerCta + warp) * 32;
+    if (chain0 >= p.nchunks || *p.stop) return;
+    double *buf = smem + (size_t)warp * 2 * NB * TILE;
+    const int64_t c = chain0 + lane;
     const int64_t x0 = c * p.P;
     const int64_t x1 = min(p.N, x0 + p.P);
+    const int ns = (int)((p.P + S - 1) / S);
     T wt[NB + 2];
     load_weights<NB, T>(wt, p.W);
     T G[NB + 1][M];
     double f[NB > 0 ? NB : 1];
+    // prefix walk
     op_identity<NB, T>(G);
-    for (int64_t x = x0; x < x1; ++x) {
-        load_f<NB>(f, p, x);
-        op_step<NB, T>(G, wt, f);
+    slab_issue<S, NB>(buf, p.bound, chain0, p.P, p.N, 0, lane);
+    cp_async_commit();
+    for (int s = 0; s < ns; ++s) {
+        if (s + 1 < ns) slab_issue<S, NB>(buf + ((s + 1) & 1) * NB * TILE, p.bound, chain0, p.P, p.N, s + 1, lane);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        const double *cur = buf + (s & 1) * NB * TILE;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            const int64_t x = x0 + (int64_t)s * S + j;
+            if (x < x1) {
+                slab_f<NB, S>(f, cur, lane, j);
+                op_step<NB, T>(G, wt, f);
+            }
+        }
+        __syncwarp();
     }
-    op_store<NB, T>(G, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ);
+    if (c < p.nchunks) op_store<NB, T>(G, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ);
+    // suffix walk
     op_identity<NB, T>(G);
-    for (int64_t x = x1 - 1; x >= x0; --x) {
-        load_f<NB>(f, p, x);
-        op_step<NB, T>(G, wt, f);
+    slab_issue<S, NB>(buf, p.bound, chain0, p.P, p.N, ns - 1, lane);
+    cp_async_commit();
+    for (int t = 0; t < ns; ++t) {
+        const int s = ns - 1 - t;
+        if (s > 0) slab_issue<S, NB>(buf + ((t + 1) & 1) * NB * TILE, p.bound, chain0, p.P, p.N, s - 1, lane);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        const double *cur = buf + (t & 1) * NB * TILE;
+#pragma unroll
+        for (int jj = S - 1; jj >= 0; --jj) {
+            const int64_t x = x0 + (int64_t)s * S + jj;
+            if (x < x1) {
+                slab_f<NB, S>(f, cur, lane, jj);
+                op_step<NB, T>(G, wt, f);
+            }
+        }
+        __syncwarp();
     }
-    op_store<NB, T>(G, static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+    if (c < p.nchunks) op_store<NB, T>(G, static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -141,6 +237,113 @@ __global__ void __launch_bounds__(64) k_ops_down(const T *ops_f, const T *ops_b,
     }
 }
 
+// Warp-cooperative variants of phase 2 (fp64, NB <= 3): one warp per group of 32 operators;
+// the group is staged through shared memory (coalesced), then composed with a shuffle tree
+// (reduce) or a Kogge-Stone scan (down).  blockIdx.y selects the direction.
+template <int NB>
+__device__ __forceinline__ void op_shfl(double (&dst)[NB + 1][1 << NB], const double (&src)[NB + 1][1 << NB],
+                                        int delta, int mode /*0 idx, 1 up, 2 down*/) {
+#pragma unroll
+    for (int c = 0; c <= NB; ++c)
+#pragma unroll
+        for (int S = 0; S < (1 << NB); ++S) {
+            if (pc(S) > NB - c) { dst[c][S] = 0.0; continue; }
+            dst[c][S] = mode == 1 ? __shfl_up_sync(0xffffffffu, src[c][S], delta)
+                                  : (mode == 2 ? __shfl_down_sync(0xffffffffu, src[c][S], delta)
+                                               : __shfl_sync(0xffffffffu, src[c][S], delta));
+        }
+}
+
+template <int NB>
+__device__ __forceinline__ void op_stage_load(double (&G)[NB + 1][1 << NB], double *sm, const double *src, int64_t first,
+                                              int64_t n_in, int lane) {
+    constexpr int SZ = OpShape<NB>::SZ;
+    const int64_t avail = min((int64_t)32, n_in - first);
+    for (int e = lane; e < 32 * SZ; e += 32) {
+        const int r = e / SZ, q = e % SZ;
+        sm[r * (SZ + 1) + q] = r < avail ? src[first * SZ + e] : (q == 0 || q % (1 << NB) == 0 ? 1.0 : 0.0);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c <= NB; ++c)
+#pragma unroll
+        for (int S = 0; S < (1 << NB); ++S)
+            G[c][S] = pc(S) <= NB - c ? sm[lane * (SZ + 1) + c * (1 << NB) + S] : 0.0;
+    __syncwarp();
+}
+
+template <int NB>
+__global__ void __launch_bounds__(128) k_ops_reduce_w(const double *in_f, const double *in_b, double *out_f,
+                                                     double *out_b, int64_t n_in, const int *stop) {
+    constexpr int M = 1 << NB;
+    constexpr int SZ = OpShape<NB>::SZ;
+    __shared__ double smem[4][32 * (SZ + 1)];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t g = (int64_t)blockIdx.x * 4 + warp;
+    const int dir = blockIdx.y;
+    const int64_t first = g * kGroup;
+    if (first >= n_in || *stop) return;
+    double A[NB + 1][M], B[NB + 1][M], C[NB + 1][M];
+    op_stage_load<NB>(A, smem[warp], dir == 0 ? in_f : in_b, first, n_in, lane);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        op_shfl<NB>(B, A, d, 2);
+        if (dir == 0) op_compose<NB, double>(A, B, C);
+        else op_compose<NB, double>(B, A, C);
+        if ((lane & (2 * d - 1)) == 0) {
+#pragma unroll
+            for (int cc = 0; cc <= NB; ++cc)
+#pragma unroll
+                for (int S = 0; S < M; ++S) A[cc][S] = C[cc][S];
+        }
+    }
+    if (lane == 0) op_store<NB, double>(A, (dir == 0 ? out_f : out_b) + g * SZ);
+}
+
+template <int NB>
+__global__ void __launch_bounds__(128) k_ops_down_w(const double *ops_f, const double *ops_b, const double *gcar_f,
+                                                   const double *gcar_b, double *car_f, double *car_b, int64_t n_in,
+                                                   const int *stop) {
+    constexpr int M = 1 << NB;
+    constexpr int SZ = OpShape<NB>::SZ;
+    __shared__ double smem[4][32 * (SZ + 1)];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t g = (int64_t)blockIdx.x * 4 + warp;
+    const int dir = blockIdx.y;
+    const int64_t first = g * kGroup;
+    if (first >= n_in || *stop) return;
+    double A[NB + 1][M], B[NB + 1][M], C[NB + 1][M];
+    op_stage_load<NB>(A, smem[warp], dir == 0 ? ops_f : ops_b, first, n_in, lane);
+    // inclusive Kogge-Stone scan of the member operators in application order
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        op_shfl<NB>(B, A, d, dir == 0 ? 1 : 2);
+        op_compose<NB, double>(B, A, C);  // the earlier-applied prefix B first, then A
+        const bool take = dir == 0 ? lane >= d : lane + d < 32;
+        if (take) {
+#pragma unroll
+            for (int cc = 0; cc <= NB; ++cc)
+#pragma unroll
+                for (int S = 0; S < M; ++S) A[cc][S] = C[cc][S];
+        }
+    }
+    const double *gc = dir == 0 ? gcar_f : gcar_b;
+    double cin[M], out[M], nb[M];
+    if (gc) vec_load<NB, double>(cin, gc + g * M);
+    else vec_unit<NB, double>(cin);
+    op_apply<NB, double>(A, cin, out);
+#pragma unroll
+    for (int S = 0; S < M; ++S)
+        nb[S] = dir == 0 ? __shfl_up_sync(0xffffffffu, out[S], 1) : __shfl_down_sync(0xffffffffu, out[S], 1);
+    const bool edge = dir == 0 ? lane == 0 : lane == 31;
+    const int64_t i = first + lane;
+    if (i < n_in) {
+        double *dst = (dir == 0 ? car_f : car_b) + i * M;
+#pragma unroll
+        for (int S = 0; S < M; ++S) dst[S] = edge ? cin[S] : nb[S];
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // Phase 3: apply.
 // ---------------------------------------------------------------------------------------
@@ -149,104 +352,207 @@ __device__ __forceinline__ void raise_status(const Plan &p, int st) {
     *(volatile int *)p.stop = 1;
 }
 
+// Vectors staged by the apply phase: the NB bound vectors, then mu_k (update / residual),
+// then phi_k (marginal / residual / cost).
+template <int NB, int MODE>
+struct ApplyVecs {
+    static constexpr bool kMu = MODE == MODE_UPD || MODE == MODE_RES;
+    static constexpr bool kPhi = MODE == MODE_MARG || MODE == MODE_RES || MODE == MODE_COST;
+    static constexpr int NV = NB + (kMu ? 1 : 0) + (kPhi ? 1 : 0);
+    static constexpr int IMU = NB;
+    static constexpr int IPHI = NB + (kMu ? 1 : 0);
+    static constexpr bool kOut = MODE == MODE_MARG || MODE == MODE_UPD;
+};
+
 template <int NB, typename T, int MODE>
-__global__ void __launch_bounds__(128) k_chunk_apply(Plan p) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p) {
+    using AV = ApplyVecs<NB, MODE>;
     constexpr int M = 1 << NB;
     constexpr int Q = sub_q(NB);
     constexpr int NSUB = nsub_max(NB);
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= p.nchunks || *p.stop) return;
+    constexpr int S = slab_s(NB);
+    constexpr int TILE = 32 * (S + 1);
+    constexpr int NV = AV::NV;
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t chain0 = ((int64_t)blockIdx.x * kWarpsPerCta + warp) * 32;
+    if (chain0 >= p.nchunks || *p.stop) return;
+    double *buf = smem + (size_t)warp * (2 * NV + 1) * TILE;
+    double *obuf = buf + 2 * NV * TILE;
+    const int64_t c = chain0 + lane;
+    const bool live = c < p.nchunks;
     const int64_t x0 = c * p.P;
     const int64_t x1 = min(p.N, x0 + p.P);
-    const int nsub = (int)((x1 - x0 + Q - 1) / Q);
+    const int ns = (int)((p.P + S - 1) / S);
+    const double *vecs[NV];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) vecs[b] = p.bound[b];
+    if (AV::kMu) vecs[AV::IMU] = p.muk;
+    if (AV::kPhi) vecs[AV::IPHI] = p.phik;
     T wt[NB + 2];
     load_weights<NB, T>(wt, p.W);
     T F[M], st[M];
-    vec_load<NB, T>(F, static_cast<const T *>(p.car_f[0]) + c * M);
-    vec_load<NB, T>(st, static_cast<const T *>(p.car_b[0]) + c * M);
-    double f[NB > 0 ? NB : 1];
-    // suffix walk with checkpoints: ck[j] = B at the right boundary of sub-block j
-    T ck[NSUB][M];
-    {
-        int j = nsub - 1;
-#pragma unroll
-        for (int S = 0; S < M; ++S) ck[j][S] = st[S];
-        for (int64_t x = x1 - 1; x > x0; --x) {
-            load_f<NB>(f, p, x);
-            dp_diag<NB, T>(st, wt);
-            dp_place<NB, T>(st, f);
-            if (x == x0 + (int64_t)j * Q) {
-                --j;
-#pragma unroll
-                for (int S = 0; S < M; ++S) ck[j][S] = st[S];
-            }
-        }
+    if (live) {
+        vec_load<NB, T>(F, static_cast<const T *>(p.car_f[0]) + c * M);
+        vec_load<NB, T>(st, static_cast<const T *>(p.car_b[0]) + c * M);
+    } else {
+        vec_unit<NB, T>(F);
+        vec_unit<NB, T>(st);
     }
-    double acc = 0.0;
-    for (int j = 0; j < nsub; ++j) {
-        const int64_t s0 = x0 + (int64_t)j * Q;
-        const int len = (int)min((int64_t)Q, x1 - s0);
-        double fq[Q][NB > 0 ? NB : 1];
-        T H[Q][M];
+    double f[NB > 0 ? NB : 1];
+    // ---- suffix walk with checkpoints: ck[j] = B at min(x0 + (j+1)Q, x1) ----
+    T ck[NSUB][M];
+    if (live && x1 > x0) {
+        const int jl = (int)((x1 - 1 - x0) / Q);
 #pragma unroll
-        for (int i = 0; i < Q; ++i)
-            if (i < len) load_f<NB>(fq[i], p, s0 + i);
+        for (int S2 = 0; S2 < M; ++S2) ck[jl][S2] = st[S2];
+    }
+    slab_issue<S, NB>(buf, vecs, chain0, p.P, p.N, ns - 1, lane);
+    cp_async_commit();
+    for (int t = 0; t < ns; ++t) {
+        const int s = ns - 1 - t;
+        if (s > 0) slab_issue<S, NB>(buf + ((t + 1) & 1) * NV * TILE, vecs, chain0, p.P, p.N, s - 1, lane);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        const double *cur = buf + (t & 1) * NV * TILE;
 #pragma unroll
-        for (int S = 0; S < M; ++S) st[S] = ck[j][S];
-        // rebuild H_m = diag(w) B_{m+1} for m = s0+len-1 .. s0
-#pragma unroll
-        for (int i = Q - 1; i >= 0; --i) {
-            if (i < len) {
+        for (int jj = S - 1; jj >= 0; --jj) {
+            const int64_t x = x0 + (int64_t)s * S + jj;
+            if (x < x1 && x > x0) {
+                slab_f<NB, S>(f, cur, lane, jj);
                 dp_diag<NB, T>(st, wt);
+                dp_place<NB, T>(st, f);
+                if ((((int)(x - x0)) % Q) == 0) {
+                    const int j = (int)((x - x0) / Q) - 1;
 #pragma unroll
-                for (int S = 0; S < M; ++S) H[i][S] = st[S];
-                if (i > 0) dp_place<NB, T>(st, fq[i]);
-            }
-        }
-        // prefix walk + combine + epilogue
-#pragma unroll
-        for (int i = 0; i < Q; ++i) {
-            if (i < len) {
-                const int64_t m = s0 + i;
-                dp_diag<NB, T>(F, wt);
-                dp_place<NB, T>(F, fq[i]);
-                T J = zero_of(T{});
-#pragma unroll
-                for (int S = 0; S < M; ++S) J = mad(F[S], H[i][(M - 1) ^ S], J);
-                if (MODE == MODE_MARG) {
-                    p.outk[m] = p.phik[m] * value_of(J);
-                } else if (MODE == MODE_UPD) {
-                    const double mu = p.muk[m];
-                    const double jv = value_of(J);
-                    double phi = 0.0;
-                    if (mu != 0.0) {
-                        phi = mu / jv;
-                        if (!(jv > 0.0) || !isfinite(jv) || !isfinite(phi)) raise_status(p, 6 /*EOVERFLOW*/);
-                    }
-                    p.outk[m] = phi;
-                } else if (MODE == MODE_RES) {
-                    acc += fabs(p.phik[m] * value_of(J) - p.muk[m]);
-                } else {  // MODE_COST
-                    if constexpr (sizeof(T) == sizeof(Dual)) acc += p.phik[m] * reinterpret_cast<const Dual &>(J).d;
+                    for (int S2 = 0; S2 < M; ++S2) ck[j][S2] = st[S2];
                 }
             }
         }
+        __syncwarp();
     }
-    if (MODE == MODE_RES || MODE == MODE_COST) p.partial[c] = acc;
+    // ---- prefix walk: per Q-block rebuild suffix states, combine, epilogue ----
+    double acc = 0.0;
+    slab_issue<S, NV>(buf, vecs, chain0, p.P, p.N, 0, lane);
+    cp_async_commit();
+    for (int s = 0; s < ns; ++s) {
+        if (s + 1 < ns) slab_issue<S, NV>(buf + ((s + 1) & 1) * NV * TILE, vecs, chain0, p.P, p.N, s + 1, lane);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        const double *cur = buf + (s & 1) * NV * TILE;
+#pragma unroll
+        for (int jb = 0; jb < S / Q; ++jb) {
+            const int64_t base = x0 + (int64_t)s * S + jb * Q;
+            const int len = (int)max((int64_t)0, min((int64_t)Q, x1 - base));
+            if (len > 0) {
+                T H[Q][M];
+#pragma unroll
+                for (int S2 = 0; S2 < M; ++S2) st[S2] = ck[(int)((base - x0) / Q)][S2];
+#pragma unroll
+                for (int i = Q - 1; i >= 0; --i) {
+                    if (i < len) {
+                        dp_diag<NB, T>(st, wt);
+#pragma unroll
+                        for (int S2 = 0; S2 < M; ++S2) H[i][S2] = st[S2];
+                        if (i > 0) {
+                            slab_f<NB, S>(f, cur, lane, jb * Q + i);
+                            dp_place<NB, T>(st, f);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < Q; ++i) {
+                    if (i < len) {
+                        const int jx = jb * Q + i;
+                        slab_f<NB, S>(f, cur, lane, jx);
+                        dp_diag<NB, T>(F, wt);
+                        dp_place<NB, T>(F, f);
+                        T J = zero_of(T{});
+#pragma unroll
+                        for (int S2 = 0; S2 < M; ++S2) J = mad(F[S2], H[i][(M - 1) ^ S2], J);
+                        const double jv = value_of(J);
+                        if (MODE == MODE_MARG) {
+                            obuf[lane * (S + 1) + jx] = cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * jv;
+                        } else if (MODE == MODE_UPD) {
+                            const double mu = cur[(AV::IMU * 32 + lane) * (S + 1) + jx];
+                            double phi = 0.0;
+                            if (mu != 0.0) {
+                                phi = mu / jv;
+                                if (!(jv > 0.0) || !isfinite(jv) || !isfinite(phi)) raise_status(p, 6 /*EOVERFLOW*/);
+                            }
+                            obuf[lane * (S + 1) + jx] = phi;
+                        } else if (MODE == MODE_RES) {
+                            acc += fabs(cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * jv -
+                                        cur[(AV::IMU * 32 + lane) * (S + 1) + jx]);
+                        } else {  // MODE_COST
+                            if constexpr (sizeof(T) == sizeof(Dual))
+                                acc += cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * reinterpret_cast<const Dual &>(J).d;
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (AV::kOut) {
+            slab_store<S>(obuf, p.outk, chain0, p.P, p.N, s, lane);
+            __syncwarp();
+        }
+    }
+    if ((MODE == MODE_RES || MODE == MODE_COST) && live) p.partial[c] = acc;
+}
+
+template <int NB, typename T>
+static size_t ops_smem() {
+    return (size_t)kWarpsPerCta * 2 * NB * 32 * (slab_s(NB) + 1) * sizeof(double);
+}
+template <int NB, int MODE>
+static size_t apply_smem() {
+    return (size_t)kWarpsPerCta * (2 * ApplyVecs<NB, MODE>::NV + 1) * 32 * (slab_s(NB) + 1) * sizeof(double);
+}
+
+template <int NB, typename T, int MODE>
+static void launch_apply(const Plan &p, int64_t nb, int tpb, cudaStream_t s) {
+    const size_t sm = apply_smem<NB, MODE>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_chunk_apply<NB, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr = true;
+    }
+    k_chunk_apply<NB, T, MODE><<<(unsigned)nb, tpb, sm, s>>>(p);
 }
 
 // ---------------------------------------------------------------------------------------
 template <int NB, typename T>
 static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *launches, cudaEvent_t *ev) {
-    const int tpb = 128;
+    const int tpb = kWarpsPerCta * 32;
     const int64_t nb = (p.nchunks + tpb - 1) / tpb;
     if (ev) cudaEventRecord(ev[0], s);
-    k_chunk_ops<NB, T><<<(unsigned)nb, tpb, 0, s>>>(p);
+    {
+        const size_t sm = ops_smem<NB, T>();
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_chunk_ops<NB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            attr = true;
+        }
+        k_chunk_ops<NB, T><<<(unsigned)nb, tpb, sm, s>>>(p);
+    }
     if (ev) cudaEventRecord(ev[1], s);
     ++*launches;
+    constexpr bool kWarpScan = NB <= 3 && sizeof(T) == sizeof(double);
     // up-sweep
     for (int i = 0; i + 1 < p.nlev; ++i) {
         const int64_t ng = p.nlev_n[i + 1];
+        if constexpr (kWarpScan) {
+            dim3 grid((unsigned)((ng + 3) / 4), 2);
+            k_ops_reduce_w<NB><<<grid, 128, 0, s>>>(static_cast<const double *>(p.ops_f[i]),
+                                                     static_cast<const double *>(p.ops_b[i]),
+                                                     static_cast<double *>(p.ops_f[i + 1]),
+                                                     static_cast<double *>(p.ops_b[i + 1]), p.nlev_n[i], p.stop);
+            ++*launches;
+            continue;
+        }
         dim3 grid((unsigned)((ng + 63) / 64), 2);
         k_ops_reduce<NB, T><<<grid, 64, 0, s>>>(static_cast<const T *>(p.ops_f[i]), static_cast<const T *>(p.ops_b[i]),
                                                static_cast<T *>(p.ops_f[i + 1]), static_cast<T *>(p.ops_b[i + 1]),
@@ -259,6 +565,17 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
         dim3 grid((unsigned)((ng + 63) / 64), 2);
         const T *gf = i + 1 < p.nlev ? static_cast<const T *>(p.car_f[i + 1]) : nullptr;
         const T *gb = i + 1 < p.nlev ? static_cast<const T *>(p.car_b[i + 1]) : nullptr;
+        if constexpr (kWarpScan) {
+            dim3 gridw((unsigned)((ng + 3) / 4), 2);
+            k_ops_down_w<NB><<<gridw, 128, 0, s>>>(static_cast<const double *>(p.ops_f[i]),
+                                                    static_cast<const double *>(p.ops_b[i]),
+                                                    reinterpret_cast<const double *>(gf),
+                                                    reinterpret_cast<const double *>(gb),
+                                                    static_cast<double *>(p.car_f[i]), static_cast<double *>(p.car_b[i]),
+                                                    p.nlev_n[i], p.stop);
+            ++*launches;
+            continue;
+        }
         k_ops_down<NB, T><<<grid, 64, 0, s>>>(static_cast<const T *>(p.ops_f[i]), static_cast<const T *>(p.ops_b[i]),
                                              gf, gb, static_cast<T *>(p.car_f[i]), static_cast<T *>(p.car_b[i]),
                                              p.nlev_n[i], p.stop);
@@ -266,10 +583,10 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
     }
     if (ev) cudaEventRecord(ev[2], s);
     switch (mode) {
-        case MODE_MARG: k_chunk_apply<NB, T, MODE_MARG><<<(unsigned)nb, tpb, 0, s>>>(p); break;
-        case MODE_UPD: k_chunk_apply<NB, T, MODE_UPD><<<(unsigned)nb, tpb, 0, s>>>(p); break;
-        case MODE_RES: k_chunk_apply<NB, T, MODE_RES><<<(unsigned)nb, tpb, 0, s>>>(p); break;
-        default: k_chunk_apply<NB, T, MODE_COST><<<(unsigned)nb, tpb, 0, s>>>(p); break;
+        case MODE_MARG: launch_apply<NB, T, MODE_MARG>(p, nb, tpb, s); break;
+        case MODE_UPD: launch_apply<NB, T, MODE_UPD>(p, nb, tpb, s); break;
+        case MODE_RES: launch_apply<NB, T, MODE_RES>(p, nb, tpb, s); break;
+        default: launch_apply<NB, T, MODE_COST>(p, nb, tpb, s); break;
     }
     ++*launches;
     if (ev) cudaEventRecord(ev[3], s);
