@@ -297,6 +297,10 @@ static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double
     p.status = &c->dsc->status;
     p.fail_iter = &c->dsc->fail_iter;
     p.iter = iter;
+    // bound set of update k+1 (mod l): for k < l-1 it is this bound set with slot k (marginal
+    // k+1) replaced by marginal k; for k = l-1 it is {1..l-1} = this set shifted by one.
+    p.nxt_slot = k;
+    p.nxt_shift = (k == c->l - 1) ? 1 : 0;
     return p;
 }
 
@@ -350,6 +354,7 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
     }
     const int check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
     bool poll_pending = false;
+    int ops_for = -1;  // bound set whose chain operators are currently in ops level 0
     for (int t = 1; t <= iters; ++t) {
         // asynchronous early exit: the device stop flag is polled without blocking
         if (poll_pending && cudaEventQuery(c->poll_ev) == cudaSuccess) {
@@ -357,13 +362,18 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
             if (*c->hstop) break;
         }
         for (int k = 0; k < l; ++k) {
+            // fused update: scan (+ operators only if not produced by the previous update),
+            // apply phi_k <- mu_k / J_k and build the operators of update k+1 in the same walk
             Plan p = make_plan(c, k, lin, mu[k], lin[k], t);
-            CK(c, mmot::launch_product(p, mmot::MODE_UPD, c->stream, &c->launches, prof_events(c, mmot::MODE_UPD)));
+            CK(c, mmot::launch_product(p, mmot::MODE_UPD, c->stream, &c->launches, prof_events(c, mmot::MODE_UPD),
+                                       ops_for != k, true));
+            ops_for = (k + 1) % l;
         }
         if (tol > 0 && (t % check_every == 0 || t == iters)) {
             for (int k = 0; k + 1 < l; ++k) {
                 Plan p = make_plan(c, k, lin, mu[k], nullptr, t);
                 CK(c, mmot::launch_product(p, mmot::MODE_RES, c->stream, &c->launches, prof_events(c, mmot::MODE_RES)));
+                ops_for = -1;  // the residual products overwrote the chain operators
                 CK(c, mmot::launch_sum(c->partial, c->nchunks, &c->dsc->res_acc, 1.0, k > 0, &c->dsc->stop, c->stream,
                                        &c->launches));
             }

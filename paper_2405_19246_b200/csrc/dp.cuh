@@ -129,6 +129,29 @@ __device__ __forceinline__ void op_step(T (&G)[NB + 1][1 << NB], const T *wt, co
     }
 }
 
+// Right-multiply a suffix operator by one grid point, R <- R o step_x (step_x applied first).
+// A suffix operator maps B_{x1} -> B_{x0} = step_{x0}(step_{x0+1}(... step_{x1-1}(B_{x1}))),
+// so walking the chain LEFT TO RIGHT it grows on the right.  In matrix form
+// R o step_x = R o place_x o diag: place_x = prod_q (I + phi_q E_q) acts on the column index
+// U (G_c[V] += phi_q G_{c+1}[V\q] for q in V), then diag scales column U by w_{|U|}
+// (G_c[V] *= w_c).  Same operation count as the left-multiplied prefix step, which lets one
+// forward walk build both the prefix and the suffix operator of a chain.
+template <int NB, typename T>
+__device__ __forceinline__ void op_rstep(T (&G)[NB + 1][1 << NB], const T *wt, const double (&f)[NB > 0 ? NB : 1]) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+#pragma unroll
+            for (int V = 0; V < (1 << NB); ++V)
+                if (((V >> b) & 1) && pc(V) <= NB - c) G[c][V] = mads(f[b], G[c + 1][V ^ (1 << b)], G[c][V]);
+#pragma unroll
+    for (int c = 0; c <= NB; ++c)
+#pragma unroll
+        for (int V = 0; V < (1 << NB); ++V)
+            if (pc(V) <= NB - c) G[c][V] = mul(wt[c], G[c][V]);
+}
+
 // out = Op(in):  out[S] = sum_{U subset S} in[U] * G[|U|][S\U]
 template <int NB, typename T>
 __device__ __forceinline__ void op_apply(const T (&G)[NB + 1][1 << NB], const T (&in)[1 << NB], T (&out)[1 << NB]) {

@@ -111,10 +111,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_ops(Plan p) {
     const int ns = (int)((p.P + S - 1) / S);
     T wt[NB + 2];
     load_weights<NB, T>(wt, p.W);
-    T G[NB + 1][M];
+    T G[NB + 1][M], R[NB + 1][M];
     double f[NB > 0 ? NB : 1];
-    // prefix walk
+    // one left-to-right walk: prefix operator by left-multiplication, suffix operator by
+    // right-multiplication (op_rstep)
     op_identity<NB, T>(G);
+    op_identity<NB, T>(R);
     slab_issue<S, NB>(buf, p.bound, chain0, p.P, p.N, 0, lane);
     cp_async_commit();
     for (int s = 0; s < ns; ++s) {
@@ -129,33 +131,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_ops(Plan p) {
             if (x < x1) {
                 slab_f<NB, S>(f, cur, lane, j);
                 op_step<NB, T>(G, wt, f);
+                op_rstep<NB, T>(R, wt, f);
             }
         }
         __syncwarp();
     }
-    if (c < p.nchunks) op_store<NB, T>(G, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ);
-    // suffix walk
-    op_identity<NB, T>(G);
-    slab_issue<S, NB>(buf, p.bound, chain0, p.P, p.N, ns - 1, lane);
-    cp_async_commit();
-    for (int t = 0; t < ns; ++t) {
-        const int s = ns - 1 - t;
-        if (s > 0) slab_issue<S, NB>(buf + ((t + 1) & 1) * NB * TILE, p.bound, chain0, p.P, p.N, s - 1, lane);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncwarp();
-        const double *cur = buf + (t & 1) * NB * TILE;
-#pragma unroll
-        for (int jj = S - 1; jj >= 0; --jj) {
-            const int64_t x = x0 + (int64_t)s * S + jj;
-            if (x < x1) {
-                slab_f<NB, S>(f, cur, lane, jj);
-                op_step<NB, T>(G, wt, f);
-            }
-        }
-        __syncwarp();
+    if (c < p.nchunks) {
+        op_store<NB, T>(G, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ);
+        op_store<NB, T>(R, static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
     }
-    if (c < p.nchunks) op_store<NB, T>(G, static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -364,7 +348,7 @@ struct ApplyVecs {
     static constexpr bool kOut = MODE == MODE_MARG || MODE == MODE_UPD;
 };
 
-template <int NB, typename T, int MODE>
+template <int NB, typename T, int MODE, bool NEXT>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p) {
     using AV = ApplyVecs<NB, MODE>;
     constexpr int M = 1 << NB;
@@ -400,6 +384,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p) {
         vec_unit<NB, T>(st);
     }
     double f[NB > 0 ? NB : 1];
+    // next update's operators (fused, MODE_UPD only): bound set of k+1 = this bound set with
+    // slot nxt_slot replaced by the new phi_k (or shifted by one when k = l-1)
+    T Gn[NEXT ? NB + 1 : 1][NEXT ? M : 1], Rn[NEXT ? NB + 1 : 1][NEXT ? M : 1];
+    if constexpr (NEXT) {
+        op_identity<NB, T>(Gn);
+        op_identity<NB, T>(Rn);
+    }
     // ---- suffix walk with checkpoints: ck[j] = B at min(x0 + (j+1)Q, x1) ----
     T ck[NSUB][M];
     if (live && x1 > x0) {
@@ -483,6 +474,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p) {
                                 if (!(jv > 0.0) || !isfinite(jv) || !isfinite(phi)) raise_status(p, 6 /*EOVERFLOW*/);
                             }
                             obuf[lane * (S + 1) + jx] = phi;
+                            if constexpr (NEXT) {
+                                double fn[NB > 0 ? NB : 1];
+#pragma unroll
+                                for (int b = 0; b < NB; ++b)
+                                    fn[b] = p.nxt_shift ? (b + 1 < NB ? f[b + 1] : phi) : (b == p.nxt_slot ? phi : f[b]);
+                                op_step<NB, T>(Gn, wt, fn);
+                                op_rstep<NB, T>(Rn, wt, fn);
+                            }
                         } else if (MODE == MODE_RES) {
                             acc += fabs(cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * jv -
                                         cur[(AV::IMU * 32 + lane) * (S + 1) + jx]);
@@ -501,6 +500,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p) {
         }
     }
     if ((MODE == MODE_RES || MODE == MODE_COST) && live) p.partial[c] = acc;
+    if constexpr (NEXT) {
+        if (live) {
+            op_store<NB, T>(Gn, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ);
+            op_store<NB, T>(Rn, static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+        }
+    }
 }
 
 template <int NB, typename T>
@@ -512,24 +517,25 @@ static size_t apply_smem() {
     return (size_t)kWarpsPerCta * (2 * ApplyVecs<NB, MODE>::NV + 1) * 32 * (slab_s(NB) + 1) * sizeof(double);
 }
 
-template <int NB, typename T, int MODE>
+template <int NB, typename T, int MODE, bool NEXT = false>
 static void launch_apply(const Plan &p, int64_t nb, int tpb, cudaStream_t s) {
     const size_t sm = apply_smem<NB, MODE>();
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_chunk_apply<NB, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_chunk_apply<NB, T, MODE, NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         attr = true;
     }
-    k_chunk_apply<NB, T, MODE><<<(unsigned)nb, tpb, sm, s>>>(p);
+    k_chunk_apply<NB, T, MODE, NEXT><<<(unsigned)nb, tpb, sm, s>>>(p);
 }
 
 // ---------------------------------------------------------------------------------------
 template <int NB, typename T>
-static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *launches, cudaEvent_t *ev) {
+static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *launches, cudaEvent_t *ev,
+                              bool with_ops, bool next) {
     const int tpb = kWarpsPerCta * 32;
     const int64_t nb = (p.nchunks + tpb - 1) / tpb;
     if (ev) cudaEventRecord(ev[0], s);
-    {
+    if (with_ops) {
         const size_t sm = ops_smem<NB, T>();
         static bool attr = false;
         if (!attr) {
@@ -537,9 +543,9 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
             attr = true;
         }
         k_chunk_ops<NB, T><<<(unsigned)nb, tpb, sm, s>>>(p);
+        ++*launches;
     }
     if (ev) cudaEventRecord(ev[1], s);
-    ++*launches;
     constexpr bool kWarpScan = NB <= 3 && sizeof(T) == sizeof(double);
     // up-sweep
     for (int i = 0; i + 1 < p.nlev; ++i) {
@@ -584,7 +590,13 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
     if (ev) cudaEventRecord(ev[2], s);
     switch (mode) {
         case MODE_MARG: launch_apply<NB, T, MODE_MARG>(p, nb, tpb, s); break;
-        case MODE_UPD: launch_apply<NB, T, MODE_UPD>(p, nb, tpb, s); break;
+        case MODE_UPD:
+            if (next) {
+                if constexpr (sizeof(T) == sizeof(double)) launch_apply<NB, T, MODE_UPD, true>(p, nb, tpb, s);
+            } else {
+                launch_apply<NB, T, MODE_UPD>(p, nb, tpb, s);
+            }
+            break;
         case MODE_RES: launch_apply<NB, T, MODE_RES>(p, nb, tpb, s); break;
         default: launch_apply<NB, T, MODE_COST>(p, nb, tpb, s); break;
     }
@@ -593,14 +605,15 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
     return cudaGetLastError();
 }
 
-cudaError_t launch_product(const Plan &p, int mode, cudaStream_t s, int64_t *launches, cudaEvent_t *ev) {
+cudaError_t launch_product(const Plan &p, int mode, cudaStream_t s, int64_t *launches, cudaEvent_t *ev,
+                           bool with_ops, bool next) {
     const bool dual = mode == MODE_COST;
     switch (p.NB) {
-        case 1: return dual ? product_nb<1, Dual>(p, mode, s, launches, ev) : product_nb<1, double>(p, mode, s, launches, ev);
-        case 2: return dual ? product_nb<2, Dual>(p, mode, s, launches, ev) : product_nb<2, double>(p, mode, s, launches, ev);
-        case 3: return dual ? product_nb<3, Dual>(p, mode, s, launches, ev) : product_nb<3, double>(p, mode, s, launches, ev);
-        case 4: return dual ? product_nb<4, Dual>(p, mode, s, launches, ev) : product_nb<4, double>(p, mode, s, launches, ev);
-        case 5: return dual ? product_nb<5, Dual>(p, mode, s, launches, ev) : product_nb<5, double>(p, mode, s, launches, ev);
+        case 1: return dual ? product_nb<1, Dual>(p, mode, s, launches, ev, with_ops, next) : product_nb<1, double>(p, mode, s, launches, ev, with_ops, next);
+        case 2: return dual ? product_nb<2, Dual>(p, mode, s, launches, ev, with_ops, next) : product_nb<2, double>(p, mode, s, launches, ev, with_ops, next);
+        case 3: return dual ? product_nb<3, Dual>(p, mode, s, launches, ev, with_ops, next) : product_nb<3, double>(p, mode, s, launches, ev, with_ops, next);
+        case 4: return dual ? product_nb<4, Dual>(p, mode, s, launches, ev, with_ops, next) : product_nb<4, double>(p, mode, s, launches, ev, with_ops, next);
+        case 5: return dual ? product_nb<5, Dual>(p, mode, s, launches, ev, with_ops, next) : product_nb<5, double>(p, mode, s, launches, ev, with_ops, next);
         default: return cudaErrorInvalidValue;
     }
 }
