@@ -277,9 +277,10 @@ static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double
     p.N = c->N;
     p.P = c->P;
     p.nchunks = c->nchunks;
-    int b = 0;
-    for (int q = 0; q < c->l; ++q)
-        if (q != k) p.bound[b++] = lin[q];
+    // Bound marginals in CYCLIC order k+1, k+2, ..., k+l-1 (mod l).  J_k is symmetric in its
+    // bound vectors, and with this order the bound set of update k+1 is this one shifted by one
+    // slot with the new phi_k appended, so the fused next-update operators need no selects.
+    for (int b = 0; b < c->l - 1; ++b) p.bound[b] = lin[(k + 1 + b) % c->l];
     p.phik = lin[k];
     p.muk = mu;
     p.outk = out;
@@ -297,10 +298,6 @@ static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double
     p.status = &c->dsc->status;
     p.fail_iter = &c->dsc->fail_iter;
     p.iter = iter;
-    // bound set of update k+1 (mod l): for k < l-1 it is this bound set with slot k (marginal
-    // k+1) replaced by marginal k; for k = l-1 it is {1..l-1} = this set shifted by one.
-    p.nxt_slot = k;
-    p.nxt_shift = (k == c->l - 1) ? 1 : 0;
     return p;
 }
 

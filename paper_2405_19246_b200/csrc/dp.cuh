@@ -71,6 +71,8 @@ __device__ __forceinline__ Dual mad(Dual a, Dual b, Dual acc) {
 __device__ __forceinline__ double mads(double f, double b, double acc) { return fma(f, b, acc); }
 __device__ __forceinline__ Dual mads(double f, Dual b, Dual acc) { return Dual{fma(f, b.v, acc.v), fma(f, b.d, acc.d)}; }
 
+__device__ __forceinline__ Dual operator+(Dual a, Dual b) { return Dual{a.v + b.v, a.d + b.d}; }
+
 __device__ __forceinline__ double value_of(double a) { return a; }
 __device__ __forceinline__ double value_of(Dual a) { return a.v; }
 
@@ -86,10 +88,11 @@ __device__ __forceinline__ void load_weight(Dual &o, const Weights &W, int a) { 
 // One grid point of the recurrence.  `wc[a]` = w_{c+a}; states S with popcount > LIMIT are
 // not needed (operators) and are skipped at compile time.
 // ---------------------------------------------------------------------------------------
-template <int NB, typename T>
+// W0ONE: wc[0] is w_0 = lambda^0 = 1 exactly, so the empty-set state needs no multiply.
+template <int NB, typename T, bool W0ONE = false>
 __device__ __forceinline__ void dp_diag(T (&st)[1 << NB], const T *wc, int limit = NB) {
 #pragma unroll
-    for (int S = 0; S < (1 << NB); ++S)
+    for (int S = W0ONE ? 1 : 0; S < (1 << NB); ++S)
         if (pc(S) <= limit) st[S] = mul(wc[pc(S)], st[S]);
 }
 
@@ -124,7 +127,8 @@ template <int NB, typename T>
 __device__ __forceinline__ void op_step(T (&G)[NB + 1][1 << NB], const T *wt, const double (&f)[NB > 0 ? NB : 1]) {
 #pragma unroll
     for (int c = 0; c <= NB; ++c) {
-        dp_diag<NB, T>(G[c], wt + c, NB - c);
+        if (c == 0) dp_diag<NB, T, true>(G[c], wt + c, NB - c);
+        else dp_diag<NB, T>(G[c], wt + c, NB - c);
         dp_place<NB, T>(G[c], f, NB - c);
     }
 }
@@ -146,7 +150,7 @@ __device__ __forceinline__ void op_rstep(T (&G)[NB + 1][1 << NB], const T *wt, c
             for (int V = 0; V < (1 << NB); ++V)
                 if (((V >> b) & 1) && pc(V) <= NB - c) G[c][V] = mads(f[b], G[c + 1][V ^ (1 << b)], G[c][V]);
 #pragma unroll
-    for (int c = 0; c <= NB; ++c)
+    for (int c = 1; c <= NB; ++c)  // slice 0 scales by w_0 = 1
 #pragma unroll
         for (int V = 0; V < (1 << NB); ++V)
             if (pc(V) <= NB - c) G[c][V] = mul(wt[c], G[c][V]);

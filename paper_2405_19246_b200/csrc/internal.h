@@ -40,15 +40,13 @@ struct Plan {
     int *status;                     // device status (mmot_status) of the run
     int *fail_iter;                  // device: sweep index of the first failure
     int iter;                        // current sweep index (for fail_iter)
-    int nxt_slot;                    // fused next-operator bound set: replace bound slot nxt_slot by phi_k
-    int nxt_shift;                   // ... or (k = l-1) drop slot 0, shift, append phi_k
 };
 
 // Enqueue one product (ops -> scan -> apply) of `mode` on `s`.  Returns the number of
 // kernels launched through *launches (accumulated).
 // with_ops = false skips the operator phase (operators already in ops_f/ops_b level 0, e.g.
 // written by the previous fused update); next = true (MODE_UPD) fuses the operators of the
-// NEXT update's bound set into the apply walk (slot nxt_slot / nxt_shift of the Plan).
+// NEXT update's bound set into the apply walk (cyclic bound order, see make_plan).
 cudaError_t launch_product(const Plan &p, int mode, cudaStream_t s, int64_t *launches,
                            cudaEvent_t *ev = nullptr /* 4 events: before ops, after ops, after scan, after apply */,
                            bool with_ops = true, bool next = false);

@@ -53,17 +53,22 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int NPEND>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
 
-// Issue the copies of slab s of NV vectors into buf[NV][32][S+1].
+// Issue the copies of slab s of NV vectors into buf[NV][32][S+1].  Element e = it*32+lane of
+// the [32 chains][S points] slab is chain r = e / S, point j = e % S; chains >= cend (dead
+// lanes of the last warp) and points beyond N are zero-filled (src-size 0).
 template <int S, int NV>
 __device__ __forceinline__ void slab_issue(double *buf, const double *const *vec, int64_t chain0, int64_t P,
                                            int64_t N, int s, int lane) {
+    constexpr int RPI = 32 / S;  // chains per warp instruction
+    const int r0 = lane / S, j = lane % S;
+    const int64_t off = (int64_t)s * S + j;
+    const int64_t xb = (chain0 + r0) * P + off;
+    const bool offok = off < P;
 #pragma unroll
     for (int it = 0; it < S; ++it) {
-        const int e = it * 32 + lane;
-        const int r = e / S, j = e % S;
-        const int64_t off = (int64_t)s * S + j;
-        const int64_t x = (chain0 + r) * P + off;
-        const bool valid = off < P && x < N;
+        const int r = it * RPI + r0;
+        const int64_t x = xb + (int64_t)(it * RPI) * P;
+        const bool valid = offok && x < N;
 #pragma unroll
         for (int v = 0; v < NV; ++v)
             cp_async8(buf + (v * 32 + r) * (S + 1) + j, vec[v] + (valid ? x : 0), valid);
@@ -72,15 +77,15 @@ __device__ __forceinline__ void slab_issue(double *buf, const double *const *vec
 
 // Store an output slab obuf[32][S+1] to global (coalesced, like slab_issue).
 template <int S>
-__device__ __forceinline__ void slab_store(const double *obuf, double *out, int64_t chain0, int64_t P, int64_t N,
-                                           int s, int lane) {
+__device__ __forceinline__ void slab_store(const double *obuf, double *out, int64_t chain0, int64_t cend, int64_t P,
+                                           int64_t N, int s, int lane) {
 #pragma unroll
     for (int it = 0; it < S; ++it) {
         const int e = it * 32 + lane;
         const int r = e / S, j = e % S;
         const int64_t off = (int64_t)s * S + j;
         const int64_t x = (chain0 + r) * P + off;
-        if (off < P && x < N) out[x] = obuf[r * (S + 1) + j];
+        if (off < P && x < N && chain0 + r < cend) out[x] = obuf[r * (S + 1) + j];
     }
 }
 
@@ -348,25 +353,90 @@ struct ApplyVecs {
     static constexpr bool kOut = MODE == MODE_MARG || MODE == MODE_UPD;
 };
 
-template <int NB, typename T, int MODE, bool NEXT>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p) {
+// mu / J with a Newton-refined reciprocal: no divide slow path, no branch.
+__device__ __forceinline__ double div_nr(double mu, double j) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(j));
+    double e = fma(-j, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-j, r, 1.0);
+    r = fma(r, e, r);
+    const double q = mu * r;
+    return fma(r, fma(-j, q, mu), q);
+}
+
+// Combine J[m] = sum_S F_m[S] H_m[S^c] with two independent accumulators.
+template <int NB, typename T>
+__device__ __forceinline__ T combine(const T (&F)[1 << NB], const T (&H)[1 << NB]) {
+    constexpr int M = 1 << NB;
+    T a = zero_of(T{}), b = zero_of(T{});
+#pragma unroll
+    for (int S = 0; S < M; S += 2) {
+        a = mad(F[S], H[(M - 1) ^ S], a);
+        if (S + 1 < M) b = mad(F[S + 1], H[(M - 1) ^ (S + 1)], b);
+    }
+    return T{a} + T{b};
+}
+
+// Per-point epilogue of the apply phase.  Returns the value written to the output slab
+// (marginal / new phi_k), accumulates residual / cost partial sums, flags loss of range.
+template <int NB, typename T, int MODE>
+__device__ __forceinline__ double epilogue(const T &J, const double *cur, int lane, int jx, double &acc, bool &bad) {
+    using AV = ApplyVecs<NB, MODE>;
+    constexpr int S = slab_s(NB);
+    const double jv = value_of(J);
+    if (MODE == MODE_MARG) {
+        return cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * jv;
+    } else if (MODE == MODE_UPD) {
+        const double mu = cur[(AV::IMU * 32 + lane) * (S + 1) + jx];
+        const double q = div_nr(mu, jv);
+        const bool nz = mu != 0.0;
+        bad |= nz && !(jv > 0.0 && jv <= 1.7976931348623157e308 && q <= 1.7976931348623157e308);
+        return nz ? q : 0.0;
+    } else if (MODE == MODE_RES) {
+        acc += fabs(cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * jv - cur[(AV::IMU * 32 + lane) * (S + 1) + jx]);
+        return 0.0;
+    } else {
+        if constexpr (sizeof(T) == sizeof(Dual))
+            acc += cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * reinterpret_cast<const Dual &>(J).d;
+        return 0.0;
+    }
+}
+
+// Next-update operator step (fused): the bound values of update k+1 at this point.
+template <int NB, typename T>
+__device__ __forceinline__ void next_ops_step(T (&Gn)[NB + 1][1 << NB], T (&Rn)[NB + 1][1 << NB], const T *wt,
+                                              const double (&f)[NB > 0 ? NB : 1], double phi, const Plan &p) {
+    double fn[NB > 0 ? NB : 1];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) fn[b] = b + 1 < NB ? f[b + 1] : phi;  // cyclic bound order (see make_plan)
+    op_step<NB, T>(Gn, wt, fn);
+    op_rstep<NB, T>(Rn, wt, fn);
+}
+
+// FULL = every live lane owns a complete chain of P points (P % S == 0): no per-point bounds
+// predicates, compile-time checkpoint positions.  The ragged last chain (and tiny P) use
+// FULL = false.  Chains [cbeg, cend) are processed.
+template <int NB, typename T, int MODE, bool NEXT, bool FULL>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64_t cbeg, int64_t cend) {
     using AV = ApplyVecs<NB, MODE>;
     constexpr int M = 1 << NB;
     constexpr int Q = sub_q(NB);
     constexpr int NSUB = nsub_max(NB);
     constexpr int S = slab_s(NB);
+    constexpr int QPS = S / Q;
     constexpr int TILE = 32 * (S + 1);
     constexpr int NV = AV::NV;
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t chain0 = ((int64_t)blockIdx.x * kWarpsPerCta + warp) * 32;
-    if (chain0 >= p.nchunks || *p.stop) return;
+    const int64_t chain0 = cbeg + ((int64_t)blockIdx.x * kWarpsPerCta + warp) * 32;
+    if (chain0 >= cend || *p.stop) return;
     double *buf = smem + (size_t)warp * (2 * NV + 1) * TILE;
     double *obuf = buf + 2 * NV * TILE;
     const int64_t c = chain0 + lane;
-    const bool live = c < p.nchunks;
+    const bool live = c < cend;
     const int64_t x0 = c * p.P;
-    const int64_t x1 = min(p.N, x0 + p.P);
+    const int64_t x1 = FULL ? x0 + p.P : min(p.N, x0 + p.P);
     const int ns = (int)((p.P + S - 1) / S);
     const double *vecs[NV];
 #pragma unroll
@@ -384,22 +454,24 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p) {
         vec_unit<NB, T>(st);
     }
     double f[NB > 0 ? NB : 1];
-    // next update's operators (fused, MODE_UPD only): bound set of k+1 = this bound set with
-    // slot nxt_slot replaced by the new phi_k (or shifted by one when k = l-1)
     T Gn[NEXT ? NB + 1 : 1][NEXT ? M : 1], Rn[NEXT ? NB + 1 : 1][NEXT ? M : 1];
     if constexpr (NEXT) {
         op_identity<NB, T>(Gn);
         op_identity<NB, T>(Rn);
     }
-    // ---- suffix walk with checkpoints: ck[j] = B at min(x0 + (j+1)Q, x1) ----
+    // ---- walk 1 (right to left): suffix states, checkpoint ck[j] = B at min(x0+(j+1)Q, x1) ----
     T ck[NSUB][M];
-    if (live && x1 > x0) {
+    if (FULL) {
+#pragma unroll
+        for (int S2 = 0; S2 < M; ++S2) ck[p.P / Q - 1][S2] = st[S2];
+    } else if (live && x1 > x0) {
         const int jl = (int)((x1 - 1 - x0) / Q);
 #pragma unroll
         for (int S2 = 0; S2 < M; ++S2) ck[jl][S2] = st[S2];
     }
     slab_issue<S, NB>(buf, vecs, chain0, p.P, p.N, ns - 1, lane);
     cp_async_commit();
+#pragma unroll 1
     for (int t = 0; t < ns; ++t) {
         const int s = ns - 1 - t;
         if (s > 0) slab_issue<S, NB>(buf + ((t + 1) & 1) * NV * TILE, vecs, chain0, p.P, p.N, s - 1, lane);
@@ -409,24 +481,38 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p) {
         const double *cur = buf + (t & 1) * NV * TILE;
 #pragma unroll
         for (int jj = S - 1; jj >= 0; --jj) {
-            const int64_t x = x0 + (int64_t)s * S + jj;
-            if (x < x1 && x > x0) {
+            if (FULL) {
+                if (jj == 0 && s == 0) break;
                 slab_f<NB, S>(f, cur, lane, jj);
-                dp_diag<NB, T>(st, wt);
+                dp_diag<NB, T, true>(st, wt);
                 dp_place<NB, T>(st, f);
-                if ((((int)(x - x0)) % Q) == 0) {
-                    const int j = (int)((x - x0) / Q) - 1;
+                if (jj % Q == 0) {
+                    const int j = s * QPS + jj / Q - 1;
 #pragma unroll
                     for (int S2 = 0; S2 < M; ++S2) ck[j][S2] = st[S2];
+                }
+            } else {
+                const int64_t x = x0 + (int64_t)s * S + jj;
+                if (x < x1 && x > x0) {
+                    slab_f<NB, S>(f, cur, lane, jj);
+                    dp_diag<NB, T, true>(st, wt);
+                    dp_place<NB, T>(st, f);
+                    if ((((int)(x - x0)) % Q) == 0) {
+                        const int j = (int)((x - x0) / Q) - 1;
+#pragma unroll
+                        for (int S2 = 0; S2 < M; ++S2) ck[j][S2] = st[S2];
+                    }
                 }
             }
         }
         __syncwarp();
     }
-    // ---- prefix walk: per Q-block rebuild suffix states, combine, epilogue ----
+    // ---- walk 2 (left to right): rebuild suffix states per Q-block, prefix step, combine ----
     double acc = 0.0;
+    bool bad = false;
     slab_issue<S, NV>(buf, vecs, chain0, p.P, p.N, 0, lane);
     cp_async_commit();
+#pragma unroll 1
     for (int s = 0; s < ns; ++s) {
         if (s + 1 < ns) slab_issue<S, NV>(buf + ((s + 1) & 1) * NV * TILE, vecs, chain0, p.P, p.N, s + 1, lane);
         cp_async_commit();
@@ -434,17 +520,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p) {
         __syncwarp();
         const double *cur = buf + (s & 1) * NV * TILE;
 #pragma unroll
-        for (int jb = 0; jb < S / Q; ++jb) {
+        for (int jb = 0; jb < QPS; ++jb) {
             const int64_t base = x0 + (int64_t)s * S + jb * Q;
-            const int len = (int)max((int64_t)0, min((int64_t)Q, x1 - base));
-            if (len > 0) {
+            const int len = FULL ? Q : (int)max((int64_t)0, min((int64_t)Q, x1 - base));
+            if (FULL || len > 0) {
                 T H[Q][M];
 #pragma unroll
-                for (int S2 = 0; S2 < M; ++S2) st[S2] = ck[(int)((base - x0) / Q)][S2];
+                for (int S2 = 0; S2 < M; ++S2) st[S2] = ck[s * QPS + jb][S2];
 #pragma unroll
                 for (int i = Q - 1; i >= 0; --i) {
-                    if (i < len) {
-                        dp_diag<NB, T>(st, wt);
+                    if (FULL || i < len) {
+                        dp_diag<NB, T, true>(st, wt);
 #pragma unroll
                         for (int S2 = 0; S2 < M; ++S2) H[i][S2] = st[S2];
                         if (i > 0) {
@@ -455,50 +541,26 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p) {
                 }
 #pragma unroll
                 for (int i = 0; i < Q; ++i) {
-                    if (i < len) {
+                    if (FULL || i < len) {
                         const int jx = jb * Q + i;
                         slab_f<NB, S>(f, cur, lane, jx);
-                        dp_diag<NB, T>(F, wt);
+                        dp_diag<NB, T, true>(F, wt);
                         dp_place<NB, T>(F, f);
-                        T J = zero_of(T{});
-#pragma unroll
-                        for (int S2 = 0; S2 < M; ++S2) J = mad(F[S2], H[i][(M - 1) ^ S2], J);
-                        const double jv = value_of(J);
-                        if (MODE == MODE_MARG) {
-                            obuf[lane * (S + 1) + jx] = cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * jv;
-                        } else if (MODE == MODE_UPD) {
-                            const double mu = cur[(AV::IMU * 32 + lane) * (S + 1) + jx];
-                            double phi = 0.0;
-                            if (mu != 0.0) {
-                                phi = mu / jv;
-                                if (!(jv > 0.0) || !isfinite(jv) || !isfinite(phi)) raise_status(p, 6 /*EOVERFLOW*/);
-                            }
-                            obuf[lane * (S + 1) + jx] = phi;
-                            if constexpr (NEXT) {
-                                double fn[NB > 0 ? NB : 1];
-#pragma unroll
-                                for (int b = 0; b < NB; ++b)
-                                    fn[b] = p.nxt_shift ? (b + 1 < NB ? f[b + 1] : phi) : (b == p.nxt_slot ? phi : f[b]);
-                                op_step<NB, T>(Gn, wt, fn);
-                                op_rstep<NB, T>(Rn, wt, fn);
-                            }
-                        } else if (MODE == MODE_RES) {
-                            acc += fabs(cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * jv -
-                                        cur[(AV::IMU * 32 + lane) * (S + 1) + jx]);
-                        } else {  // MODE_COST
-                            if constexpr (sizeof(T) == sizeof(Dual))
-                                acc += cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * reinterpret_cast<const Dual &>(J).d;
-                        }
+                        const T J = combine<NB, T>(F, H[i]);
+                        const double o = epilogue<NB, T, MODE>(J, cur, lane, jx, acc, bad);
+                        if (AV::kOut) obuf[lane * (S + 1) + jx] = o;
+                        if constexpr (NEXT) next_ops_step<NB, T>(Gn, Rn, wt, f, o, p);
                     }
                 }
             }
         }
         __syncwarp();
         if (AV::kOut) {
-            slab_store<S>(obuf, p.outk, chain0, p.P, p.N, s, lane);
+            slab_store<S>(obuf, p.outk, chain0, cend, p.P, p.N, s, lane);
             __syncwarp();
         }
     }
+    if (bad && live) raise_status(p, 6 /*EOVERFLOW*/);
     if ((MODE == MODE_RES || MODE == MODE_COST) && live) p.partial[c] = acc;
     if constexpr (NEXT) {
         if (live) {
@@ -517,15 +579,30 @@ static size_t apply_smem() {
     return (size_t)kWarpsPerCta * (2 * ApplyVecs<NB, MODE>::NV + 1) * 32 * (slab_s(NB) + 1) * sizeof(double);
 }
 
-template <int NB, typename T, int MODE, bool NEXT = false>
-static void launch_apply(const Plan &p, int64_t nb, int tpb, cudaStream_t s) {
+template <int NB, typename T, int MODE, bool NEXT, bool FULL>
+static void launch_apply_range(const Plan &p, int64_t cbeg, int64_t cend, cudaStream_t s, int64_t *launches) {
+    if (cend <= cbeg) return;
     const size_t sm = apply_smem<NB, MODE>();
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_chunk_apply<NB, T, MODE, NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_chunk_apply<NB, T, MODE, NEXT, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
         attr = true;
     }
-    k_chunk_apply<NB, T, MODE, NEXT><<<(unsigned)nb, tpb, sm, s>>>(p);
+    const int tpb = kWarpsPerCta * 32;
+    const int64_t nb = (cend - cbeg + tpb - 1) / tpb;
+    k_chunk_apply<NB, T, MODE, NEXT, FULL><<<(unsigned)nb, tpb, sm, s>>>(p, cbeg, cend);
+    ++*launches;
+}
+
+// Full chains through the predicate-free kernel, the ragged last chain (or every chain when
+// P is not a multiple of the slab length) through the general one.
+template <int NB, typename T, int MODE, bool NEXT = false>
+static void launch_apply(const Plan &p, int64_t /*nb*/, int /*tpb*/, cudaStream_t s, int64_t *launches) {
+    const bool full_ok = p.P % slab_s(NB) == 0;
+    const int64_t nfull = full_ok ? p.N / p.P : 0;
+    launch_apply_range<NB, T, MODE, NEXT, true>(p, 0, nfull, s, launches);
+    launch_apply_range<NB, T, MODE, NEXT, false>(p, nfull, p.nchunks, s, launches);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -589,18 +666,17 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
     }
     if (ev) cudaEventRecord(ev[2], s);
     switch (mode) {
-        case MODE_MARG: launch_apply<NB, T, MODE_MARG>(p, nb, tpb, s); break;
+        case MODE_MARG: launch_apply<NB, T, MODE_MARG>(p, nb, tpb, s, launches); break;
         case MODE_UPD:
             if (next) {
-                if constexpr (sizeof(T) == sizeof(double)) launch_apply<NB, T, MODE_UPD, true>(p, nb, tpb, s);
+                if constexpr (sizeof(T) == sizeof(double)) launch_apply<NB, T, MODE_UPD, true>(p, nb, tpb, s, launches);
             } else {
-                launch_apply<NB, T, MODE_UPD>(p, nb, tpb, s);
+                launch_apply<NB, T, MODE_UPD>(p, nb, tpb, s, launches);
             }
             break;
-        case MODE_RES: launch_apply<NB, T, MODE_RES>(p, nb, tpb, s); break;
-        default: launch_apply<NB, T, MODE_COST>(p, nb, tpb, s); break;
+        case MODE_RES: launch_apply<NB, T, MODE_RES>(p, nb, tpb, s, launches); break;
+        default: launch_apply<NB, T, MODE_COST>(p, nb, tpb, s, launches); break;
     }
-    ++*launches;
     if (ev) cudaEventRecord(ev[3], s);
     return cudaGetLastError();
 }
