@@ -16,10 +16,14 @@
 // Everything is fp64 (double or dual numbers for the cost).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "internal.h"
 
 namespace mmot {
+
+// MMOT_NO_TMEM=1 disables the TMEM checkpoint kernels (A/B testing).
+static const bool g_no_tmem = [] { const char *e = getenv("MMOT_NO_TMEM"); return e && e[0] == '1'; }();
 
 // ---------------------------------------------------------------------------------------
 template <int NB, typename T>
@@ -353,6 +357,84 @@ struct ApplyVecs {
     static constexpr bool kOut = MODE == MODE_MARG || MODE == MODE_UPD;
 };
 
+// ---------------------------------------------------------------------------------------
+// Tensor memory (TMEM) as a per-warp checkpoint store.  The path has no MMA, so the 256 KB of
+// TMEM per SM are free; a CTA of 4 warps allocates 256 columns (2 CTAs per SM), warp w owns TMEM
+// lanes [32w, 32w+32) and therefore 256 x 32-bit words per lane: 128 doubles = the suffix
+// checkpoints of one chain (every 2Q points), instead of local memory that spills to DRAM.
+// ---------------------------------------------------------------------------------------
+constexpr int kTmemCols = 256;
+
+__device__ __forceinline__ void tmem_alloc(uint32_t *smem_slot) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(smem_slot);
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(a), "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(kTmemCols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// Store / load M doubles (2M 32-bit columns) of this thread's TMEM lane at column offset col.
+template <int M>
+__device__ __forceinline__ void tmem_st_vec(uint32_t taddr, const double (&v)[M]) {
+    uint32_t r[2 * M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        r[2 * i] = __double2loint(v[i]);
+        r[2 * i + 1] = __double2hiint(v[i]);
+    }
+    if constexpr (M == 2) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+                     "r"(r[2]), "r"(r[3])
+                     : "memory");
+    } else if constexpr (M == 4) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr),
+                     "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                     : "memory");
+    } else {
+        static_assert(M == 8, "tmem_st_vec: M in {2,4,8}");
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+            "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(taddr),
+            "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+            "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+            : "memory");
+    }
+}
+
+template <int M>
+__device__ __forceinline__ void tmem_ld_vec(uint32_t taddr, double (&v)[M]) {
+    uint32_t r[2 * M];
+    if constexpr (M == 2) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                     : "r"(taddr)
+                     : "memory");
+    } else if constexpr (M == 4) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                     : "r"(taddr)
+                     : "memory");
+    } else {
+        static_assert(M == 8, "tmem_ld_vec: M in {2,4,8}");
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr)
+            : "memory");
+    }
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+
 // mu / J with a Newton-refined reciprocal: no divide slow path, no branch.
 __device__ __forceinline__ double div_nr(double mu, double j) {
     double r;
@@ -570,6 +652,154 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64
     }
 }
 
+// FULL-chain apply with the suffix checkpoints in TMEM (fp64, NB <= 3).  Walk 1 (right to left)
+// stores B at every 2Q-block end (one slab = one 2Q-block).  Walk 2 (left to right), per block:
+// reload B_end from TMEM, walk the right half back to get B_mid (Q extra steps), rebuild the
+// left half's suffix states from B_mid and run the prefix/combine/epilogue over it, then the
+// same for the right half from B_end.
+template <int NB, int MODE, bool NEXT>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply_tm(Plan p, int64_t cbeg, int64_t cend) {
+    using T = double;
+    using AV = ApplyVecs<NB, MODE>;
+    constexpr int M = 1 << NB;
+    constexpr int Q = sub_q(NB);
+    constexpr int Q2 = 2 * Q;
+    constexpr int S = slab_s(NB);
+    static_assert(S == Q2, "one slab per checkpoint block");
+    constexpr int TILE = 32 * (S + 1);
+    constexpr int NV = AV::NV;
+    __shared__ uint32_t tmem_slot;
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t chain0 = cbeg + ((int64_t)blockIdx.x * kWarpsPerCta + warp) * 32;
+    const bool active = chain0 < cend && !*(volatile int *)p.stop;
+    if (warp == 0) tmem_alloc(&tmem_slot);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tbase = tmem_slot + ((uint32_t)(32 * warp) << 16);
+    if (active) {
+        double *buf = smem + (size_t)warp * (2 * NV + 1) * TILE;
+        double *obuf = buf + 2 * NV * TILE;
+        const int64_t c = chain0 + lane;
+        const bool live = c < cend;
+        const int ns = (int)(p.P / S);
+        const double *vecs[NV];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) vecs[b] = p.bound[b];
+        if (AV::kMu) vecs[AV::IMU] = p.muk;
+        if (AV::kPhi) vecs[AV::IPHI] = p.phik;
+        T wt[NB + 2];
+        load_weights<NB, T>(wt, p.W);
+        T F[M], st[M];
+        if (live) {
+            vec_load<NB, T>(F, static_cast<const T *>(p.car_f[0]) + c * M);
+            vec_load<NB, T>(st, static_cast<const T *>(p.car_b[0]) + c * M);
+        } else {
+            vec_unit<NB, T>(F);
+            vec_unit<NB, T>(st);
+        }
+        double f[NB > 0 ? NB : 1];
+        T Gn[NEXT ? NB + 1 : 1][NEXT ? M : 1], Rn[NEXT ? NB + 1 : 1][NEXT ? M : 1];
+        if constexpr (NEXT) {
+            op_identity<NB, T>(Gn);
+            op_identity<NB, T>(Rn);
+        }
+        // ---- walk 1: right to left, checkpoint B at every block end into TMEM ----
+        slab_issue<S, NB>(buf, vecs, chain0, p.P, p.N, ns - 1, lane);
+        cp_async_commit();
+#pragma unroll 1
+        for (int t = 0; t < ns; ++t) {
+            const int s = ns - 1 - t;
+            tmem_st_vec<M>(tbase + (uint32_t)(s * 2 * M), st);
+            if (s > 0) slab_issue<S, NB>(buf + ((t + 1) & 1) * NV * TILE, vecs, chain0, p.P, p.N, s - 1, lane);
+            cp_async_commit();
+            if (s == 0) break;  // the state left of the chain is not needed
+            cp_async_wait<1>();
+            __syncwarp();
+            const double *cur = buf + (t & 1) * NV * TILE;
+#pragma unroll
+            for (int jj = S - 1; jj >= 0; --jj) {
+                slab_f<NB, S>(f, cur, lane, jj);
+                dp_diag<NB, T, true>(st, wt);
+                dp_place<NB, T>(st, f);
+            }
+            __syncwarp();
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+        tmem_wait_st();
+        // ---- walk 2: left to right ----
+        double acc = 0.0;
+        bool bad = false;
+        slab_issue<S, NV>(buf, vecs, chain0, p.P, p.N, 0, lane);
+        cp_async_commit();
+#pragma unroll 1
+        for (int s = 0; s < ns; ++s) {
+            if (s + 1 < ns) slab_issue<S, NV>(buf + ((s + 1) & 1) * NV * TILE, vecs, chain0, p.P, p.N, s + 1, lane);
+            cp_async_commit();
+            T bend[M];
+            tmem_ld_vec<M>(tbase + (uint32_t)(s * 2 * M), bend);
+            cp_async_wait<1>();
+            __syncwarp();
+            const double *cur = buf + (s & 1) * NV * TILE;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                // suffix state at the right end of this half-block
+#pragma unroll
+                for (int S2 = 0; S2 < M; ++S2) st[S2] = bend[S2];
+                if (half == 0) {
+#pragma unroll
+                    for (int i = Q2 - 1; i >= Q; --i) {
+                        slab_f<NB, S>(f, cur, lane, i);
+                        dp_diag<NB, T, true>(st, wt);
+                        dp_place<NB, T>(st, f);
+                    }
+                }
+                T H[Q][M];
+#pragma unroll
+                for (int i = Q - 1; i >= 0; --i) {
+                    dp_diag<NB, T, true>(st, wt);
+#pragma unroll
+                    for (int S2 = 0; S2 < M; ++S2) H[i][S2] = st[S2];
+                    if (i > 0) {
+                        slab_f<NB, S>(f, cur, lane, half * Q + i);
+                        dp_place<NB, T>(st, f);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < Q; ++i) {
+                    const int jx = half * Q + i;
+                    slab_f<NB, S>(f, cur, lane, jx);
+                    dp_diag<NB, T, true>(F, wt);
+                    dp_place<NB, T>(F, f);
+                    const T J = combine<NB, T>(F, H[i]);
+                    const double o = epilogue<NB, T, MODE>(J, cur, lane, jx, acc, bad);
+                    if (AV::kOut) obuf[lane * (S + 1) + jx] = o;
+                    if constexpr (NEXT) next_ops_step<NB, T>(Gn, Rn, wt, f, o, p);
+                }
+            }
+            __syncwarp();
+            if (AV::kOut) {
+                slab_store<S>(obuf, p.outk, chain0, cend, p.P, p.N, s, lane);
+                __syncwarp();
+            }
+        }
+        if (bad && live) raise_status(p, 6 /*EOVERFLOW*/);
+        if ((MODE == MODE_RES || MODE == MODE_COST) && live) p.partial[c] = acc;
+        if constexpr (NEXT) {
+            if (live) {
+                op_store<NB, T>(Gn, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ);
+                op_store<NB, T>(Rn, static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+            }
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(tmem_slot);
+}
+
 template <int NB, typename T>
 static size_t ops_smem() {
     return (size_t)kWarpsPerCta * 2 * NB * 32 * (slab_s(NB) + 1) * sizeof(double);
@@ -597,10 +827,32 @@ static void launch_apply_range(const Plan &p, int64_t cbeg, int64_t cend, cudaSt
 
 // Full chains through the predicate-free kernel, the ragged last chain (or every chain when
 // P is not a multiple of the slab length) through the general one.
+template <int NB, int MODE, bool NEXT>
+static void launch_apply_tm(const Plan &p, int64_t cbeg, int64_t cend, cudaStream_t s, int64_t *launches) {
+    if (cend <= cbeg) return;
+    const size_t sm = apply_smem<NB, MODE>();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_chunk_apply_tm<NB, MODE, NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr = true;
+    }
+    const int tpb = kWarpsPerCta * 32;
+    const int64_t nb = (cend - cbeg + tpb - 1) / tpb;
+    k_chunk_apply_tm<NB, MODE, NEXT><<<(unsigned)nb, tpb, sm, s>>>(p, cbeg, cend);
+    ++*launches;
+}
+
 template <int NB, typename T, int MODE, bool NEXT = false>
 static void launch_apply(const Plan &p, int64_t /*nb*/, int /*tpb*/, cudaStream_t s, int64_t *launches) {
     const bool full_ok = p.P % slab_s(NB) == 0;
     const int64_t nfull = full_ok ? p.N / p.P : 0;
+    if constexpr (NB <= 3 && sizeof(T) == sizeof(double)) {
+        if (p.P % (2 * sub_q(NB)) == 0 && p.P / (2 * sub_q(NB)) * 2 * (1 << NB) <= kTmemCols && !g_no_tmem) {
+            launch_apply_tm<NB, MODE, NEXT>(p, 0, nfull, s, launches);
+            launch_apply_range<NB, T, MODE, NEXT, false>(p, nfull, p.nchunks, s, launches);
+            return;
+        }
+    }
     launch_apply_range<NB, T, MODE, NEXT, true>(p, 0, nfull, s, launches);
     launch_apply_range<NB, T, MODE, NEXT, false>(p, nfull, p.nchunks, s, launches);
 }
