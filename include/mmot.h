@@ -72,11 +72,21 @@ typedef enum {
 /* Uniform grid x_i = x_min + i h, i = 0..N-1 (endpoints included, A1). */
 typedef struct { double x_min, x_max; } mmot_grid;
 
+/* Kernel family of the single-instance products.
+ *   AUTO: single-walk kernels when a chain of >= 64 points satisfies
+ *         P * max_a a(l-a) * h/eta <= 1 (large N, small h/eta: e.g. C4), else two-walk.
+ *   TWO_WALK: suffix states by a right-to-left walk with TMEM / local checkpoints (any eta).
+ *   SINGLE_WALK: suffix states walked forward through the inverse recurrence step (each grid
+ *         point read once); l <= 5.  Its rounding error grows like exp(P * max_a a(l-a) h/eta),
+ *         so outside the bound above the caller accepts the accuracy loss. */
+typedef enum { MMOT_KERNEL_AUTO = 0, MMOT_KERNEL_TWO_WALK = 1, MMOT_KERNEL_SINGLE_WALK = 2 } mmot_kernel;
+
 typedef struct {
     int check_every;    /* residual cadence in sweeps; 0 = only when tol > 0, every sweep (default) */
     int residual_mode;  /* 0 = paper: sum_{k<l} ||m_k - mu_k||_1 (Alg. 1 line 7, generalised) */
     mmot_repr repr;     /* representation of u[] (default MMOT_LOG) */
-    int chunk;          /* grid points per chunk; 0 = automatic */
+    int chunk;          /* grid points per chunk (chain); 0 = automatic */
+    mmot_kernel kernel; /* kernel family (default MMOT_KERNEL_AUTO) */
 } mmot_opts;
 
 typedef struct {
@@ -143,6 +153,10 @@ MMOT_API const char *mmot_last_error(const mmot_ctx *ctx);
 
 /* Library version as (major << 16 | minor). */
 MMOT_API int mmot_version(void);
+
+/* Launch plan of a context: grid points per chain P, number of chains, kernel family actually
+ * used (MMOT_KERNEL_TWO_WALK or MMOT_KERNEL_SINGLE_WALK).  Any output pointer may be NULL. */
+MMOT_API mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t *nchains, int *kernel);
 
 /* Kernel-launch counter: number of CUDA kernels this context has launched so far. */
 MMOT_API int64_t mmot_launch_count(const mmot_ctx *ctx);

@@ -41,7 +41,7 @@ class _Grid(ctypes.Structure):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("check_every", ctypes.c_int), ("residual_mode", ctypes.c_int),
-                ("repr", ctypes.c_int), ("chunk", ctypes.c_int)]
+                ("repr", ctypes.c_int), ("chunk", ctypes.c_int), ("kernel", ctypes.c_int)]
 
 
 class _Report(ctypes.Structure):
@@ -85,6 +85,9 @@ def load_library():
     lib.mmot_last_error.restype = ctypes.c_char_p
     lib.mmot_version.argtypes = []
     lib.mmot_version.restype = ctypes.c_int
+    lib.mmot_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                              ctypes.POINTER(ctypes.c_int)]
+    lib.mmot_info.restype = ctypes.c_int
     lib.mmot_launch_count.argtypes = [vp]
     lib.mmot_launch_count.restype = ctypes.c_int64
     lib.mmot_profile_enable.argtypes = [vp, ctypes.c_int]
@@ -118,7 +121,8 @@ class Context:
     """
 
     def __init__(self, l: int, N: int, eta: float, grid=(0.0, 1.0), dtype: str = "f64",
-                 repr: str = "log", check_every: int = 0, chunk: int = 0, stream=None):
+                 repr: str = "log", check_every: int = 0, chunk: int = 0, stream=None,
+                 kernel: str = "auto"):
         import torch
         self._lib = load_library()
         if not torch.cuda.is_available():
@@ -128,7 +132,8 @@ class Context:
         self.repr = repr
         self.h = (self.grid[1] - self.grid[0]) / (self.N - 1) if self.N > 1 else 1.0
         self.stream = stream if stream is not None else torch.cuda.current_stream()
-        opts = _Opts(int(check_every), 0, LOG if repr == "log" else LINEAR, int(chunk))
+        kern = {"auto": 0, "two_walk": 1, "single_walk": 2}[kernel]
+        opts = _Opts(int(check_every), 0, LOG if repr == "log" else LINEAR, int(chunk), kern)
         ctx = ctypes.c_void_p()
         st = self._lib.mmot_create(self.l, self.N, self.eta, _Grid(*self.grid), F64 if dtype == "f64" else F32,
                                    ctypes.byref(opts), ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx))
@@ -148,6 +153,13 @@ class Context:
             if not t.is_cuda or not t.is_contiguous() or t.numel() != self.N:
                 raise MMOTError(2, "vectors must be contiguous CUDA tensors of length N")
         return _ptr_array([t.data_ptr() for t in ts])
+
+    @property
+    def info(self) -> dict:
+        """Launch plan: chain length P, number of chains, kernel family ("two_walk"/"single_walk")."""
+        P, n, k = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+        self._check(self._lib.mmot_info(self._ctx, ctypes.byref(P), ctypes.byref(n), ctypes.byref(k)))
+        return dict(chain_len=P.value, nchains=n.value, kernel={1: "two_walk", 2: "single_walk"}[k.value])
 
     @property
     def launches(self) -> int:

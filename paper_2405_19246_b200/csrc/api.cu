@@ -41,7 +41,9 @@ struct mmot_ctx {
     double eta = 0, h = 0;
     mmot_grid grid{0, 1};
     mmot_dtype dt = MMOT_F64;
-    mmot_opts opts{0, 0, MMOT_LOG, 0};
+    mmot_opts opts{0, 0, MMOT_LOG, 0, MMOT_KERNEL_AUTO};
+    bool sw = false;
+    void *car_bi = nullptr;
     cudaStream_t stream = nullptr;
     int device = 0;
     mmot::Weights W{};
@@ -127,6 +129,14 @@ int mmot_version(void) { return (MMOT_VERSION_MAJOR << 16) | MMOT_VERSION_MINOR;
 
 int64_t mmot_launch_count(const mmot_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
+mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t *nchains, int *kernel) {
+    if (!ctx) { set_err(nullptr, "NULL context"); return MMOT_EINVAL; }
+    if (chain_len) *chain_len = ctx->P;
+    if (nchains) *nchains = ctx->nchunks;
+    if (kernel) *kernel = ctx->sw ? MMOT_KERNEL_SINGLE_WALK : MMOT_KERNEL_TWO_WALK;
+    return MMOT_OK;
+}
+
 void mmot_destroy(mmot_ctx *ctx) {
     if (!ctx) return;
     int cur = 0;
@@ -160,7 +170,8 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
         return MMOT_EINVAL;
     }
     if (dt != MMOT_F64 && dt != MMOT_F32) { set_err(nullptr, "bad dtype"); return MMOT_EINVAL; }
-    if (opts && (opts->check_every < 0 || opts->chunk < 0 || (opts->repr != MMOT_LOG && opts->repr != MMOT_LINEAR))) {
+    if (opts && (opts->check_every < 0 || opts->chunk < 0 || (opts->repr != MMOT_LOG && opts->repr != MMOT_LINEAR) ||
+                 opts->kernel < MMOT_KERNEL_AUTO || opts->kernel > MMOT_KERNEL_SINGLE_WALK)) {
         set_err(nullptr, "bad opts");
         return MMOT_EINVAL;
     }
@@ -186,15 +197,43 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
     const int NB = l - 1;
     const int64_t pmax = mmot::chunk_max(NB);
     const int q = mmot::sub_q(NB);
+    // Single-walk kernels (k_sw_apply): the suffix states are walked forward through the
+    // inverse step, whose error growth over a chain is bounded by (1/w_min)^P =
+    // exp(P * emax * h/eta), emax = max_a a(l-a).  Auto-selected when a chain of >= 64 points
+    // keeps that exponent <= kSwBound.
+    const double emax = (double)((l / 2) * ((l + 1) / 2));
+    const double hoe = c->h / eta;
+    const int slab = mmot::slab_s(NB);
     int64_t P;
-    if (c->opts.chunk > 0) {
-        P = std::min<int64_t>(c->opts.chunk, pmax);
-    } else {
-        const int64_t target = 148 * 256;
-        P = (N + target - 1) / target;
-        P = ((P + q - 1) / q) * q;
-        P = std::max<int64_t>(q, std::min<int64_t>(P, pmax));
+    bool sw = false;
+    if (c->opts.kernel == MMOT_KERNEL_SINGLE_WALK) {
+        sw = NB <= 4;
+        if (!sw) { set_err(nullptr, "single-walk kernels support l <= 5"); delete c; return MMOT_EUNSUPPORTED; }
     }
+    if (c->opts.chunk > 0) {
+        P = sw ? (int64_t)c->opts.chunk : std::min<int64_t>(c->opts.chunk, pmax);
+    } else {
+        // one chain per lane, 2 waves of (SMs x resident warps x 32 lanes)
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+        const int64_t target = (NB <= 4 ? (int64_t)nsm * mmot::sw_blocks_per_sm(NB) * mmot::kWarpsPerCtaHost * 32 * 2
+                                        : (int64_t)nsm * 8 * 32 * 2);
+        int64_t Psw = (N + target - 1) / target;
+        Psw = std::max<int64_t>(64, ((Psw + slab - 1) / slab) * slab);
+        const double capd = mmot::kSwBound / (emax * hoe);
+        const int64_t Pcap = capd > 1e15 ? (int64_t)1e15 : (int64_t)capd;
+        if (Psw > Pcap) Psw = (Pcap / slab) * slab;
+        if (c->opts.kernel == MMOT_KERNEL_AUTO && NB <= 4 && Psw >= 64 && N >= 64LL * 148 * 8 * 32) sw = true;
+        if (sw) {
+            P = std::max<int64_t>(slab, Psw);
+        } else {
+            const int64_t target2 = 148 * 256;
+            P = (N + target2 - 1) / target2;
+            P = ((P + q - 1) / q) * q;
+            P = std::max<int64_t>(q, std::min<int64_t>(P, pmax));
+        }
+    }
+    c->sw = sw;
     c->P = P;
     c->nchunks = (N + P - 1) / P;
     // levels of the hierarchical operator scan
@@ -219,6 +258,9 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
         total += 2 * (size_t)c->nlev_n[i] * carsz;
         total = (total + 255) & ~(size_t)255;
     }
+    const size_t off_bi = total;
+    total += (size_t)c->nchunks * carsz;
+    total = (total + 255) & ~(size_t)255;
     const size_t off_part = total;
     total += (size_t)c->nchunks * sizeof(double);
     total = (total + 255) & ~(size_t)255;
@@ -238,6 +280,7 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
         c->car_f[i] = base + off_car[i];
         c->car_b[i] = base + off_car[i] + (size_t)c->nlev_n[i] * carsz;
     }
+    c->car_bi = base + off_bi;
     c->partial = reinterpret_cast<double *>(base + off_part);
     c->dsc = reinterpret_cast<DevScalars *>(base + off_sc);
     if (c->opts.repr == MMOT_LOG) {
@@ -293,6 +336,8 @@ static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double
         p.car_f[i] = c->car_f[i];
         p.car_b[i] = c->car_b[i];
     }
+    p.car_bi = c->car_bi;
+    p.sw = c->sw ? 1 : 0;
     p.partial = c->partial;
     p.stop = &c->dsc->stop;
     p.status = &c->dsc->status;

@@ -107,6 +107,25 @@ __device__ __forceinline__ void dp_place(T (&st)[1 << NB], const double (&f)[NB 
     }
 }
 
+// Inverse of dp_place: st <- place_x^{-1}(st).  place_x = prod_q (I + phi_q[x] E_q) with
+// commuting nilpotent E_q (E_q^2 = 0), so place_x^{-1} = prod_q (I - phi_q[x] E_q).
+template <int NB, typename T>
+__device__ __forceinline__ void dp_unplace(T (&st)[1 << NB], const double (&f)[NB > 0 ? NB : 1]) {
+#pragma unroll
+    for (int b = NB - 1; b >= 0; --b) {
+#pragma unroll
+        for (int S = 0; S < (1 << NB); ++S)
+            if ((S >> b) & 1) st[S] = mads(-f[b], st[S ^ (1 << b)], st[S]);
+    }
+}
+
+// st[S] *= winv[|S|] for S != {} (winv[0] = 1/w_0 = 1).
+template <int NB, typename T>
+__device__ __forceinline__ void dp_diag_inv(T (&st)[1 << NB], const T *winv) {
+#pragma unroll
+    for (int S = 1; S < (1 << NB); ++S) st[S] = mul(winv[pc(S)], st[S]);
+}
+
 // Operator storage: G[c][S], c = 0..NB, S = 0..2^NB-1 (entries with pc(S) > NB-c unused).
 template <int NB>
 struct OpShape {
@@ -154,6 +173,66 @@ __device__ __forceinline__ void op_rstep(T (&G)[NB + 1][1 << NB], const T *wt, c
 #pragma unroll
         for (int V = 0; V < (1 << NB); ++V)
             if (pc(V) <= NB - c) G[c][V] = mul(wt[c], G[c][V]);
+}
+
+// ---------------------------------------------------------------------------------------
+// One walk for both chain operators (prefix/suffix duality).
+//
+// Let Gt_c be the chain DP from e_{} with weights w_{c+|V|}, WITHOUT the diag of its first
+// grid point (the edge entering the chain).  Then the prefix operator is G_c = w_c Gt_c and,
+// because the edge weight of a suffix walk counts the indices to the RIGHT of an edge
+// (|V| - #left) and w_a = w_{l-a}, the suffix operator is
+//     R_c[V] = w_c * Gt_{l-c-|V|}[V]                     (l = NB+1; Gt_l[{}] = 1)
+// (exact identity of the two sums; pinned by the GPU parity tests and DESIGN.md §1).
+// Gt is needed on the extended range c + |V| <= l, slices c = 0..NB: one walk of ~2/3 the
+// cost of op_step + op_rstep.
+// ---------------------------------------------------------------------------------------
+template <int NB, typename T>
+__device__ __forceinline__ void opx_identity(T (&G)[NB + 1][1 << NB]) {
+#pragma unroll
+    for (int c = 0; c <= NB; ++c)
+#pragma unroll
+        for (int S = 0; S < (1 << NB); ++S) G[c][S] = (S == 0) ? one_of(T{}) : zero_of(T{});
+}
+
+// wt[a] = w_a, a = 0..NB+1 (w_{NB+1} = w_l = 1 and w_0 = 1 are not multiplied).
+template <int NB, typename T>
+__device__ __forceinline__ void opx_step(T (&G)[NB + 1][1 << NB], const T *wt, const double (&f)[NB > 0 ? NB : 1],
+                                         bool skip_diag) {
+    constexpr int L = NB + 1;
+    if (!skip_diag) {
+#pragma unroll
+        for (int c = 0; c <= NB; ++c)
+#pragma unroll
+            for (int V = 0; V < (1 << NB); ++V) {
+                const int a = c + pc(V);
+                if (a < L && a > 0) G[c][V] = mul(wt[a], G[c][V]);
+            }
+    }
+#pragma unroll
+    for (int c = 0; c <= NB; ++c)
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int V = (1 << NB) - 1; V >= 0; --V)
+                if (((V >> b) & 1) && c + pc(V) <= L) G[c][V] = mads(f[b], G[c][V ^ (1 << b)], G[c][V]);
+}
+
+// Store the prefix operator (w_c Gt_c) and the suffix operator (w_c Gt_{l-c-|V|}) in op_store
+// layout.
+template <int NB, typename T>
+__device__ __forceinline__ void opx_store(const T (&G)[NB + 1][1 << NB], const T *wt, T *pf, T *pb) {
+    constexpr int M = 1 << NB;
+#pragma unroll
+    for (int c = 0; c <= NB; ++c)
+#pragma unroll
+        for (int V = 0; V < M; ++V)
+            if (c + pc(V) <= NB) {
+                const int cp = NB + 1 - c - pc(V);
+                pf[c * M + V] = c == 0 ? G[0][V] : mul(wt[c], G[c][V]);
+                const T r = cp > NB ? one_of(T{}) : G[cp][V];
+                pb[c * M + V] = c == 0 ? r : mul(wt[c], r);
+            }
 }
 
 // out = Op(in):  out[S] = sum_{U subset S} in[U] * G[|U|][S\U]

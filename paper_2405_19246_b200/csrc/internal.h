@@ -14,7 +14,8 @@ enum Mode : int {
     MODE_COST = 3,  // partial[c] = sum phi_k * hatJ_k (duals)   (W)
 };
 
-constexpr int kGroup = 32;      // operators composed per thread in the hierarchical scan
+constexpr int kGroup = 32;
+constexpr double kSwBound = 1.0;   // max P * max_a a(l-a) * h/eta for the single-walk kernels      // operators composed per thread in the hierarchical scan
 constexpr int kMaxLevels = 8;
 
 // Sub-block length Q (registers hold Q suffix states) and max sub-blocks per chunk
@@ -22,6 +23,7 @@ constexpr int kMaxLevels = 8;
 __host__ __device__ constexpr int sub_q(int NB) { return NB <= 2 ? 8 : (NB == 3 ? 4 : (NB == 4 ? 2 : 1)); }
 __host__ __device__ constexpr int nsub_max(int NB) { return 256 >> NB; }
 __host__ __device__ constexpr int chunk_max(int NB) { return sub_q(NB) * nsub_max(NB); }
+__host__ __device__ constexpr int slab_s(int NB) { return NB <= 2 ? 16 : 8; }
 
 struct Plan {
     int NB;                          // l - 1
@@ -35,6 +37,8 @@ struct Plan {
     int64_t nlev_n[kMaxLevels];      // entries per level (level 0 = chunks)
     void *ops_f[kMaxLevels], *ops_b[kMaxLevels];
     void *car_f[kMaxLevels], *car_b[kMaxLevels];
+    void *car_bi;                    // level 0: suffix state at the START of every chain (inclusive)
+    int sw;                          // 1: single-walk kernels (stable regime, see mmot_create)
     double *partial;                 // nchunks partial sums
     int *stop;                       // device flag: nonzero -> every kernel returns at once
     int *status;                     // device status (mmot_status) of the run
@@ -50,6 +54,10 @@ struct Plan {
 cudaError_t launch_product(const Plan &p, int mode, cudaStream_t s, int64_t *launches,
                            cudaEvent_t *ev = nullptr /* 4 events: before ops, after ops, after scan, after apply */,
                            bool with_ops = true, bool next = false);
+
+// Resident CTAs (of kWarpsPerCta warps) per SM of the single-walk update kernel.
+int sw_blocks_per_sm(int NB);
+constexpr int kWarpsPerCtaHost = 4;
 
 // Deterministic single-block sum of partial[0..n) -> *out = scale * sum (+ *out if accumulate).
 cudaError_t launch_sum(const double *partial, int64_t n, double *out, double scale, int accumulate,

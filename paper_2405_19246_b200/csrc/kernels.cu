@@ -46,7 +46,6 @@ __device__ __forceinline__ void load_f(double (&f)[NB > 0 ? NB : 1], const Plan 
 // the [32][S+1] tile (odd row pitch: conflict-free 8-byte reads).  Two buffers: the next
 // slab is in flight while the current one is consumed.
 // ---------------------------------------------------------------------------------------
-__host__ __device__ constexpr int slab_s(int NB) { return NB <= 2 ? 16 : 8; }
 
 __device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool valid) {
     const unsigned saddr = (unsigned)__cvta_generic_to_shared(sdst);
@@ -120,12 +119,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_ops(Plan p) {
     const int ns = (int)((p.P + S - 1) / S);
     T wt[NB + 2];
     load_weights<NB, T>(wt, p.W);
-    T G[NB + 1][M], R[NB + 1][M];
+    T G[NB + 1][M];
     double f[NB > 0 ? NB : 1];
-    // one left-to-right walk: prefix operator by left-multiplication, suffix operator by
-    // right-multiplication (op_rstep)
-    op_identity<NB, T>(G);
-    op_identity<NB, T>(R);
+    // one left-to-right walk of the extended operator; prefix and suffix operators follow from
+    // the duality R_c[V] = w_c Gt_{l-c-|V|}[V] (dp.cuh, opx_*)
+    opx_identity<NB, T>(G);
     slab_issue<S, NB>(buf, p.bound, chain0, p.P, p.N, 0, lane);
     cp_async_commit();
     for (int s = 0; s < ns; ++s) {
@@ -139,16 +137,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_ops(Plan p) {
             const int64_t x = x0 + (int64_t)s * S + j;
             if (x < x1) {
                 slab_f<NB, S>(f, cur, lane, j);
-                op_step<NB, T>(G, wt, f);
-                op_rstep<NB, T>(R, wt, f);
+                opx_step<NB, T>(G, wt, f, s == 0 && j == 0);
             }
         }
         __syncwarp();
     }
-    if (c < p.nchunks) {
-        op_store<NB, T>(G, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ);
-        op_store<NB, T>(R, static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
-    }
+    if (c < p.nchunks)
+        opx_store<NB, T>(G, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
+                         static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -196,7 +192,7 @@ __global__ void __launch_bounds__(64) k_ops_reduce(const T *in_f, const T *in_b,
 template <int NB, typename T>
 __global__ void __launch_bounds__(64) k_ops_down(const T *ops_f, const T *ops_b, const T *gcar_f,
                                                  const T *gcar_b, T *car_f, T *car_b, int64_t n_in,
-                                                 const int *stop) {
+                                                 const int *stop, T *car_bi) {
     constexpr int M = 1 << NB;
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int dir = blockIdx.y;
@@ -221,11 +217,12 @@ __global__ void __launch_bounds__(64) k_ops_down(const T *ops_f, const T *ops_b,
     } else {
         for (int64_t i = last; i >= first; --i) {
             vec_store<NB, T>(cur, car + i * M);
-            if (i == first) break;
+            if (i == first && !car_bi) break;
             op_load<NB, T>(G, ops + i * OpShape<NB>::SZ);
             op_apply<NB, T>(G, cur, nxt);
 #pragma unroll
             for (int S = 0; S < M; ++S) cur[S] = nxt[S];
+            if (car_bi) vec_store<NB, T>(cur, car_bi + i * M);  // inclusive: suffix state at chain start
         }
     }
 }
@@ -296,7 +293,7 @@ __global__ void __launch_bounds__(128) k_ops_reduce_w(const double *in_f, const 
 template <int NB>
 __global__ void __launch_bounds__(128) k_ops_down_w(const double *ops_f, const double *ops_b, const double *gcar_f,
                                                    const double *gcar_b, double *car_f, double *car_b, int64_t n_in,
-                                                   const int *stop) {
+                                                   const int *stop, double *car_bi) {
     constexpr int M = 1 << NB;
     constexpr int SZ = OpShape<NB>::SZ;
     __shared__ double smem[4][32 * (SZ + 1)];
@@ -334,6 +331,10 @@ __global__ void __launch_bounds__(128) k_ops_down_w(const double *ops_f, const d
         double *dst = (dir == 0 ? car_f : car_b) + i * M;
 #pragma unroll
         for (int S = 0; S < M; ++S) dst[S] = edge ? cin[S] : nb[S];
+        if (dir == 1 && car_bi) {
+#pragma unroll
+            for (int S = 0; S < M; ++S) car_bi[i * M + S] = out[S];  // inclusive: suffix state at chain start
+        }
     }
 }
 
@@ -447,6 +448,26 @@ __device__ __forceinline__ double div_nr(double mu, double j) {
     return fma(r, fma(-j, q, mu), q);
 }
 
+// mu / J with one Newton step on the reciprocal (relative error ~2^-46) and a residual
+// correction of the quotient, which squares that error: q' - mu/J = O(2^-92) + rounding.
+__device__ __forceinline__ double div_nr1(double mu, double j) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(j));
+    const double e = fma(-j, r, 1.0);
+    r = fma(r, e, r);
+    const double q = mu * r;
+    return fma(r, fma(-j, q, mu), q);
+}
+
+// Integer tests on the bit pattern (keep the FP64 pipe free).
+__device__ __forceinline__ bool finite_positive(double q) {  // 0 < q < inf
+    const unsigned long long b = (unsigned long long)__double_as_longlong(q);
+    return b != 0ull && b < 0x7ff0000000000000ull;
+}
+__device__ __forceinline__ bool nonzero(double q) {
+    return ((unsigned long long)__double_as_longlong(q) & 0x7fffffffffffffffull) != 0ull;
+}
+
 // Combine J[m] = sum_S F_m[S] H_m[S^c] with two independent accumulators.
 template <int NB, typename T>
 __device__ __forceinline__ T combine(const T (&F)[1 << NB], const T (&H)[1 << NB]) {
@@ -471,9 +492,9 @@ __device__ __forceinline__ double epilogue(const T &J, const double *cur, int la
         return cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * jv;
     } else if (MODE == MODE_UPD) {
         const double mu = cur[(AV::IMU * 32 + lane) * (S + 1) + jx];
-        const double q = div_nr(mu, jv);
-        const bool nz = mu != 0.0;
-        bad |= nz && !(jv > 0.0 && jv <= 1.7976931348623157e308 && q <= 1.7976931348623157e308);
+        const double q = div_nr1(mu, jv);
+        const bool nz = nonzero(mu);
+        bad |= nz && !finite_positive(q);  // J = 0 / inf / NaN or mu/J out of range
         return nz ? q : 0.0;
     } else if (MODE == MODE_RES) {
         acc += fabs(cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * jv - cur[(AV::IMU * 32 + lane) * (S + 1) + jx]);
@@ -485,15 +506,15 @@ __device__ __forceinline__ double epilogue(const T &J, const double *cur, int la
     }
 }
 
-// Next-update operator step (fused): the bound values of update k+1 at this point.
+// Next-update operator step (fused): the bound values of update k+1 at this point, cyclic bound
+// order (see make_plan); one extended operator walk gives both scan directions (dp.cuh opx_*).
 template <int NB, typename T>
-__device__ __forceinline__ void next_ops_step(T (&Gn)[NB + 1][1 << NB], T (&Rn)[NB + 1][1 << NB], const T *wt,
-                                              const double (&f)[NB > 0 ? NB : 1], double phi, const Plan &p) {
+__device__ __forceinline__ void next_ops_step(T (&Gx)[NB + 1][1 << NB], const T *wt, const double (&f)[NB > 0 ? NB : 1],
+                                              double phi, bool first) {
     double fn[NB > 0 ? NB : 1];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) fn[b] = b + 1 < NB ? f[b + 1] : phi;  // cyclic bound order (see make_plan)
-    op_step<NB, T>(Gn, wt, fn);
-    op_rstep<NB, T>(Rn, wt, fn);
+    for (int b = 0; b < NB; ++b) fn[b] = b + 1 < NB ? f[b + 1] : phi;
+    opx_step<NB, T>(Gx, wt, fn, first);
 }
 
 // FULL = every live lane owns a complete chain of P points (P % S == 0): no per-point bounds
@@ -536,11 +557,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64
         vec_unit<NB, T>(st);
     }
     double f[NB > 0 ? NB : 1];
-    T Gn[NEXT ? NB + 1 : 1][NEXT ? M : 1], Rn[NEXT ? NB + 1 : 1][NEXT ? M : 1];
-    if constexpr (NEXT) {
-        op_identity<NB, T>(Gn);
-        op_identity<NB, T>(Rn);
-    }
+    T Gx[NEXT ? NB + 1 : 1][NEXT ? M : 1];
+    if constexpr (NEXT) opx_identity<NB, T>(Gx);
     // ---- walk 1 (right to left): suffix states, checkpoint ck[j] = B at min(x0+(j+1)Q, x1) ----
     T ck[NSUB][M];
     if (FULL) {
@@ -631,7 +649,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64
                         const T J = combine<NB, T>(F, H[i]);
                         const double o = epilogue<NB, T, MODE>(J, cur, lane, jx, acc, bad);
                         if (AV::kOut) obuf[lane * (S + 1) + jx] = o;
-                        if constexpr (NEXT) next_ops_step<NB, T>(Gn, Rn, wt, f, o, p);
+                        if constexpr (NEXT) next_ops_step<NB, T>(Gx, wt, f, o, s == 0 && jb == 0 && i == 0);
                     }
                 }
             }
@@ -646,8 +664,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64
     if ((MODE == MODE_RES || MODE == MODE_COST) && live) p.partial[c] = acc;
     if constexpr (NEXT) {
         if (live) {
-            op_store<NB, T>(Gn, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ);
-            op_store<NB, T>(Rn, static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+            opx_store<NB, T>(Gx, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
+                             static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
         }
     }
 }
@@ -700,11 +718,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply_tm(Plan p, in
             vec_unit<NB, T>(st);
         }
         double f[NB > 0 ? NB : 1];
-        T Gn[NEXT ? NB + 1 : 1][NEXT ? M : 1], Rn[NEXT ? NB + 1 : 1][NEXT ? M : 1];
-        if constexpr (NEXT) {
-            op_identity<NB, T>(Gn);
-            op_identity<NB, T>(Rn);
-        }
+        T Gx[NEXT ? NB + 1 : 1][NEXT ? M : 1];
+        if constexpr (NEXT) opx_identity<NB, T>(Gx);
         // ---- walk 1: right to left, checkpoint B at every block end into TMEM ----
         slab_issue<S, NB>(buf, vecs, chain0, p.P, p.N, ns - 1, lane);
         cp_async_commit();
@@ -776,7 +791,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply_tm(Plan p, in
                     const T J = combine<NB, T>(F, H[i]);
                     const double o = epilogue<NB, T, MODE>(J, cur, lane, jx, acc, bad);
                     if (AV::kOut) obuf[lane * (S + 1) + jx] = o;
-                    if constexpr (NEXT) next_ops_step<NB, T>(Gn, Rn, wt, f, o, p);
+                    if constexpr (NEXT) next_ops_step<NB, T>(Gx, wt, f, o, s == 0 && half == 0 && i == 0);
                 }
             }
             __syncwarp();
@@ -789,8 +804,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply_tm(Plan p, in
         if ((MODE == MODE_RES || MODE == MODE_COST) && live) p.partial[c] = acc;
         if constexpr (NEXT) {
             if (live) {
-                op_store<NB, T>(Gn, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ);
-                op_store<NB, T>(Rn, static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+                opx_store<NB, T>(Gx, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
+                                 static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
             }
         }
     }
@@ -798,6 +813,124 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply_tm(Plan p, in
     __syncthreads();
     tmem_fence_after();
     if (warp == 0) tmem_dealloc(tmem_slot);
+}
+
+// ---------------------------------------------------------------------------------------
+// Single-walk apply (stable regime: P * max_a a(l-a) * h/eta <= kSwBound, see mmot_create).
+// Every chain is walked ONCE, left to right; each grid point is read from HBM once.
+//   prefix:  F_m = place_m(D F_{m-1})                         (exact carry F_{x0-1} from the scan)
+//   suffix:  U_m = place_m^{-1}(B_m) = D B_{m+1},  B_{m+1} = D^{-1} U_m
+//            (exact inclusive carry B_{x0} from the scan; the inverse step is well conditioned
+//             because D^{-1} = diag(w^{-1}) grows by at most e^{kSwBound} over a chain)
+//   combine: J[m] = sum_S F_m[S] w_{|S|+1} B_{m+1}[S^c] = sum_S F_m[S] U_m[S^c]   (w_a = w_{l-a})
+// The next update's chain operators come from ONE extended walk (opx_step, prefix/suffix
+// duality in dp.cuh).
+// ---------------------------------------------------------------------------------------
+template <int NB, typename T>
+__device__ __forceinline__ void load_winv(T (&wi)[NB + 2], const Weights &W) {
+#pragma unroll
+    for (int a = 0; a <= NB + 1; ++a) {
+        double v;
+        load_weight(v, W, a);
+        const double r = 1.0 / v;
+        if constexpr (sizeof(T) == sizeof(double)) {
+            reinterpret_cast<double &>(wi[a]) = r;
+        } else {
+            // d(1/w)/dlog(lambda) = -e_a / w_a
+            reinterpret_cast<Dual &>(wi[a]) = Dual{r, -W.e[a] * r};
+        }
+    }
+}
+
+// Per-warp body; FULL = all 32 chains of the warp are complete and P % S == 0 (no predicates).
+// The output slab is written into the consumed slot of the input tile (mu_k for updates, phi_k
+// for marginals), so a warp needs 2 * NV tiles of shared memory and 3 CTAs fit per SM.
+template <int NB, typename T, int MODE, bool NEXT, bool FULL>
+__device__ __forceinline__ void sw_body(const Plan &p, int64_t chain0, int64_t cend, double *buf, int lane) {
+    using AV = ApplyVecs<NB, MODE>;
+    constexpr int M = 1 << NB;
+    constexpr int S = slab_s(NB);
+    constexpr int TILE = 32 * (S + 1);
+    constexpr int NV = AV::NV;
+    constexpr int OSLOT = MODE == MODE_UPD ? AV::IMU : AV::IPHI;
+    const int64_t c = chain0 + lane;
+    const bool live = FULL || c < cend;
+    const int64_t x0 = c * p.P;
+    const int64_t x1 = FULL ? x0 + p.P : min(p.N, x0 + p.P);
+    const int ns = (int)((p.P + S - 1) / S);
+    const double *vecs[NV];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) vecs[b] = p.bound[b];
+    if (AV::kMu) vecs[AV::IMU] = p.muk;
+    if (AV::kPhi) vecs[AV::IPHI] = p.phik;
+    T wt[NB + 2], wi[NB + 2];
+    load_weights<NB, T>(wt, p.W);
+    load_winv<NB, T>(wi, p.W);
+    T F[M], B[M];
+    if (live) {
+        vec_load<NB, T>(F, static_cast<const T *>(p.car_f[0]) + c * M);
+        vec_load<NB, T>(B, static_cast<const T *>(p.car_bi) + c * M);
+    } else {
+        vec_unit<NB, T>(F);
+        vec_unit<NB, T>(B);
+    }
+    double f[NB > 0 ? NB : 1];
+    T Gx[NEXT ? NB + 1 : 1][NEXT ? M : 1];
+    if constexpr (NEXT) opx_identity<NB, T>(Gx);
+    double acc = 0.0;
+    bool bad = false;
+    slab_issue<S, NV>(buf, vecs, chain0, p.P, p.N, 0, lane);
+    cp_async_commit();
+#pragma unroll 1
+    for (int s = 0; s < ns; ++s) {
+        if (s + 1 < ns) slab_issue<S, NV>(buf + ((s + 1) & 1) * NV * TILE, vecs, chain0, p.P, p.N, s + 1, lane);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        double *cur = buf + (s & 1) * NV * TILE;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            const int64_t x = x0 + (int64_t)s * S + j;
+            if (FULL || x < x1) {
+                slab_f<NB, S>(f, cur, lane, j);
+                dp_diag<NB, T, true>(F, wt);
+                dp_place<NB, T>(F, f);
+                dp_unplace<NB, T>(B, f);          // B := U_m = D B_{m+1}
+                const T J = combine<NB, T>(F, B);
+                dp_diag_inv<NB, T>(B, wi);        // B := B_{m+1}
+                const double o = epilogue<NB, T, MODE>(J, cur, lane, j, acc, bad);
+                if (AV::kOut) cur[(OSLOT * 32 + lane) * (S + 1) + j] = o;
+                if constexpr (NEXT) next_ops_step<NB, T>(Gx, wt, f, o, j == 0 && s == 0);
+            }
+        }
+        __syncwarp();
+        if (AV::kOut) {
+            slab_store<S>(cur + OSLOT * TILE, p.outk, chain0, cend, p.P, p.N, s, lane);
+            __syncwarp();
+        }
+    }
+    if (bad && live) raise_status(p, 6 /*EOVERFLOW*/);
+    if ((MODE == MODE_RES || MODE == MODE_COST) && live) p.partial[c] = acc;
+    if constexpr (NEXT) {
+        if (live)
+            opx_store<NB, T>(Gx, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
+                             static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+    }
+}
+
+// Chains [0, nfull) are complete (and P % S == 0 when nfull > 0); the warp holding the ragged
+// last chain takes the predicated body inside the same launch.
+template <int NB, typename T, int MODE, bool NEXT>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply(Plan p, int64_t nfull) {
+    using AV = ApplyVecs<NB, MODE>;
+    constexpr int TILE = 32 * (slab_s(NB) + 1);
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t chain0 = ((int64_t)blockIdx.x * kWarpsPerCta + warp) * 32;
+    if (chain0 >= p.nchunks || *(volatile int *)p.stop) return;
+    double *buf = smem + (size_t)warp * 2 * AV::NV * TILE;
+    if (chain0 + 32 <= nfull) sw_body<NB, T, MODE, NEXT, true>(p, chain0, p.nchunks, buf, lane);
+    else sw_body<NB, T, MODE, NEXT, false>(p, chain0, p.nchunks, buf, lane);
 }
 
 template <int NB, typename T>
@@ -842,10 +975,48 @@ static void launch_apply_tm(const Plan &p, int64_t cbeg, int64_t cend, cudaStrea
     ++*launches;
 }
 
+template <int NB, typename T, int MODE, bool NEXT>
+static void launch_sw(const Plan &p, int64_t nfull, cudaStream_t s, int64_t *launches) {
+    const size_t sm = (size_t)kWarpsPerCta * 2 * ApplyVecs<NB, MODE>::NV * 32 * (slab_s(NB) + 1) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_sw_apply<NB, T, MODE, NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr = true;
+    }
+    const int tpb = kWarpsPerCta * 32;
+    const int64_t nb = (p.nchunks + tpb - 1) / tpb;
+    k_sw_apply<NB, T, MODE, NEXT><<<(unsigned)nb, tpb, sm, s>>>(p, nfull);
+    ++*launches;
+}
+
+// Resident CTAs per SM of the single-walk update kernel (sizes the chain length in mmot_create).
+int sw_blocks_per_sm(int NB) {
+    int n = 0;
+    const int tpb = kWarpsPerCta * 32;
+    auto q = [&](auto kern, int nv, int S) {
+        const size_t sm = (size_t)kWarpsPerCta * 2 * nv * 32 * (S + 1) * sizeof(double);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, tpb, sm);
+    };
+    switch (NB) {
+        case 1: q(k_sw_apply<1, double, MODE_UPD, true>, 2, slab_s(1)); break;
+        case 2: q(k_sw_apply<2, double, MODE_UPD, true>, 3, slab_s(2)); break;
+        case 3: q(k_sw_apply<3, double, MODE_UPD, true>, 4, slab_s(3)); break;
+        case 4: q(k_sw_apply<4, double, MODE_UPD, true>, 5, slab_s(4)); break;
+        default: n = 0;
+    }
+    cudaGetLastError();
+    return n > 0 ? n : 2;
+}
+
 template <int NB, typename T, int MODE, bool NEXT = false>
 static void launch_apply(const Plan &p, int64_t /*nb*/, int /*tpb*/, cudaStream_t s, int64_t *launches) {
     const bool full_ok = p.P % slab_s(NB) == 0;
     const int64_t nfull = full_ok ? p.N / p.P : 0;
+    if (p.sw) {
+        if constexpr (NB <= 4) launch_sw<NB, T, MODE, NEXT>(p, nfull, s, launches);
+        return;
+    }
     if constexpr (NB <= 3 && sizeof(T) == sizeof(double)) {
         if (p.P % (2 * sub_q(NB)) == 0 && p.P / (2 * sub_q(NB)) * 2 * (1 << NB) <= kTmemCols && !g_no_tmem) {
             launch_apply_tm<NB, MODE, NEXT>(p, 0, nfull, s, launches);
@@ -907,13 +1078,14 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
                                                     reinterpret_cast<const double *>(gf),
                                                     reinterpret_cast<const double *>(gb),
                                                     static_cast<double *>(p.car_f[i]), static_cast<double *>(p.car_b[i]),
-                                                    p.nlev_n[i], p.stop);
+                                                    p.nlev_n[i], p.stop,
+                                                    i == 0 && p.sw ? static_cast<double *>(p.car_bi) : nullptr);
             ++*launches;
             continue;
         }
         k_ops_down<NB, T><<<grid, 64, 0, s>>>(static_cast<const T *>(p.ops_f[i]), static_cast<const T *>(p.ops_b[i]),
                                              gf, gb, static_cast<T *>(p.car_f[i]), static_cast<T *>(p.car_b[i]),
-                                             p.nlev_n[i], p.stop);
+                                             p.nlev_n[i], p.stop, i == 0 && p.sw ? static_cast<T *>(p.car_bi) : nullptr);
         ++*launches;
     }
     if (ev) cudaEventRecord(ev[2], s);

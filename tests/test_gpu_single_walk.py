@@ -1,0 +1,113 @@
+"""GPU parity of the single-walk kernels (k_sw_apply: suffix states walked forward through the
+inverse recurrence step, one extended operator walk for both scan directions) against the fp64
+CPU oracle (oracle/regions.c, §4.2 region chains).
+
+The single-walk family is selected automatically for large N at small h/eta (C4); here it is
+forced (kernel="single_walk") at small sizes inside its stability bound
+P * max_a a(l-a) * h/eta <= 1, with chain lengths that leave ragged tails,
+chains shorter than a slab, and thousands of chains (3-4 scan levels).
+Tolerance: north_star fp64, 1e-10 relative (elementwise for products, L1 for Sinkhorn).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import mmot_inputs  # noqa: E402
+import paper_2405_19246_b200 as mm  # noqa: E402
+from oracle import regions, sinkhorn as osk  # noqa: E402
+
+DEV = "cuda:0"
+RTOL = 1e-10
+
+
+def _dev(vs):
+    return [torch.from_numpy(np.ascontiguousarray(v)).to(DEV) for v in vs]
+
+
+def _emax(l):
+    return (l // 2) * ((l + 1) // 2)
+
+
+def _eta_for(l, N, chunk, frac=0.9):
+    """Largest h/eta inside the stability bound for this chain length (times frac)."""
+    h = mmot_inputs.grid_h(N)
+    return h / (frac / (chunk * _emax(l)))
+
+
+def _oracle_marginals(phis, h, eta):
+    l = len(phis)
+    w = regions.edge_weights(l, h, eta)
+    return [phis[k] * regions.marginal_product(list(phis), k, w) for k in range(l)]
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+@pytest.mark.parametrize("l", [2, 3, 4, 5])
+@pytest.mark.parametrize("N,chunk", [(1, 8), (7, 8), (64, 8), (1000, 13), (4097, 64), (20000, 8), (20001, 100)])
+def test_single_walk_marginal_parity(l, N, chunk):
+    phis = mmot_inputs.random_positive(4000 + 10 * l + N, l, N)
+    h = mmot_inputs.grid_h(N)
+    eta = _eta_for(l, N, chunk)
+    ctx = mm.Context(l, N, eta, repr="linear", chunk=chunk, kernel="single_walk")
+    assert ctx.info["kernel"] == "single_walk"
+    u = _dev(phis)
+    got = [ctx.marginal(k, u).cpu().numpy() for k in range(l)]
+    ctx.close()
+    want = _oracle_marginals(phis, h, eta)
+    for k in range(l):
+        assert _rel(got[k], want[k]) <= RTOL, (l, N, chunk, k)
+
+
+@pytest.mark.parametrize("l", [3, 4])
+def test_single_walk_cost_parity(l):
+    N, chunk = 5000, 40
+    h = mmot_inputs.grid_h(N)
+    eta = _eta_for(l, N, chunk)
+    phis = mmot_inputs.random_positive(500 + l, l, N)
+    ctx = mm.Context(l, N, eta, repr="linear", chunk=chunk, kernel="single_walk")
+    W = ctx.cost(_dev(phis))
+    ctx.close()
+    w = regions.edge_weights(l, h, eta)
+    _, jh = regions.marginal_product(list(phis), l - 1, w, want_hat=True)
+    W_ref = h * float(np.dot(phis[l - 1], jh))
+    assert abs(W - W_ref) <= RTOL * abs(W_ref)
+
+
+@pytest.mark.parametrize("l,N,chunk,T", [(2, 3000, 16, 6), (3, 5000, 24, 5), (4, 20000, 64, 4), (5, 3000, 16, 3)])
+def test_single_walk_sinkhorn_lockstep(l, N, chunk, T):
+    """Fused updates: phi_k <- mu_k / J_k with the next update's operators built in the same walk."""
+    h = mmot_inputs.grid_h(N)
+    eta = _eta_for(l, N, chunk)
+    mus = np.stack(mmot_inputs.random_marginals(600 + l, l, N))
+    ctx = mm.Context(l, N, eta, repr="log", chunk=chunk, kernel="single_walk")
+    u = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in range(l)]
+    ctx.init_uniform(u)
+    rep = ctx.sinkhorn(_dev(mus), T, 0.0, u)
+    assert rep["status"] == 0 and rep["iters_done"] == T
+    marg = np.stack([ctx.marginal(k, u).cpu().numpy() for k in range(l)])
+    g = np.stack([x.cpu().numpy() for x in u])
+    ctx.close()
+    g_ref, _, _ = osk.sinkhorn(mus, h, eta, T, domain="plain")
+    g_ref = np.log(g_ref)
+    m_ref = osk.marginals(np.exp(g_ref), h, eta)
+    for k in range(l):
+        assert np.abs(marg[k] - m_ref[k]).sum() / np.abs(m_ref[k]).sum() <= RTOL, k
+    assert np.max(np.abs(g - g_ref)) <= 1e-9
+
+
+def test_auto_selects_single_walk_for_c4_shape():
+    cfg = mmot_inputs.CONFIGS["C4"]
+    ctx = mm.Context(cfg.l, cfg.N, cfg.eta)
+    info = ctx.info
+    ctx.close()
+    h = mmot_inputs.grid_h(cfg.N)
+    assert info["kernel"] == "single_walk"
+    assert info["chain_len"] * _emax(cfg.l) * h / cfg.eta <= 1.0
+    small = mm.Context(4, 1000, 0.01)
+    assert small.info["kernel"] == "two_walk"
+    small.close()
