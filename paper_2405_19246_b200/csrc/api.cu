@@ -56,7 +56,10 @@ struct mmot_ctx {
     double *partial = nullptr;
     DevScalars *dsc = nullptr;
     DevScalars *hsc = nullptr;  // pinned host mirror
-    double *lin[mmot::kMaxL] = {nullptr};  // internal linear scalings (MMOT_LOG repr)
+    double *lin[mmot::kMaxL] = {nullptr};  // internal linear scalings (MMOT_LOG repr, or any repr when sw)
+    int64_t nchp = 0;                       // sw: chains rounded up to 32 (transposed row length)
+    double *mu_t[mmot::kMaxL] = {nullptr};  // sw: marginals in the chain-transposed layout
+    double *out_t = nullptr;                // sw: marginal output in the chain-transposed layout
     double *stage_mu[mmot::kMaxL] = {nullptr};
     double *stage_u[mmot::kMaxL] = {nullptr};
     int *hstop = nullptr;       // pinned, async stop polling
@@ -145,8 +148,10 @@ void mmot_destroy(mmot_ctx *ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     else cudaDeviceSynchronize();
     cudaFree(ctx->ws);
+    cudaFree(ctx->out_t);
     for (int q = 0; q < mmot::kMaxL; ++q) {
         cudaFree(ctx->lin[q]);
+        cudaFree(ctx->mu_t[q]);
         cudaFree(ctx->stage_mu[q]);
         cudaFree(ctx->stage_u[q]);
     }
@@ -203,7 +208,7 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
     // keeps that exponent <= kSwBound.
     const double emax = (double)((l / 2) * ((l + 1) / 2));
     const double hoe = c->h / eta;
-    const int slab = mmot::slab_s(NB);
+    const int slab = mmot::kSwSlab;
     int64_t P;
     bool sw = false;
     if (c->opts.kernel == MMOT_KERNEL_SINGLE_WALK) {
@@ -211,7 +216,8 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
         if (!sw) { set_err(nullptr, "single-walk kernels support l <= 5"); delete c; return MMOT_EUNSUPPORTED; }
     }
     if (c->opts.chunk > 0) {
-        P = sw ? (int64_t)c->opts.chunk : std::min<int64_t>(c->opts.chunk, pmax);
+        P = sw ? ((int64_t)c->opts.chunk + mmot::kSwSlab - 1) / mmot::kSwSlab * mmot::kSwSlab
+               : std::min<int64_t>(c->opts.chunk, pmax);
     } else {
         // one chain per lane, 2 waves of (SMs x resident warps x 32 lanes)
         int nsm = 148;
@@ -283,7 +289,23 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
     c->car_bi = base + off_bi;
     c->partial = reinterpret_cast<double *>(base + off_part);
     c->dsc = reinterpret_cast<DevScalars *>(base + off_sc);
-    if (c->opts.repr == MMOT_LOG) {
+    c->nchp = (c->nchunks + 31) / 32 * 32;
+    if (c->sw) {
+        // chain-transposed internal vectors; zero-filled once so the tail of the last chain
+        // (points >= N) holds phi = mu = 0 for the whole life of the context
+        const size_t tb = (size_t)c->nchp * (size_t)c->P * sizeof(double);
+        bool ok = cudaMalloc(&c->out_t, tb) == cudaSuccess && cudaMemsetAsync(c->out_t, 0, tb, c->stream) == cudaSuccess;
+        for (int qq = 0; qq < l && ok; ++qq)
+            ok = cudaMalloc(&c->lin[qq], tb) == cudaSuccess && cudaMalloc(&c->mu_t[qq], tb) == cudaSuccess &&
+                 cudaMemsetAsync(c->lin[qq], 0, tb, c->stream) == cudaSuccess &&
+                 cudaMemsetAsync(c->mu_t[qq], 0, tb, c->stream) == cudaSuccess;
+        if (!ok) {
+            set_err(c, "cudaMalloc of the transposed vectors (%zu B each) failed", tb);
+            snprintf(g_err, sizeof g_err, "%s", c->err);
+            mmot_destroy(c);
+            return MMOT_ENOMEM;
+        }
+    } else if (c->opts.repr == MMOT_LOG) {
         for (int qq = 0; qq < l; ++qq) {
             e = cudaMalloc(&c->lin[qq], (size_t)N * sizeof(double));
             if (e != cudaSuccess) {
@@ -338,6 +360,8 @@ static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double
     }
     p.car_bi = c->car_bi;
     p.sw = c->sw ? 1 : 0;
+    p.nchp = c->nchp;
+    if (c->sw && mu) p.muk = c->mu_t[k];
     p.partial = c->partial;
     p.stop = &c->dsc->stop;
     p.status = &c->dsc->status;
@@ -355,7 +379,11 @@ static mmot_status reset_scalars(mmot_ctx *c) {
 static mmot_status to_linear(mmot_ctx *c, const void *const *u, const double **lin) {
     for (int q = 0; q < c->l; ++q) {
         if (!u[q]) { set_err(c, "u[%d] is NULL", q); return MMOT_EINVAL; }
-        if (c->opts.repr == MMOT_LOG) {
+        if (c->sw) {
+            CK(c, mmot::launch_to_t(static_cast<const double *>(u[q]), c->lin[q], c->N, c->P, c->nchunks, c->nchp,
+                                    c->opts.repr == MMOT_LOG ? 1 : 0, c->stream, &c->launches));
+            lin[q] = c->lin[q];
+        } else if (c->opts.repr == MMOT_LOG) {
             CK(c, mmot::launch_exp(static_cast<const double *>(u[q]), c->lin[q], c->N, c->stream, &c->launches));
             lin[q] = c->lin[q];
         } else {
@@ -387,7 +415,12 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
     // working scalings
     double *lin[mmot::kMaxL];
     for (int q = 0; q < l; ++q) {
-        if (c->opts.repr == MMOT_LOG) {
+        if (c->sw) {
+            CK(c, mmot::launch_to_t(static_cast<const double *>(u[q]), c->lin[q], c->N, c->P, c->nchunks, c->nchp,
+                                    c->opts.repr == MMOT_LOG ? 1 : 0, c->stream, &c->launches));
+            CK(c, mmot::launch_to_t(mu[q], c->mu_t[q], c->N, c->P, c->nchunks, c->nchp, 0, c->stream, &c->launches));
+            lin[q] = c->lin[q];
+        } else if (c->opts.repr == MMOT_LOG) {
             CK(c, mmot::launch_exp(static_cast<const double *>(u[q]), c->lin[q], c->N, c->stream, &c->launches));
             lin[q] = c->lin[q];
         } else {
@@ -430,9 +463,14 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
             poll_pending = true;
         }
     }
-    if (c->opts.repr == MMOT_LOG)
+    if (c->sw) {
+        for (int q = 0; q < l; ++q)
+            CK(c, mmot::launch_from_t(c->lin[q], static_cast<double *>(u[q]), c->N, c->P, c->nchunks, c->nchp,
+                                      c->opts.repr == MMOT_LOG ? 2 : 0, c->stream, &c->launches));
+    } else if (c->opts.repr == MMOT_LOG) {
         for (int q = 0; q < l; ++q)
             CK(c, mmot::launch_log(c->lin[q], static_cast<double *>(u[q]), c->N, c->stream, &c->launches));
+    }
     st = sync_report(c);
     if (st) return st;
     const DevScalars &h = *c->hsc;
@@ -458,8 +496,11 @@ mmot_status mmot_marginal(mmot_ctx *c, int k, const void *const *u, void *out) {
     const double *lin[mmot::kMaxL];
     st = to_linear(c, u, lin);
     if (st) return st;
-    Plan p = make_plan(c, k, lin, nullptr, static_cast<double *>(out), 0);
+    Plan p = make_plan(c, k, lin, nullptr, c->sw ? c->out_t : static_cast<double *>(out), 0);
     CK(c, mmot::launch_product(p, mmot::MODE_MARG, c->stream, &c->launches, prof_events(c, mmot::MODE_MARG)));
+    if (c->sw)
+        CK(c, mmot::launch_from_t(c->out_t, static_cast<double *>(out), c->N, c->P, c->nchunks, c->nchp, 0, c->stream,
+                                  &c->launches));
     return MMOT_OK;
 }
 

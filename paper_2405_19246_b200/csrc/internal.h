@@ -38,7 +38,9 @@ struct Plan {
     void *ops_f[kMaxLevels], *ops_b[kMaxLevels];
     void *car_f[kMaxLevels], *car_b[kMaxLevels];
     void *car_bi;                    // level 0: suffix state at the START of every chain (inclusive)
-    int sw;                          // 1: single-walk kernels (stable regime, see mmot_create)
+    int sw;                          // 1: single-walk kernels (stable regime, see mmot_create); vectors are
+                                     //    then in the chain-blocked layout ((c/32)*32P + t*32 + c%32)
+    int64_t nchp;                    // chain count rounded up to 32 (transposed row length)
     double *partial;                 // nchunks partial sums
     int *stop;                       // device flag: nonzero -> every kernel returns at once
     int *status;                     // device status (mmot_status) of the run
@@ -62,6 +64,13 @@ constexpr int kWarpsPerCtaHost = 4;
 // Deterministic single-block sum of partial[0..n) -> *out = scale * sum (+ *out if accumulate).
 cudaError_t launch_sum(const double *partial, int64_t n, double *out, double scale, int accumulate,
                        const int *stop, cudaStream_t s, int64_t *launches);
+
+// Natural <-> chain-blocked layout (x = c*P + t <-> (c/32)*32P + t*32 + c%32); op 0 copy, 1 exp, 2 log.
+cudaError_t launch_to_t(const double *src, double *dst, int64_t N, int64_t P, int64_t nchains, int64_t nchp, int op,
+                        cudaStream_t s, int64_t *launches);
+cudaError_t launch_from_t(const double *src, double *dst, int64_t N, int64_t P, int64_t nchains, int64_t nchp, int op,
+                          cudaStream_t s, int64_t *launches);
+constexpr int kSwSlab = 8;  // chain length of single-walk contexts is a multiple of this
 
 // Elementwise helpers.
 cudaError_t launch_exp(const double *in, double *out, int64_t n, cudaStream_t s, int64_t *launches);

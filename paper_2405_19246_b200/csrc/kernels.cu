@@ -842,22 +842,79 @@ __device__ __forceinline__ void load_winv(T (&wi)[NB + 2], const Weights &W) {
     }
 }
 
-// Per-warp body; FULL = all 32 chains of the warp are complete and P % S == 0 (no predicates).
-// The output slab is written into the consumed slot of the input tile (mu_k for updates, phi_k
-// for marginals), so a warp needs 2 * NV tiles of shared memory and 3 CTAs fit per SM.
-template <int NB, typename T, int MODE, bool NEXT, bool FULL>
-__device__ __forceinline__ void sw_body(const Plan &p, int64_t chain0, int64_t cend, double *buf, int lane) {
+// ---------------------------------------------------------------------------------------
+// Chain-blocked transposed layout (single-walk contexts).  Chains are grouped by 32 (one warp);
+// element (chain c, offset t) lives at (c/32)*32P + t*32 + c%32.  A warp's slab (S offsets of one
+// vector for its 32 chains) is then S*256 contiguous bytes: ONE bulk copy (cp.async.bulk +
+// mbarrier transaction count) per vector per slab, landing in shared memory as [NV][S][32]
+// (conflict-free reads: lane r reads column r); outputs are stored straight from registers,
+// 256 contiguous bytes per warp store.  Points beyond N (tail of the last chain, and the padding
+// chains up to a multiple of 32) are zeros: phi = mu = 0 there contributes nothing to any carry
+// that is used.
+// ---------------------------------------------------------------------------------------
+constexpr int kSwS = 8;      // offsets per slab
+constexpr int kSwStages = 3; // slab stages per warp (two in flight while one is consumed)
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *sdst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Issue slab s (offsets s*S .. s*S+S-1) of NV vectors for the warp's 32 chains (block base
+// offset wbase = chain0 * P) into stage buffer sbuf [NV][S][32]: NV bulk copies of S*256 bytes.
+template <int NV>
+__device__ __forceinline__ void sw_issue(double *sbuf, uint64_t *bar, const double *const *vecs, int64_t wbase, int s,
+                                         int lane) {
+    constexpr int S = kSwS;
+    if (lane == 0) {
+        mbar_arrive_expect_tx(bar, (uint32_t)(NV * S * 32 * sizeof(double)));
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+            bulk_g2s(sbuf + v * S * 32, vecs[v] + wbase + (int64_t)s * S * 32, S * 32 * sizeof(double), bar);
+    }
+}
+
+template <int NB, typename T, int MODE, bool NEXT>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply(Plan p) {
     using AV = ApplyVecs<NB, MODE>;
     constexpr int M = 1 << NB;
-    constexpr int S = slab_s(NB);
-    constexpr int TILE = 32 * (S + 1);
+    constexpr int S = kSwS;
     constexpr int NV = AV::NV;
-    constexpr int OSLOT = MODE == MODE_UPD ? AV::IMU : AV::IPHI;
+    constexpr int STG = NV * S * 32;  // doubles per stage
+    extern __shared__ __align__(128) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t chain0 = ((int64_t)blockIdx.x * kWarpsPerCta + warp) * 32;
+    if (chain0 >= p.nchunks || *(volatile int *)p.stop) return;
+    double *buf = smem + (size_t)warp * kSwStages * STG;
+    __shared__ uint64_t bars[kWarpsPerCta][kSwStages];
+    uint64_t *bar = bars[warp];
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < kSwStages; ++i) mbar_init(&bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
     const int64_t c = chain0 + lane;
-    const bool live = FULL || c < cend;
-    const int64_t x0 = c * p.P;
-    const int64_t x1 = FULL ? x0 + p.P : min(p.N, x0 + p.P);
-    const int ns = (int)((p.P + S - 1) / S);
+    const bool live = c < p.nchunks;
+    const int ns = (int)(p.P / S);
     const double *vecs[NV];
 #pragma unroll
     for (int b = 0; b < NB; ++b) vecs[b] = p.bound[b];
@@ -874,40 +931,67 @@ __device__ __forceinline__ void sw_body(const Plan &p, int64_t chain0, int64_t c
         vec_unit<NB, T>(F);
         vec_unit<NB, T>(B);
     }
-    double f[NB > 0 ? NB : 1];
     T Gx[NEXT ? NB + 1 : 1][NEXT ? M : 1];
     if constexpr (NEXT) opx_identity<NB, T>(Gx);
+    // the next-update operator step of point m is issued after the scans of point m+1
+    // (software pipelining: the division of point m overlaps the scans of point m+1)
+    double fprev[NB > 0 ? NB : 1], oprev = 0.0;
+    bool have_prev = false;
     double acc = 0.0;
     bool bad = false;
-    slab_issue<S, NV>(buf, vecs, chain0, p.P, p.N, 0, lane);
-    cp_async_commit();
+#pragma unroll
+    for (int i = 0; i < kSwStages - 1; ++i)
+        if (i < ns) sw_issue<NV>(buf + i * STG, &bar[i], vecs, chain0 * p.P, i, lane);
 #pragma unroll 1
     for (int s = 0; s < ns; ++s) {
-        if (s + 1 < ns) slab_issue<S, NV>(buf + ((s + 1) & 1) * NV * TILE, vecs, chain0, p.P, p.N, s + 1, lane);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncwarp();
-        double *cur = buf + (s & 1) * NV * TILE;
+        {
+            const int sn = s + kSwStages - 1;  // refill the stage consumed in iteration s-1
+            if (sn < ns) sw_issue<NV>(buf + (sn % kSwStages) * STG, &bar[sn % kSwStages], vecs, chain0 * p.P, sn, lane);
+        }
+        mbar_wait(&bar[s % kSwStages], (uint32_t)((s / kSwStages) & 1));
+        const double *cur = buf + (s % kSwStages) * STG;
+        double *outp = AV::kOut ? p.outk + chain0 * p.P + (int64_t)s * S * 32 + lane : nullptr;
 #pragma unroll
         for (int j = 0; j < S; ++j) {
-            const int64_t x = x0 + (int64_t)s * S + j;
-            if (FULL || x < x1) {
-                slab_f<NB, S>(f, cur, lane, j);
-                dp_diag<NB, T, true>(F, wt);
-                dp_place<NB, T>(F, f);
-                dp_unplace<NB, T>(B, f);          // B := U_m = D B_{m+1}
-                const T J = combine<NB, T>(F, B);
-                dp_diag_inv<NB, T>(B, wi);        // B := B_{m+1}
-                const double o = epilogue<NB, T, MODE>(J, cur, lane, j, acc, bad);
-                if (AV::kOut) cur[(OSLOT * 32 + lane) * (S + 1) + j] = o;
-                if constexpr (NEXT) next_ops_step<NB, T>(Gx, wt, f, o, j == 0 && s == 0);
+            double f[NB > 0 ? NB : 1];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) f[b] = cur[(b * S + j) * 32 + lane];
+            dp_diag<NB, T, true>(F, wt);
+            dp_place<NB, T>(F, f);
+            dp_unplace<NB, T>(B, f);          // B := U_m = D B_{m+1}
+            const T J = combine<NB, T>(F, B);
+            dp_diag_inv<NB, T>(B, wi);        // B := B_{m+1}
+            if constexpr (NEXT) {
+                if (j > 0 || have_prev) next_ops_step<NB, T>(Gx, wt, fprev, oprev, j == 1 && s == 0);
+            }
+            const double jv = value_of(J);
+            double o = 0.0;
+            if (MODE == MODE_MARG) {
+                o = cur[(AV::IPHI * S + j) * 32 + lane] * jv;
+            } else if (MODE == MODE_UPD) {
+                const double mu = cur[(AV::IMU * S + j) * 32 + lane];
+                const double q = div_nr1(mu, jv);
+                const bool nz = nonzero(mu);
+                bad |= nz && !finite_positive(q);
+                o = nz ? q : 0.0;
+            } else if (MODE == MODE_RES) {
+                acc += fabs(cur[(AV::IPHI * S + j) * 32 + lane] * jv - cur[(AV::IMU * S + j) * 32 + lane]);
+            } else {
+                if constexpr (sizeof(T) == sizeof(Dual))
+                    acc += cur[(AV::IPHI * S + j) * 32 + lane] * reinterpret_cast<const Dual &>(J).d;
+            }
+            if (AV::kOut) outp[j * 32] = o;
+            if constexpr (NEXT) {
+#pragma unroll
+                for (int b = 0; b < NB; ++b) fprev[b] = f[b];
+                oprev = o;
             }
         }
-        __syncwarp();
-        if (AV::kOut) {
-            slab_store<S>(cur + OSLOT * TILE, p.outk, chain0, cend, p.P, p.N, s, lane);
-            __syncwarp();
-        }
+        have_prev = true;
+        __syncwarp();  // every lane is done with this stage before it is refilled
+    }
+    if constexpr (NEXT) {
+        if (have_prev) next_ops_step<NB, T>(Gx, wt, fprev, oprev, ns == 1 && kSwS == 1);
     }
     if (bad && live) raise_status(p, 6 /*EOVERFLOW*/);
     if ((MODE == MODE_RES || MODE == MODE_COST) && live) p.partial[c] = acc;
@@ -918,19 +1002,116 @@ __device__ __forceinline__ void sw_body(const Plan &p, int64_t chain0, int64_t c
     }
 }
 
-// Chains [0, nfull) are complete (and P % S == 0 when nfull > 0); the warp holding the ragged
-// last chain takes the predicated body inside the same launch.
-template <int NB, typename T, int MODE, bool NEXT>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply(Plan p, int64_t nfull) {
-    using AV = ApplyVecs<NB, MODE>;
-    constexpr int TILE = 32 * (slab_s(NB) + 1);
-    extern __shared__ double smem[];
+// Chain operators of a bound set in the transposed layout (first update of a solve).
+template <int NB, typename T>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_sw_ops(Plan p) {
+    constexpr int M = 1 << NB;
+    constexpr int S = kSwS;
+    constexpr int NV = NB;
+    constexpr int STG = NV * S * 32;
+    extern __shared__ __align__(128) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t chain0 = ((int64_t)blockIdx.x * kWarpsPerCta + warp) * 32;
     if (chain0 >= p.nchunks || *(volatile int *)p.stop) return;
-    double *buf = smem + (size_t)warp * 2 * AV::NV * TILE;
-    if (chain0 + 32 <= nfull) sw_body<NB, T, MODE, NEXT, true>(p, chain0, p.nchunks, buf, lane);
-    else sw_body<NB, T, MODE, NEXT, false>(p, chain0, p.nchunks, buf, lane);
+    double *buf = smem + (size_t)warp * kSwStages * STG;
+    __shared__ uint64_t bars[kWarpsPerCta][kSwStages];
+    uint64_t *bar = bars[warp];
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < kSwStages; ++i) mbar_init(&bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    const int64_t c = chain0 + lane;
+    const int ns = (int)(p.P / S);
+    const double *vecs[NV];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) vecs[b] = p.bound[b];
+    T wt[NB + 2];
+    load_weights<NB, T>(wt, p.W);
+    T G[NB + 1][M];
+    opx_identity<NB, T>(G);
+#pragma unroll
+    for (int i = 0; i < kSwStages - 1; ++i)
+        if (i < ns) sw_issue<NV>(buf + i * STG, &bar[i], vecs, chain0 * p.P, i, lane);
+#pragma unroll 1
+    for (int s = 0; s < ns; ++s) {
+        const int sn = s + kSwStages - 1;
+        if (sn < ns) sw_issue<NV>(buf + (sn % kSwStages) * STG, &bar[sn % kSwStages], vecs, chain0 * p.P, sn, lane);
+        mbar_wait(&bar[s % kSwStages], (uint32_t)((s / kSwStages) & 1));
+        const double *cur = buf + (s % kSwStages) * STG;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            double f[NB > 0 ? NB : 1];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) f[b] = cur[(b * S + j) * 32 + lane];
+            opx_step<NB, T>(G, wt, f, s == 0 && j == 0);
+        }
+        __syncwarp();
+    }
+    if (c < p.nchunks)
+        opx_store<NB, T>(G, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
+                         static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+}
+
+// Natural <-> chain-blocked layout: natural x = c*P + t  <->  (c/32)*32P + t*32 + c%32.
+// op: 0 copy, 1 exp (natural log-scalings -> linear), 2 log (linear -> log-scalings).
+// One CTA per 32 chains x 32 offsets tile (blockIdx.y = chain group).
+__global__ void k_to_t(const double *__restrict__ src, double *__restrict__ dst, int64_t N, int64_t P, int64_t nchains,
+                       int op) {
+    __shared__ double tile[32][33];
+    const int64_t t0 = (int64_t)blockIdx.x * 32, g = blockIdx.y, c0 = g * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {  // r: chain within tile, threadIdx.x: offset t
+        const int64_t c = c0 + r, t = t0 + threadIdx.x;
+        const int64_t x = c * P + t;
+        double v = 0.0;
+        if (c < nchains && t < P && x < N) {
+            v = src[x];
+            if (op == 1) v = exp(v);
+        }
+        tile[r][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {  // r: offset within tile, threadIdx.x: chain
+        const int64_t t = t0 + r;
+        if (t < P) dst[g * 32 * P + t * 32 + threadIdx.x] = tile[threadIdx.x][r];
+    }
+}
+
+__global__ void k_from_t(const double *__restrict__ src, double *__restrict__ dst, int64_t N, int64_t P, int64_t nchains,
+                         int op) {
+    __shared__ double tile[32][33];
+    const int64_t t0 = (int64_t)blockIdx.x * 32, g = blockIdx.y, c0 = g * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {  // r: offset, threadIdx.x: chain
+        const int64_t t = t0 + r;
+        tile[r][threadIdx.x] = t < P ? src[g * 32 * P + t * 32 + threadIdx.x] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {  // r: chain, threadIdx.x: offset
+        const int64_t c = c0 + r, t = t0 + threadIdx.x;
+        const int64_t x = c * P + t;
+        if (c < nchains && t < P && x < N) {
+            double v = tile[threadIdx.x][r];
+            if (op == 2) v = log(v);
+            dst[x] = v;
+        }
+    }
+}
+
+cudaError_t launch_to_t(const double *src, double *dst, int64_t N, int64_t P, int64_t nchains, int64_t nchp, int op,
+                        cudaStream_t s, int64_t *launches) {
+    dim3 grid((unsigned)((P + 31) / 32), (unsigned)(nchp / 32));
+    k_to_t<<<grid, dim3(32, 8), 0, s>>>(src, dst, N, P, nchains, op);
+    ++*launches;
+    return cudaGetLastError();
+}
+cudaError_t launch_from_t(const double *src, double *dst, int64_t N, int64_t P, int64_t nchains, int64_t nchp, int op,
+                          cudaStream_t s, int64_t *launches) {
+    dim3 grid((unsigned)((P + 31) / 32), (unsigned)((nchains + 31) / 32));
+    (void)nchp;
+    k_from_t<<<grid, dim3(32, 8), 0, s>>>(src, dst, N, P, nchains, op);
+    ++*launches;
+    return cudaGetLastError();
 }
 
 template <int NB, typename T>
@@ -975,17 +1156,22 @@ static void launch_apply_tm(const Plan &p, int64_t cbeg, int64_t cend, cudaStrea
     ++*launches;
 }
 
+template <int NB, int MODE>
+static constexpr size_t sw_smem() {
+    return (size_t)kWarpsPerCta * kSwStages * ApplyVecs<NB, MODE>::NV * kSwS * 32 * sizeof(double);
+}
+
 template <int NB, typename T, int MODE, bool NEXT>
-static void launch_sw(const Plan &p, int64_t nfull, cudaStream_t s, int64_t *launches) {
-    const size_t sm = (size_t)kWarpsPerCta * 2 * ApplyVecs<NB, MODE>::NV * 32 * (slab_s(NB) + 1) * sizeof(double);
+static void launch_sw(const Plan &p, cudaStream_t s, int64_t *launches) {
+    constexpr size_t sm = sw_smem<NB, MODE>();
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_sw_apply<NB, T, MODE, NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         attr = true;
     }
     const int tpb = kWarpsPerCta * 32;
-    const int64_t nb = (p.nchunks + tpb - 1) / tpb;
-    k_sw_apply<NB, T, MODE, NEXT><<<(unsigned)nb, tpb, sm, s>>>(p, nfull);
+    const int64_t nb = (p.nchp + tpb - 1) / tpb;
+    k_sw_apply<NB, T, MODE, NEXT><<<(unsigned)nb, tpb, sm, s>>>(p);
     ++*launches;
 }
 
@@ -993,8 +1179,8 @@ static void launch_sw(const Plan &p, int64_t nfull, cudaStream_t s, int64_t *lau
 int sw_blocks_per_sm(int NB) {
     int n = 0;
     const int tpb = kWarpsPerCta * 32;
-    auto q = [&](auto kern, int nv, int S) {
-        const size_t sm = (size_t)kWarpsPerCta * 2 * nv * 32 * (S + 1) * sizeof(double);
+    auto q = [&](auto kern, int nv, int) {
+        const size_t sm = (size_t)kWarpsPerCta * kSwStages * nv * kSwS * 32 * sizeof(double);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, tpb, sm);
     };
@@ -1014,7 +1200,7 @@ static void launch_apply(const Plan &p, int64_t /*nb*/, int /*tpb*/, cudaStream_
     const bool full_ok = p.P % slab_s(NB) == 0;
     const int64_t nfull = full_ok ? p.N / p.P : 0;
     if (p.sw) {
-        if constexpr (NB <= 4) launch_sw<NB, T, MODE, NEXT>(p, nfull, s, launches);
+        if constexpr (NB <= 4) launch_sw<NB, T, MODE, NEXT>(p, s, launches);
         return;
     }
     if constexpr (NB <= 3 && sizeof(T) == sizeof(double)) {
@@ -1035,7 +1221,18 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
     const int tpb = kWarpsPerCta * 32;
     const int64_t nb = (p.nchunks + tpb - 1) / tpb;
     if (ev) cudaEventRecord(ev[0], s);
-    if (with_ops) {
+    if (with_ops && p.sw) {
+        if constexpr (NB <= 4) {
+            constexpr size_t sm = (size_t)kWarpsPerCta * kSwStages * NB * kSwS * 32 * sizeof(double);
+            static bool attr_sw = false;
+            if (!attr_sw) {
+                cudaFuncSetAttribute(k_sw_ops<NB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                attr_sw = true;
+            }
+            k_sw_ops<NB, T><<<(unsigned)((p.nchp + tpb - 1) / tpb), tpb, sm, s>>>(p);
+            ++*launches;
+        }
+    } else if (with_ops) {
         const size_t sm = ops_smem<NB, T>();
         static bool attr = false;
         if (!attr) {
