@@ -107,6 +107,19 @@ typedef struct {
 MMOT_API mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype dt,
                         const mmot_opts *opts, void *cuda_stream, mmot_ctx **out);
 
+/* Create a context for `batch` independent instances of (l, N) on the same grid, instance b
+ * with its own eta_host[b] (BASELINE C5: 8192 x (l=5, N=4096), eta ~ logU[1e-3, 1e-1]).
+ *   l in [2, 5] in this build (EUNSUPPORTED above), N >= 1, batch >= 1, every eta finite > 0;
+ *   dt: MMOT_F64 (MMOT_F32 -> EUNSUPPORTED in this build).  eta_host is copied.
+ * Layouts for the compute calls on a batched context: every array argument is a plane of
+ * `batch` consecutive N-vectors ([batch][N], instance-major); mmot_cost fills W[batch] (host);
+ * mmot_sinkhorn runs exactly `iters` sweeps per instance (tol must be <= 0, else EUNSUPPORTED),
+ * one warp per instance on device, and reports the first failing instance (if any).
+ * Internally each instance's scalings carry one exponent per 1/32 of the grid and marginal,
+ * so instances whose |log phi| exceeds the fp64 range (eta = 1e-3) stay representable. */
+MMOT_API mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *eta_host, mmot_grid grid,
+                                         mmot_dtype dt, const mmot_opts *opts, void *cuda_stream, mmot_ctx **out);
+
 /* m_k = phi_k * J_k(phi_{-k}) -- the k-th marginal of K . (phi_1 x ... x phi_l)
  * (P:1021), computed by the O(N) separated-summation scans.
  *   k in [0, l); u: host array of l device pointers (repr per opts, float64, length N each);

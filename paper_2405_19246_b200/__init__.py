@@ -67,6 +67,9 @@ def load_library():
     lib.mmot_create.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_double, _Grid, ctypes.c_int,
                                 ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
     lib.mmot_create.restype = ctypes.c_int
+    lib.mmot_create_batched.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
+                                        _Grid, ctypes.c_int, ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
+    lib.mmot_create_batched.restype = ctypes.c_int
     lib.mmot_marginal.argtypes = [vp, ctypes.c_int, vpp, vp]
     lib.mmot_marginal.restype = ctypes.c_int
     lib.mmot_sinkhorn.argtypes = [vp, vpp, ctypes.c_int, ctypes.c_double, vpp, ctypes.POINTER(_Report)]
@@ -120,14 +123,18 @@ class Context:
     forwards their data pointers and the current CUDA stream to the C ABI.
     """
 
-    def __init__(self, l: int, N: int, eta: float, grid=(0.0, 1.0), dtype: str = "f64",
+    def __init__(self, l: int, N: int, eta, grid=(0.0, 1.0), dtype: str = "f64",
                  repr: str = "log", check_every: int = 0, chunk: int = 0, stream=None,
-                 kernel: str = "auto"):
+                 kernel: str = "auto", batch: Optional[int] = None):
+        """Single instance (eta: float), or a batched context (batch=B, eta: B per-instance
+        values) whose array arguments are [B][N] planes (mmot_create_batched)."""
         import torch
         self._lib = load_library()
         if not torch.cuda.is_available():
             raise MMOTError(7, "no CUDA device: the library has no CPU path")
-        self.l, self.N, self.eta = int(l), int(N), float(eta)
+        self.batch = None if batch is None else int(batch)
+        self.l, self.N = int(l), int(N)
+        self.eta = float(eta) if self.batch is None else [float(e) for e in eta]
         self.grid = (float(grid[0]), float(grid[1]))
         self.repr = repr
         self.h = (self.grid[1] - self.grid[0]) / (self.N - 1) if self.N > 1 else 1.0
@@ -135,8 +142,16 @@ class Context:
         kern = {"auto": 0, "two_walk": 1, "single_walk": 2}[kernel]
         opts = _Opts(int(check_every), 0, LOG if repr == "log" else LINEAR, int(chunk), kern)
         ctx = ctypes.c_void_p()
-        st = self._lib.mmot_create(self.l, self.N, self.eta, _Grid(*self.grid), F64 if dtype == "f64" else F32,
-                                   ctypes.byref(opts), ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx))
+        if self.batch is None:
+            st = self._lib.mmot_create(self.l, self.N, self.eta, _Grid(*self.grid), F64 if dtype == "f64" else F32,
+                                       ctypes.byref(opts), ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx))
+        else:
+            if len(self.eta) != self.batch:
+                raise MMOTError(2, f"expected {self.batch} eta values, got {len(self.eta)}")
+            etas = (ctypes.c_double * self.batch)(*self.eta)
+            st = self._lib.mmot_create_batched(self.l, self.N, self.batch, etas, _Grid(*self.grid),
+                                               F64 if dtype == "f64" else F32, ctypes.byref(opts),
+                                               ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx))
         if st != 0:
             raise MMOTError(st, self._lib.mmot_last_error(None).decode())
         self._ctx = ctx
@@ -149,9 +164,10 @@ class Context:
     def _ptrs(self, ts) -> ctypes.Array:
         if len(ts) != self.l:
             raise MMOTError(2, f"expected {self.l} vectors, got {len(ts)}")
+        n = self.N * (self.batch or 1)
         for t in ts:
-            if not t.is_cuda or not t.is_contiguous() or t.numel() != self.N:
-                raise MMOTError(2, "vectors must be contiguous CUDA tensors of length N")
+            if not t.is_cuda or not t.is_contiguous() or t.numel() != n:
+                raise MMOTError(2, f"vectors must be contiguous CUDA tensors of {n} elements")
         return _ptr_array([t.data_ptr() for t in ts])
 
     @property
@@ -172,7 +188,8 @@ class Context:
     def marginal(self, k: int, u, out=None):
         import torch
         if out is None:
-            out = torch.empty(self.N, dtype=torch.float64, device=u[0].device)
+            shape = (self.N,) if self.batch is None else (self.batch, self.N)
+            out = torch.empty(shape, dtype=torch.float64, device=u[0].device)
         self._check(self._lib.mmot_marginal(self._ctx, int(k), self._ptrs(u), ctypes.c_void_p(out.data_ptr())))
         return out
 
@@ -199,7 +216,12 @@ class Context:
         return dict(iters_done=rep.iters_done, residual=rep.residual, converged=bool(rep.converged),
                     status=rep.status, fail_iter=rep.fail_iter)
 
-    def cost(self, u) -> float:
+    def cost(self, u):
+        """W (float), or for a batched context a list of the B per-instance costs."""
+        if self.batch is not None:
+            Wb = (ctypes.c_double * self.batch)()
+            self._check(self._lib.mmot_cost(self._ctx, self._ptrs(u), Wb))
+            return list(Wb)
         W = ctypes.c_double()
         self._check(self._lib.mmot_cost(self._ctx, self._ptrs(u), ctypes.byref(W)))
         return W.value

@@ -7,8 +7,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRCS = ["csrc/api.cu", "csrc/kernels.cu"]
-DEPS = SRCS + ["csrc/dp.cuh", "csrc/internal.h", "../include/mmot.h"]
+SRCS = ["csrc/api.cu", "csrc/kernels.cu", "csrc/batched.cu"]
+DEPS = SRCS + ["csrc/dp.cuh", "csrc/walk.cuh", "csrc/internal.h", "../include/mmot.h"]
 LIB = os.path.join(HERE, "libmmot.so")
 
 NVCC_FLAGS = [

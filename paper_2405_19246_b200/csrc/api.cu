@@ -60,6 +60,15 @@ struct mmot_ctx {
     int64_t nchp = 0;                       // sw: chains rounded up to 32 (transposed row length)
     double *mu_t[mmot::kMaxL] = {nullptr};  // sw: marginals in the chain-transposed layout
     double *out_t = nullptr;                // sw: marginal output in the chain-transposed layout
+    // batched contexts (mmot_create_batched)
+    bool batched = false;
+    int64_t batch = 1;
+    mmot::BatchArgs ba{};
+    double *bat_mem = nullptr;              // eta, phit, scratch, wout (one allocation)
+    int *bat_int = nullptr;                 // E, status, fail_iter
+    void **bat_ptrs = nullptr;              // device array of l pointers (u[] for import/export)
+    double *bat_whost = nullptr;            // pinned [batch]
+    int *bat_shost = nullptr;               // pinned [2*batch]
     double *stage_mu[mmot::kMaxL] = {nullptr};
     double *stage_u[mmot::kMaxL] = {nullptr};
     int *hstop = nullptr;       // pinned, async stop polling
@@ -149,6 +158,11 @@ void mmot_destroy(mmot_ctx *ctx) {
     else cudaDeviceSynchronize();
     cudaFree(ctx->ws);
     cudaFree(ctx->out_t);
+    cudaFree(ctx->bat_mem);
+    cudaFree(ctx->bat_int);
+    cudaFree(ctx->bat_ptrs);
+    if (ctx->bat_whost) cudaFreeHost(ctx->bat_whost);
+    if (ctx->bat_shost) cudaFreeHost(ctx->bat_shost);
     for (int q = 0; q < mmot::kMaxL; ++q) {
         cudaFree(ctx->lin[q]);
         cudaFree(ctx->mu_t[q]);
@@ -333,7 +347,161 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
     return MMOT_OK;
 }
 
+mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *eta_host, mmot_grid grid,
+                                mmot_dtype dt, const mmot_opts *opts, void *cuda_stream, mmot_ctx **out) {
+    if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
+    *out = nullptr;
+    if (l < 2 || l > 8) { set_err(nullptr, "l=%d outside [2,8]", l); return MMOT_EINVAL; }
+    if (N < 1 || batch < 1 || !eta_host) { set_err(nullptr, "N, batch must be >= 1 and eta_host non-NULL"); return MMOT_EINVAL; }
+    for (int64_t b = 0; b < batch; ++b)
+        if (!(eta_host[b] > 0) || !isfinite(eta_host[b])) { set_err(nullptr, "eta[%lld] must be finite and > 0", (long long)b); return MMOT_EINVAL; }
+    if (!isfinite(grid.x_min) || !isfinite(grid.x_max) || (N > 1 && !(grid.x_max > grid.x_min))) {
+        set_err(nullptr, "grid must satisfy x_max > x_min");
+        return MMOT_EINVAL;
+    }
+    if (dt != MMOT_F64 && dt != MMOT_F32) { set_err(nullptr, "bad dtype"); return MMOT_EINVAL; }
+    if (opts && (opts->check_every < 0 || opts->chunk < 0 || (opts->repr != MMOT_LOG && opts->repr != MMOT_LINEAR))) {
+        set_err(nullptr, "bad opts");
+        return MMOT_EINVAL;
+    }
+    if (l > 5) { set_err(nullptr, "batched contexts support l <= 5 in this build"); return MMOT_EUNSUPPORTED; }
+    if (dt == MMOT_F32) { set_err(nullptr, "MMOT_F32 batched contexts are not implemented yet"); return MMOT_EUNSUPPORTED; }
+    mmot_ctx *c = new mmot_ctx();
+    c->l = l;
+    c->N = N;
+    c->eta = eta_host[0];
+    c->grid = grid;
+    c->dt = dt;
+    if (opts) c->opts = *opts;
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    cudaGetDevice(&c->device);
+    c->h = N > 1 ? (grid.x_max - grid.x_min) / (double)(N - 1) : 1.0;
+    c->batched = true;
+    c->batch = batch;
+    mmot::BatchArgs &a = c->ba;
+    a.l = l;
+    a.N = N;
+    a.batch = batch;
+    a.P = (int)(((N + 31) / 32 + 7) / 8 * 8);
+    a.h = c->h;
+    a.slots = std::min<int64_t>(mmot::bat_slots(l), (batch + 3) / 4 * 4);
+    const int NB = l - 1, M = 1 << NB;
+    const size_t opsz = (size_t)2 * (NB + 1) * M * 32 * sizeof(mmot::Dual);      // per slot
+    const size_t cksz = (size_t)(a.P / 8) * M * 32 * sizeof(mmot::Dual);         // per slot
+    const size_t nd = (size_t)batch                      // eta
+                      + (size_t)l * batch * N            // phit
+                      + (size_t)a.slots * (opsz + cksz) / sizeof(double)
+                      + (size_t)batch;                   // wout
+    const size_t ni = (size_t)batch * l * 32 + 2 * (size_t)batch;
+    bool ok = cudaMalloc(&c->bat_mem, nd * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&c->bat_int, ni * sizeof(int)) == cudaSuccess &&
+              cudaMalloc(&c->bat_ptrs, 2 * mmot::kMaxL * sizeof(void *)) == cudaSuccess &&
+              cudaMallocHost(&c->bat_whost, (size_t)batch * sizeof(double)) == cudaSuccess &&
+              cudaMallocHost(&c->bat_shost, 2 * (size_t)batch * sizeof(int)) == cudaSuccess &&
+              cudaMallocHost(&c->hsc, sizeof(DevScalars)) == cudaSuccess &&
+              cudaMalloc(&c->ws, sizeof(DevScalars)) == cudaSuccess;
+    if (!ok) {
+        set_err(c, "batched workspace allocation failed (%zu B)", nd * sizeof(double));
+        snprintf(g_err, sizeof g_err, "%s", c->err);
+        mmot_destroy(c);
+        return MMOT_ENOMEM;
+    }
+    c->dsc = static_cast<DevScalars *>(c->ws);
+    double *p = c->bat_mem;
+    a.eta = p;
+    p += batch;
+    for (int q = 0; q < l; ++q) {
+        a.phit[q] = p;
+        p += (size_t)batch * N;
+    }
+    a.ops = p;
+    p += (size_t)a.slots * opsz / sizeof(double);
+    a.ckpt = p;
+    p += (size_t)a.slots * cksz / sizeof(double);
+    a.wout = p;
+    a.E = c->bat_int;
+    a.status = c->bat_int + (size_t)batch * l * 32;
+    a.fail_iter = a.status + batch;
+    if (cudaMemsetAsync(c->bat_mem, 0, nd * sizeof(double), c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->bat_int, 0, ni * sizeof(int), c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->dsc, 0, sizeof(DevScalars), c->stream) != cudaSuccess ||
+        cudaMemcpyAsync(c->bat_mem, eta_host, (size_t)batch * sizeof(double), cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess) {
+        set_err(c, "batched workspace init failed");
+        mmot_destroy(c);
+        return MMOT_ECUDA;
+    }
+    *out = c;
+    return MMOT_OK;
+}
+
 }  // extern "C"
+
+static mmot_status reset_scalars(mmot_ctx *c);
+
+// Upload an array of l device pointers (for the batched import / export kernels).
+static mmot_status bat_upload_ptrs(mmot_ctx *c, const void *const *u, int slot) {
+    void *h[mmot::kMaxL] = {nullptr};
+    for (int q = 0; q < c->l; ++q) {
+        if (!u[q]) { set_err(c, "u[%d] is NULL", q); return MMOT_EINVAL; }
+        h[q] = const_cast<void *>(u[q]);
+    }
+    CK(c, cudaMemcpyAsync(c->bat_ptrs + slot * mmot::kMaxL, h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+    return MMOT_OK;
+}
+
+static mmot_status bat_import(mmot_ctx *c, const void *const *u) {
+    mmot_status st = bat_upload_ptrs(c, u, 0);
+    if (st) return st;
+    CK(c, mmot::launch_bat_convert(c->ba, c->bat_ptrs, 1, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
+    return MMOT_OK;
+}
+
+static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters, double tol, void *const *u,
+                                mmot_report *rep) {
+    if (tol > 0) { set_err(c, "batched contexts run a fixed number of sweeps (tol must be <= 0)"); return MMOT_EUNSUPPORTED; }
+    mmot_status st = reset_scalars(c);
+    if (st) return st;
+    const int64_t n = c->batch * c->N;
+    for (int q = 0; q < c->l; ++q) {
+        CK(c, mmot::launch_check(mu[q], n, 0, &c->dsc->flags[q], &c->dsc->mass[q], c->stream, &c->launches));
+        CK(c, mmot::launch_check(static_cast<const double *>(u[q]), n, c->opts.repr == MMOT_LOG ? 1 : 0,
+                                 &c->dsc->flags[c->l + q], nullptr, c->stream, &c->launches));
+    }
+    CK(c, mmot::launch_check_finish(c->dsc->flags, c->dsc->mass, 2 * c->l, c->l, &c->dsc->status, &c->dsc->stop,
+                                    &c->dsc->fail_iter, c->stream, &c->launches));
+    CK(c, cudaMemcpyAsync(c->hsc, c->dsc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    if (c->hsc->status) {
+        if (rep) { rep->status = c->hsc->status; rep->fail_iter = 0; }
+        set_err(c, "%s", mmot_strerror((mmot_status)c->hsc->status));
+        return (mmot_status)c->hsc->status;
+    }
+    st = bat_import(c, u);
+    if (st) return st;
+    mmot::BatchArgs a = c->ba;
+    for (int q = 0; q < c->l; ++q) a.mu[q] = mu[q];
+    a.iters = iters;
+    CK(c, mmot::launch_batched(a, 0, c->stream, &c->launches));
+    st = bat_upload_ptrs(c, const_cast<const void *const *>(u), 0);
+    if (st) return st;
+    CK(c, mmot::launch_bat_convert(c->ba, c->bat_ptrs, 0, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
+    CK(c, cudaMemcpyAsync(c->bat_shost, c->ba.status, 2 * (size_t)c->batch * sizeof(int), cudaMemcpyDeviceToHost,
+                          c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    int status = 0, fail = -1;
+    for (int64_t b = 0; b < c->batch && !status; ++b)
+        if (c->bat_shost[b]) { status = c->bat_shost[b]; fail = c->bat_shost[c->batch + b]; }
+    if (rep) {
+        rep->iters_done = status ? fail : iters;
+        rep->residual = NAN;
+        rep->converged = 0;
+        rep->status = status;
+        rep->fail_iter = status ? fail : -1;
+    }
+    if (status) set_err(c, "%s (an instance failed at sweep %d)", mmot_strerror((mmot_status)status), fail);
+    return (mmot_status)status;
+}
 
 // ---------------------------------------------------------------------------------------
 static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double *mu, double *out, int iter) {
@@ -491,6 +659,15 @@ mmot_status mmot_marginal(mmot_ctx *c, int k, const void *const *u, void *out) {
     if (!c || !u || !out) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
     if (k < 0 || k >= c->l) { set_err(c, "k=%d outside [0,%d)", k, c->l); return MMOT_EINVAL; }
     cudaSetDevice(c->device);
+    if (c->batched) {
+        mmot_status st = bat_import(c, u);
+        if (st) return st;
+        mmot::BatchArgs a = c->ba;
+        a.k = k;
+        a.out = static_cast<double *>(out);
+        CK(c, mmot::launch_batched(a, 1, c->stream, &c->launches));
+        return MMOT_OK;
+    }
     mmot_status st = reset_scalars(c);
     if (st) return st;
     const double *lin[mmot::kMaxL];
@@ -515,6 +692,7 @@ mmot_status mmot_sinkhorn(mmot_ctx *c, const void *const *marginals, int iters, 
         mu[q] = static_cast<const double *>(marginals[q]);
     }
     cudaSetDevice(c->device);
+    if (c->batched) return bat_sinkhorn(c, mu, iters, tol, u, rep);
     return sinkhorn_impl(c, mu, iters, tol, u, rep);
 }
 
@@ -548,6 +726,18 @@ mmot_status mmot_sinkhorn_host(mmot_ctx *c, const void *const *marginals_host, i
 mmot_status mmot_cost(mmot_ctx *c, const void *const *u, double *W) {
     if (!c || !u || !W) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
     cudaSetDevice(c->device);
+    if (c->batched) {
+        mmot_status st = bat_import(c, u);
+        if (st) return st;
+        mmot::BatchArgs a = c->ba;
+        a.k = c->l - 1;
+        CK(c, mmot::launch_batched(a, 2, c->stream, &c->launches));
+        CK(c, cudaMemcpyAsync(c->bat_whost, c->ba.wout, (size_t)c->batch * sizeof(double), cudaMemcpyDeviceToHost,
+                              c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        memcpy(W, c->bat_whost, (size_t)c->batch * sizeof(double));
+        return MMOT_OK;
+    }
     mmot_status st = reset_scalars(c);
     if (st) return st;
     const double *lin[mmot::kMaxL];
@@ -599,7 +789,7 @@ mmot_status mmot_init_uniform(mmot_ctx *c, void *const *u) {
     const double v = c->opts.repr == MMOT_LOG ? -log((double)c->N) : 1.0 / (double)c->N;
     for (int q = 0; q < c->l; ++q) {
         if (!u[q]) { set_err(c, "u[%d] is NULL", q); return MMOT_EINVAL; }
-        CK(c, mmot::launch_fill(static_cast<double *>(u[q]), v, c->N, c->stream, &c->launches));
+        CK(c, mmot::launch_fill(static_cast<double *>(u[q]), v, c->N * c->batch, c->stream, &c->launches));
     }
     return MMOT_OK;
 }

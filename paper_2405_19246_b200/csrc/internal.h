@@ -72,6 +72,30 @@ cudaError_t launch_from_t(const double *src, double *dst, int64_t N, int64_t P, 
                           cudaStream_t s, int64_t *launches);
 constexpr int kSwSlab = 8;  // chain length of single-walk contexts is a multiple of this
 
+// Batched contexts (batched.cu): one warp per instance, persistent over the sweeps.
+struct BatchArgs {
+    int l;
+    int64_t N, batch;
+    int P;                       // chain length (multiple of 8), 32 chains per instance
+    double h;
+    const double *eta;           // device [batch]
+    double *phit[kMaxL];         // device [batch][N] mantissas of phi_q
+    int *E;                      // device [batch][l][32] chain exponents
+    const double *mu[kMaxL];     // device [batch][N]
+    double *ops, *ckpt;          // scratch, sized by bat_scratch_bytes
+    int64_t slots;               // resident warps (= scratch slots)
+    int iters, k;
+    double *out;                 // [batch][N] (marginal)
+    double *wout;                // [batch] (cost)
+    int *status, *fail_iter;     // [batch]
+};
+int64_t bat_slots(int l);
+// what: 0 Sinkhorn (iters sweeps), 1 marginal k -> out, 2 cost -> wout
+cudaError_t launch_batched(const BatchArgs &a, int what, cudaStream_t s, int64_t *launches);
+// u: DEVICE array of l device pointers; import: u -> (phit, E), else (phit, E) -> u
+cudaError_t launch_bat_convert(const BatchArgs &a, void *const *u_dev_ptrs, int import, int is_log, cudaStream_t s,
+                               int64_t *launches);
+
 // Elementwise helpers.
 cudaError_t launch_exp(const double *in, double *out, int64_t n, cudaStream_t s, int64_t *launches);
 cudaError_t launch_log(const double *in, double *out, int64_t n, cudaStream_t s, int64_t *launches);

@@ -19,6 +19,7 @@
 #include <stdlib.h>
 
 #include "internal.h"
+#include "walk.cuh"
 
 namespace mmot {
 
@@ -26,78 +27,6 @@ namespace mmot {
 static const bool g_no_tmem = [] { const char *e = getenv("MMOT_NO_TMEM"); return e && e[0] == '1'; }();
 
 // ---------------------------------------------------------------------------------------
-template <int NB, typename T>
-__device__ __forceinline__ void load_weights(T (&wt)[NB + 2], const Weights &W) {
-#pragma unroll
-    for (int a = 0; a <= NB + 1; ++a) load_weight(wt[a], W, a);
-}
-
-template <int NB>
-__device__ __forceinline__ void load_f(double (&f)[NB > 0 ? NB : 1], const Plan &p, int64_t x) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) f[b] = __ldg(p.bound[b] + x);
-}
-
-// ---------------------------------------------------------------------------------------
-// Warp-cooperative slab staging.  A warp owns 32 consecutive chains (chunks of P points,
-// lane r <-> chain r).  The chains' data are moved through shared memory in slabs of S
-// points per chain: each warp-wide cp.async instruction copies 32/S chains' contiguous
-// S-point segments (full 32-byte sectors), lanes then read their own chain's values from
-// the [32][S+1] tile (odd row pitch: conflict-free 8-byte reads).  Two buffers: the next
-// slab is in flight while the current one is consumed.
-// ---------------------------------------------------------------------------------------
-
-__device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc, bool valid) {
-    const unsigned saddr = (unsigned)__cvta_generic_to_shared(sdst);
-    const int sz = valid ? 8 : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(sz) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int NPEND>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
-
-// Issue the copies of slab s of NV vectors into buf[NV][32][S+1].  Element e = it*32+lane of
-// the [32 chains][S points] slab is chain r = e / S, point j = e % S; chains >= cend (dead
-// lanes of the last warp) and points beyond N are zero-filled (src-size 0).
-template <int S, int NV>
-__device__ __forceinline__ void slab_issue(double *buf, const double *const *vec, int64_t chain0, int64_t P,
-                                           int64_t N, int s, int lane) {
-    constexpr int RPI = 32 / S;  // chains per warp instruction
-    const int r0 = lane / S, j = lane % S;
-    const int64_t off = (int64_t)s * S + j;
-    const int64_t xb = (chain0 + r0) * P + off;
-    const bool offok = off < P;
-#pragma unroll
-    for (int it = 0; it < S; ++it) {
-        const int r = it * RPI + r0;
-        const int64_t x = xb + (int64_t)(it * RPI) * P;
-        const bool valid = offok && x < N;
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-            cp_async8(buf + (v * 32 + r) * (S + 1) + j, vec[v] + (valid ? x : 0), valid);
-    }
-}
-
-// Store an output slab obuf[32][S+1] to global (coalesced, like slab_issue).
-template <int S>
-__device__ __forceinline__ void slab_store(const double *obuf, double *out, int64_t chain0, int64_t cend, int64_t P,
-                                           int64_t N, int s, int lane) {
-#pragma unroll
-    for (int it = 0; it < S; ++it) {
-        const int e = it * 32 + lane;
-        const int r = e / S, j = e % S;
-        const int64_t off = (int64_t)s * S + j;
-        const int64_t x = (chain0 + r) * P + off;
-        if (off < P && x < N && chain0 + r < cend) out[x] = obuf[r * (S + 1) + j];
-    }
-}
-
-template <int NB, int S>
-__device__ __forceinline__ void slab_f(double (&f)[NB > 0 ? NB : 1], const double *buf, int lane, int j) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) f[b] = buf[(b * 32 + lane) * (S + 1) + j];
-}
-
 // ---------------------------------------------------------------------------------------
 // Phase 1: chain operators (prefix walk and suffix walk of every chain).
 // ---------------------------------------------------------------------------------------
@@ -434,51 +363,6 @@ __device__ __forceinline__ void tmem_ld_vec(uint32_t taddr, double (&v)[M]) {
     tmem_wait_ld();
 #pragma unroll
     for (int i = 0; i < M; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
-}
-
-// mu / J with a Newton-refined reciprocal: no divide slow path, no branch.
-__device__ __forceinline__ double div_nr(double mu, double j) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(j));
-    double e = fma(-j, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-j, r, 1.0);
-    r = fma(r, e, r);
-    const double q = mu * r;
-    return fma(r, fma(-j, q, mu), q);
-}
-
-// mu / J with one Newton step on the reciprocal (relative error ~2^-46) and a residual
-// correction of the quotient, which squares that error: q' - mu/J = O(2^-92) + rounding.
-__device__ __forceinline__ double div_nr1(double mu, double j) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(j));
-    const double e = fma(-j, r, 1.0);
-    r = fma(r, e, r);
-    const double q = mu * r;
-    return fma(r, fma(-j, q, mu), q);
-}
-
-// Integer tests on the bit pattern (keep the FP64 pipe free).
-__device__ __forceinline__ bool finite_positive(double q) {  // 0 < q < inf
-    const unsigned long long b = (unsigned long long)__double_as_longlong(q);
-    return b != 0ull && b < 0x7ff0000000000000ull;
-}
-__device__ __forceinline__ bool nonzero(double q) {
-    return ((unsigned long long)__double_as_longlong(q) & 0x7fffffffffffffffull) != 0ull;
-}
-
-// Combine J[m] = sum_S F_m[S] H_m[S^c] with two independent accumulators.
-template <int NB, typename T>
-__device__ __forceinline__ T combine(const T (&F)[1 << NB], const T (&H)[1 << NB]) {
-    constexpr int M = 1 << NB;
-    T a = zero_of(T{}), b = zero_of(T{});
-#pragma unroll
-    for (int S = 0; S < M; S += 2) {
-        a = mad(F[S], H[(M - 1) ^ S], a);
-        if (S + 1 < M) b = mad(F[S + 1], H[(M - 1) ^ (S + 1)], b);
-    }
-    return T{a} + T{b};
 }
 
 // Per-point epilogue of the apply phase.  Returns the value written to the output slab

@@ -1,0 +1,153 @@
+"""GPU parity of batched contexts (mmot_create_batched: one warp per instance, per-chain
+exponents, persistent Sinkhorn) against the fp64 CPU oracle (oracle/regions.c, §4.2 region
+chains; log-domain chains where linear fp64 overflows).
+
+Tolerance (north_star fp64): 1e-10 relative -- elementwise for single products, L1-relative
+per marginal for Sinkhorn, relative for W.  Instances are independent: every instance of a
+batch is compared on its own (different eta per instance, as in BASELINE C5).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import mmot_inputs  # noqa: E402
+import paper_2405_19246_b200 as mm  # noqa: E402
+from oracle import regions, sinkhorn as osk  # noqa: E402
+
+DEV = "cuda:0"
+RTOL = 1e-10
+
+
+def _planes(arrs):
+    """list over q of [B][N] arrays -> list of contiguous device tensors."""
+    return [torch.from_numpy(np.ascontiguousarray(a)).to(DEV) for a in arrs]
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+@pytest.mark.parametrize("l", [2, 3, 4, 5])
+@pytest.mark.parametrize("N", [1, 7, 64, 257, 1000])
+def test_batched_marginal_parity(l, N):
+    B = 3
+    etas = [0.5, 0.02, 0.003]
+    h = mmot_inputs.grid_h(N)
+    phis = [mmot_inputs.random_positive(7000 + 100 * l + N + b, l, N) for b in range(B)]
+    u = _planes([np.stack([np.log(phis[b][q]) for b in range(B)]) for q in range(l)])
+    ctx = mm.Context(l, N, etas, batch=B)
+    for k in range(l):
+        got = ctx.marginal(k, u).cpu().numpy()
+        for b in range(B):
+            w = regions.edge_weights(l, h, etas[b])
+            want = phis[b][k] * regions.marginal_product(list(phis[b]), k, w)
+            assert _rel(got[b], want) <= RTOL, (l, N, k, b)
+    ctx.close()
+
+
+def test_batched_marginal_huge_dynamic_range():
+    """Gauge offsets of +-1400 in log phi (beyond fp64's e^709; the C5 runs at eta = 1e-3
+    drift to |log phi| ~ 1.8e3): sum_q c_q = 0 leaves every plan entry and
+    marginal unchanged (A16), so the products must equal the plain oracle on the offset-free
+    scalings; the per-chain exponents keep every intermediate representable."""
+    l, N, B = 4, 600, 2
+    etas = [1e-3, 0.05]
+    h = mmot_inputs.grid_h(N)
+    offs = np.array([1400.0, -1400.0, 900.0, -900.0])
+    phis = [mmot_inputs.random_positive(8800 + b, l, N) for b in range(B)]
+    u = _planes([np.stack([np.log(phis[b][q]) + offs[q] for b in range(B)]) for q in range(l)])
+    ctx = mm.Context(l, N, etas, batch=B)
+    for k in range(l):
+        got = ctx.marginal(k, u).cpu().numpy()
+        for b in range(B):
+            w = regions.edge_weights(l, h, etas[b])
+            want = phis[b][k] * regions.marginal_product(list(phis[b]), k, w)
+            assert _rel(got[b], want) <= RTOL, (k, b)
+    ctx.close()
+
+
+@pytest.mark.parametrize("l,N,T", [(3, 64, 20), (4, 300, 10), (5, 256, 6)])
+def test_batched_sinkhorn_lockstep(l, N, T):
+    """Per-instance eta from 1e-3 to 1e-1; the oracle runs the log-domain driver."""
+    etas = [1e-3, 1e-2, 1e-1]
+    B = len(etas)
+    h = mmot_inputs.grid_h(N)
+    mus = [np.stack([mmot_inputs.c2_marginals(b, N, l)[q] for q in range(l)]) for b in range(B)]
+    mu_d = _planes([np.stack([mus[b][q] for b in range(B)]) for q in range(l)])
+    ctx = mm.Context(l, N, etas, batch=B)
+    u = [torch.empty((B, N), dtype=torch.float64, device=DEV) for _ in range(l)]
+    ctx.init_uniform(u)
+    rep = ctx.sinkhorn(mu_d, T, 0.0, u)
+    assert rep["status"] == 0 and rep["iters_done"] == T
+    marg = [ctx.marginal(k, u).cpu().numpy() for k in range(l)]
+    g = np.stack([x.cpu().numpy() for x in u])  # [l][B][N]
+    ctx.close()
+    for b in range(B):
+        g_ref, _, _ = osk.sinkhorn(mus[b], h, etas[b], T, domain="log")
+        lw = np.array([-(a * (l - a)) * h / etas[b] for a in range(l + 1)])
+        for k in range(l):
+            m_ref = np.exp(g_ref[k] + regions.marginal_product_log(list(g_ref), k, lw))
+            err = np.abs(marg[k][b] - m_ref).sum() / np.abs(m_ref).sum()
+            assert err <= RTOL, (b, k, err)
+        gg = g[:, b, :]
+        fin = np.isfinite(g_ref)
+        assert np.max(np.abs(gg[fin] - g_ref[fin]) / np.maximum(1.0, np.abs(g_ref[fin]))) <= 1e-9
+
+
+def test_batched_cost_parity():
+    l, N = 4, 500
+    etas = [0.05, 0.02, 0.1]
+    B = len(etas)
+    h = mmot_inputs.grid_h(N)
+    phis = [mmot_inputs.random_positive(9100 + b, l, N) for b in range(B)]
+    u = _planes([np.stack([np.log(phis[b][q]) for b in range(B)]) for q in range(l)])
+    ctx = mm.Context(l, N, etas, batch=B)
+    W = ctx.cost(u)
+    ctx.close()
+    for b in range(B):
+        W_ref = osk.cost(phis[b], h, etas[b])
+        assert abs(W[b] - W_ref) <= RTOL * abs(W_ref), (b, W[b], W_ref)
+
+
+def test_batched_c5_shape_sampled_instances():
+    """C5 shape (l=5, N=4096, per-instance eta, 3-component mixtures) at 64 instances; two
+    instances (smallest and largest eta) checked against the log-domain oracle after 3 sweeps."""
+    cfg = mmot_inputs.CONFIGS["C5"]
+    l, N, B, T = cfg.l, cfg.N, 64, 3
+    etas = mmot_inputs.c5_etas(B)
+    mus = [mmot_inputs.c5_marginals(b, N, l) for b in range(B)]
+    mu_d = _planes([np.stack([mus[b][q] for b in range(B)]) for q in range(l)])
+    ctx = mm.Context(l, N, list(etas), batch=B)
+    u = [torch.empty((B, N), dtype=torch.float64, device=DEV) for _ in range(l)]
+    ctx.init_uniform(u)
+    rep = ctx.sinkhorn(mu_d, T, 0.0, u)
+    assert rep["status"] == 0
+    g = np.stack([x.cpu().numpy() for x in u])
+    ctx.close()
+    h = mmot_inputs.grid_h(N)
+    for b in (int(np.argmin(etas)), int(np.argmax(etas))):
+        g_ref, _, _ = osk.sinkhorn(mus[b], h, etas[b], T, domain="log")
+        fin = np.isfinite(g_ref)
+        assert np.max(np.abs(g[:, b, :][fin] - g_ref[fin]) / np.maximum(1.0, np.abs(g_ref[fin]))) <= 1e-9, b
+
+
+def test_batched_argument_errors():
+    with pytest.raises(mm.MMOTError) as e:
+        mm.Context(4, 100, [0.1, -1.0], batch=2)
+    assert e.value.name == "MMOT_EINVAL"
+    with pytest.raises(mm.MMOTError) as e:
+        mm.Context(6, 100, [0.1], batch=1)
+    assert e.value.name == "MMOT_EUNSUPPORTED"
+    ctx = mm.Context(3, 50, [0.1, 0.2], batch=2)
+    mu = _planes([np.full((2, 50), 1 / 50.0)] * 3)
+    u = [torch.empty((2, 50), dtype=torch.float64, device=DEV) for _ in range(3)]
+    ctx.init_uniform(u)
+    with pytest.raises(mm.MMOTError) as e:
+        ctx.sinkhorn(mu, 5, 1e-6, u)
+    assert e.value.name == "MMOT_EUNSUPPORTED"
+    ctx.close()
