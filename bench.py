@@ -40,7 +40,7 @@ def _args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="mmot", choices=["mmot", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -125,21 +125,43 @@ def oracle_update_rate(cfg, mus, n_sample: int):
     return l * N / dt, dt
 
 
+def oracle_batched_rate(cfg, n_inst: int = 2, sweeps: int = 2):
+    """The CPU oracle as it stands (oracle/sinkhorn.py log-domain driver over oracle/regions.c,
+    single thread) on `n_inst` C5 instances x `sweeps` sweeps: elements/s in the metric's unit."""
+    from oracle import sinkhorn as osk
+    etas = mmot_inputs.c5_etas(n_inst)
+    h = mmot_inputs.grid_h(cfg.N)
+    t0 = time.perf_counter()
+    for b in range(n_inst):
+        mus = mmot_inputs.c5_marginals(b, cfg.N, cfg.l)
+        osk.sinkhorn(mus, h, float(etas[b]), sweeps, domain="log")
+    dt = time.perf_counter() - t0
+    elems = n_inst * sweeps * cfg.l * cfg.l * cfg.N
+    return elems / dt, dt
+
+
 def run_reference(args, cfg):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    n_sample = min(cfg.N, 10_000_000)
-    mus = mmot_inputs.make_marginals(cfg.name, 0, None if cfg.N <= 2_000_000 else n_sample)
     rates = []
-    for i in range(args.warmup + args.steps):
-        r, dt = oracle_update_rate(cfg, mus, n_sample)
-        if i >= args.warmup:
-            rates.append((r, dt))
+    if cfg.batch > 1:
+        for i in range(min(args.warmup, 1) + args.steps):
+            r, dt = oracle_batched_rate(cfg, 1, 2)
+            if i >= min(args.warmup, 1):
+                rates.append((r, dt))
+        sample = f"2 log-domain Sinkhorn sweeps of 1 {cfg.name} instance (l={cfg.l}, N={cfg.N})"
+    else:
+        n_sample = min(cfg.N, 10_000_000)
+        mus = mmot_inputs.make_marginals(cfg.name, 0, None if cfg.N <= 2_000_000 else n_sample)
+        for i in range(args.warmup + args.steps):
+            r, dt = oracle_update_rate(cfg, mus, n_sample)
+            if i >= args.warmup:
+                rates.append((r, dt))
+        sample = (f"one Sinkhorn update (J_0 by the oracle's region chains + division) on the first {n_sample} "
+                  f"grid points of {cfg.name}'s marginals, config lambda")
     value = statistics.median(r for r, _ in rates)
     ms = statistics.median(dt for _, dt in rates) * 1e3
-    sample = (f"one Sinkhorn update (J_0 by the oracle's region chains + division) on the first {n_sample} "
-              f"grid points of {cfg.name}'s marginals, config lambda")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -152,6 +174,133 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------------------------------
+FP64_PEAK = 148 * 64 * 2 * 1.965e9 / 1e12  # TFLOP/s: SMs x FP64 FMA/clk x 2 x max SM clock
+
+
+def run_batched(args, cfg):
+    """C5: `cfg.batch` independent instances sharded contiguously over the ranks, one batched
+    context per rank (no collective in the loop)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_19246_b200 as mm
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    l, N, T = cfg.l, cfg.N, cfg.iters
+    b0, b1 = rank * cfg.batch // ws, (rank + 1) * cfg.batch // ws
+    B = b1 - b0
+    etas = [float(e) for e in mmot_inputs.c5_etas(cfg.batch)[b0:b1]]
+    mus_h = mmot_inputs.c5_batch_marginals(b0, B, N, l)            # [l][B][N] fp64, seeded
+    mus_d = [torch.from_numpy(mus_h[q]).to(dev) for q in range(l)]
+    ctx = mm.Context(l, N, etas, batch=B, repr="log")
+    u = [torch.empty((B, N), dtype=torch.float64, device=dev) for _ in range(l)]
+    state = {}
+    stream = ctx.stream
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * max(args.steps, 1))]
+    sk_ms = []
+
+    def step(i=None):
+        ctx.init_uniform(u)
+        if i is not None:
+            ev[2 * i].record(stream)
+        state["rep"] = ctx.sinkhorn(mus_d, T, 0.0, u)
+        if i is not None:
+            ev[2 * i + 1].record(stream)
+        state["W"] = ctx.cost(u)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    launches0 = ctx.launches
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    sk_ms = [ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(args.steps)]
+    launches = (ctx.launches - launches0) // args.steps
+    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    evals_all = cfg.batch * T * l            # every rank's share, whole job
+    value = evals_all * l * N / (ms / 1e3)
+    # roofline of the dominant kernel (k_bat_sinkhorn, one launch per step): algorithmic FLOPs
+    # = 2 * 2^(l-1) (l+3) per grid point per update (SURVEY §8(d)), FP64 ALU peak
+    flop = B * T * l * N * 2 * (2 ** (l - 1)) * (l + 3)
+    sk = statistics.median(sk_ms)
+    achieved = flop / (sk / 1e3) / 1e12
+    roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK, "traffic": None,
+                "kernel": "k_bat_sinkhorn (all sweeps of all instances of the rank, one launch)",
+                "alg_flop_per_launch": flop, "ms_per_launch": sk,
+                "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5)"}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r, dt = oracle_batched_rate(cfg, 4, 2)
+        cpu = {"value": r, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"2 log-domain sweeps of 4 C5 instances (oracle region chains), {dt:.1f} s single-thread "
+                         f"of {os.cpu_count()} host cores"}
+    e2e = None
+    if not args.no_e2e:
+        # through the C ABI with host buffers: H2D of marginals + initial scalings, D2H of the
+        # final scalings and W, every step
+        mh = [torch.from_numpy(mus_h[q]).pin_memory() for q in range(l)]
+        uh = [torch.empty((B, N), dtype=torch.float64).pin_memory() for _ in range(l)]
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            md = [x.to(dev, non_blocking=True) for x in mh]
+            ctx.init_uniform(u)
+            ctx.sinkhorn(md, T, 0.0, u)
+            W = ctx.cost(u)
+            for q in range(l):
+                uh[q].copy_(u[q], non_blocking=True)
+            torch.cuda.synchronize()
+        barrier()
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = float(te.item())
+        e2e = {"value": evals_all * l * N / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": l * B * N * 8, "d2h_bytes_per_step": l * B * N * 8 + B * 8}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C5: {cfg.batch} instances x (l={l}, N={N}), eta_b ~ logU[1e-3,1e-1], "
+                                   f"T={T}, f64 arithmetic with per-chain exponents", "l": l, "N": N,
+                       "batch": cfg.batch, "iters": T, "parallelism": f"instances sharded over {ws} GPU(s)",
+                       "l2": "per-instance working set L2/SMEM resident; no flush (ALU-bound)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": int(launches), "iters_per_s": cfg.batch * T / (ms / 1e3),
+            "W_first": state["W"][0], "impl": "mmot",
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def run_mmot(args, cfg):
     import torch
     import torch.distributed as dist
@@ -294,6 +443,8 @@ def main():
     cfg = mmot_inputs.CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif cfg.batch > 1:
+        run_batched(args, cfg)
     else:
         run_mmot(args, cfg)
 

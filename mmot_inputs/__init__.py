@@ -23,7 +23,7 @@ import numpy as np
 __all__ = [
     "Config", "CONFIGS", "config", "grid_h", "gaussian_bump", "mixture",
     "c1_marginals", "c2_marginals", "c3_marginals", "c4_marginals",
-    "c5_marginals", "c5_etas", "random_marginals", "random_positive",
+    "c5_marginals", "c5_etas", "c5_batch_marginals", "random_marginals", "random_positive",
     "make_marginals",
 ]
 
@@ -142,6 +142,31 @@ def c5_marginals(b: int, N: int = 4096, l: int = 5) -> np.ndarray:
     rng = np.random.default_rng(1000 * 5 + b)
     rng.uniform(-3.0, -1.0)  # eta draw (see c5_etas) keeps the stream aligned
     return np.stack([_normalise(mixture(rng, N, 3)) for _ in range(l)])
+
+
+def c5_batch_marginals(b0: int, nb: int, N: int = 4096, l: int = 5) -> np.ndarray:
+    """C5 instances b0 .. b0+nb-1 as [l][nb][N] planes; identical values to c5_marginals(b)
+    (same per-instance draws, Gaussians evaluated in the same order, vectorised over instances)."""
+    x = _grid(N)
+    wts = np.empty((l, nb, 3))
+    mus = np.empty((l, nb, 3))
+    sds = np.empty((l, nb, 3))
+    for i in range(nb):
+        rng = np.random.default_rng(1000 * 5 + b0 + i)
+        rng.uniform(-3.0, -1.0)
+        for q in range(l):
+            wts[q, i] = rng.dirichlet(np.ones(3))
+            mus[q, i] = rng.uniform(0.2, 0.8, size=3)
+            sds[q, i] = rng.uniform(0.05, 0.15, size=3)
+    out = np.zeros((l, nb, N))
+    for q in range(l):
+        u = out[q]
+        for c in range(3):
+            m = mus[q, :, c][:, None]
+            sd = sds[q, :, c][:, None]
+            u += wts[q, :, c][:, None] * np.exp(-((x[None, :] - m) ** 2) / (2.0 * sd * sd))
+        u /= u.sum(axis=1, keepdims=True)
+    return out
 
 
 def random_marginals(seed: int, l: int, N: int, floor: float = 0.0) -> np.ndarray:

@@ -23,6 +23,7 @@
 //   5. chain operators (extended walk, prefix/suffix duality) of the next update's bound set.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "internal.h"
 #include "walk.cuh"
@@ -31,6 +32,7 @@ namespace mmot {
 
 constexpr int kBS = 8;          // slab = checkpoint block (points per chain)
 constexpr int kBWarps = 4;      // warps (instances) per CTA
+constexpr int kRenorm = 48;     // lazy renormalisation threshold: |max exponent of a chain| (products of l mantissas stay far inside fp64)
 
 // exact 2^n as a double (0 below the normal range, inf above)
 __device__ __forceinline__ double pow2i(int n) {
@@ -281,6 +283,8 @@ __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB 
     double *obuf = buf + 2 * NV * TILE;
     int emax = -1000000;
     const int e_true = sumE_bound + Ek;  // exponent of phi_k J_k's chain scale (MARG / COST)
+    const bool shok = Ek >= -1022 && Ek <= 1022;
+    const double shsc = MODE == MODE_UPD && shok ? pow2i(-Ek) : 1.0;  // UPD: Ek = pending shift of phi_k
     slab_issue<S, NV>(buf, vecs, 0, bp.P, N, 0, lane);
     cp_async_commit();
     for (int s = 0; s < ns; ++s) {
@@ -329,7 +333,7 @@ __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB 
                     const bool nz = nonzero(vk);
                     const int64_t x = x0 + (int64_t)s * S + jx;
                     bad |= nz && x < N && !finite_positive(q);
-                    const double o = nz ? q : 0.0;
+                    const double o = nz ? (shok ? q * shsc : scale2(q, -Ek)) : 0.0;
                     obuf[lane * (S + 1) + jx] = o;
                     if (nz) emax = max(emax, ilog2d(o));
                 } else if (MODE == MODE_MARG) {
@@ -377,6 +381,14 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
         int E[kMaxL];
 #pragma unroll
         for (int q = 0; q < kMaxL; ++q) E[q] = q < L ? bp.E[(inst * L + q) * 32 + lane] : 0;
+        int Sh[kMaxL];  // per marginal: exponent of E_q relative to -sum_{p != q} E_p (lazy renormalisation)
+#pragma unroll
+        for (int q = 0; q < kMaxL; ++q) {
+            int s2 = 0;
+#pragma unroll
+            for (int p = 0; p < L; ++p) s2 += E[p];
+            Sh[q] = q < L ? s2 : 0;  // E_q = -sum_{p != q} E_p + Sh_q  <=>  Sh_q = sum_p E_p
+        }
         bool bad = false;
         int fail = -1;
         bat_ops<NB, T>(bp, inst, 0, wt, buf, ops, lane);
@@ -391,17 +403,29 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
                     if (q != k) sumE += E[q];
                 double acc = 0.0;
                 bool b2 = false;
-                const int emax = bat_walk2<NB, T, MODE_UPD, 4>(bp, inst, k, wt, F, buf, ck, sumE, 0, acc, b2, lane);
+                // phit_k is written as (mu_k / J~) * 2^{-sh_k}, sh_k = the shift chosen at the previous
+                // update of marginal k (lazy renormalisation: fp64 leaves ~2^900 of headroom, so the
+                // chain is rescaled only when its maximum exponent drifts beyond +-kRenorm)
+                int shk = 0;
+#pragma unroll
+                for (int q = 0; q < L; ++q)
+                    if (q == k) shk = Sh[q];
+                const int emax = bat_walk2<NB, T, MODE_UPD, 4>(bp, inst, k, wt, F, buf, ck, sumE, shk, acc, b2, lane);
                 if (b2 && fail < 0) fail = t;
                 bad |= b2;
-                // renormalise phi_k of this chain: max mantissa in [1, 2)
-                const int sh = emax > -1000000 ? emax : 0;
-                __syncwarp();
-                bat_rescale(bp.phit[k] + inst * bp.N, x0, x1, sh);
+                int sh = shk;
+                if (emax > -1000000 && (emax > kRenorm || emax < -kRenorm)) {
+                    // (walk 2 ended with a __syncwarp after its last slab store: the chain is visible)
+                    bat_rescale(bp.phit[k] + inst * bp.N, x0, x1, emax);
+                    sh += emax;
+                }
                 __syncwarp();
 #pragma unroll
                 for (int q = 0; q < L; ++q)
-                    if (q == k) E[q] = -sumE + sh;
+                    if (q == k) {
+                        E[q] = -sumE + sh;
+                        Sh[q] = sh;
+                    }
                 // chain operators of the next update's bound set
                 bat_ops<NB, T>(bp, inst, (k + 1) % L, wt, buf, ops, lane);
             }
@@ -547,6 +571,7 @@ static size_t bat_smem() {
 }
 
 int64_t bat_slots(int l) {
+    if (const char *e = getenv("MMOT_BAT_SLOTS")) return atoll(e);  // experiments only
     int n = 0;
     const int NB = l - 1;
     auto q = [&](auto kern, size_t sm) {
