@@ -120,6 +120,32 @@ MMOT_API mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, m
 MMOT_API mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *eta_host, mmot_grid grid,
                                          mmot_dtype dt, const mmot_opts *opts, void *cuda_stream, mmot_ctx **out);
 
+/* Create rank `rank`'s part of ONE instance sharded over `world` GPUs by contiguous grid
+ * chunks (BASELINE C4 on 1/2/4/8 GPUs).  The rank owns global points
+ * [lo, hi) = mmot_shard_range(N_global, rank, world) of every vector; all array arguments of
+ * the compute calls are that rank's local chunks (hi - lo elements).  The grid spacing is the
+ * global h = (x_max - x_min)/(N_global - 1).  nccl_unique_id: 128 bytes from
+ * mmot_nccl_unique_id on one rank, broadcast by the caller (e.g. torch.distributed).  Every
+ * rank must make the same sequence of calls (each product performs one ncclAllGather of the
+ * whole-shard prefix/suffix operators, ~2 (l) 2^(l-1) doubles per rank; residual and cost one
+ * ncclAllReduce of a double).  Returns ENCCL if NCCL cannot be loaded or initialised. */
+MMOT_API mmot_status mmot_create_sharded(int l, int64_t N_global, double eta, mmot_grid grid, mmot_dtype dt,
+                                         const void *nccl_unique_id, int rank, int world, const mmot_opts *opts,
+                                         void *cuda_stream, mmot_ctx **out);
+
+/* 128-byte NCCL unique id for mmot_create_sharded (host memory). */
+MMOT_API mmot_status mmot_nccl_unique_id(void *out);
+
+/* Grid chunk [*lo, *hi) of `rank` out of `world` for N_global points: lo = floor(rank N / world). */
+MMOT_API void mmot_shard_range(int64_t N_global, int rank, int world, int64_t *lo, int64_t *hi);
+
+/* Host reference of the carry composition the sharded contexts run on device (no GPU needed):
+ * ops_all = [world][2][l 2^(l-1)] gathered whole-shard operators (prefix, suffix; entry
+ * G_c[S] at c 2^(l-1) + S, c = 0..l-1, S a subset of the l-1 bound marginals), fin / bin =
+ * the 2^(l-1) prefix / suffix states entering shard `rank` from the left / right. */
+MMOT_API mmot_status mmot_compose_rank_carries(int l, const double *ops_all, int world, int rank, double *fin,
+                                               double *bin);
+
 /* m_k = phi_k * J_k(phi_{-k}) -- the k-th marginal of K . (phi_1 x ... x phi_l)
  * (P:1021), computed by the O(N) separated-summation scans.
  *   k in [0, l); u: host array of l device pointers (repr per opts, float64, length N each);

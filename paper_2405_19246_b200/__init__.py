@@ -12,7 +12,8 @@ import math
 import os
 from typing import List, Optional, Sequence
 
-__all__ = ["Context", "MMOTError", "lib_path", "load_library", "STATUS", "exported_symbols"]
+__all__ = ["Context", "MMOTError", "lib_path", "load_library", "STATUS", "exported_symbols", "nccl_unique_id",
+           "shard_range", "compose_rank_carries"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libmmot.so")
@@ -70,6 +71,17 @@ def load_library():
     lib.mmot_create_batched.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
                                         _Grid, ctypes.c_int, ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
     lib.mmot_create_batched.restype = ctypes.c_int
+    lib.mmot_create_sharded.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_double, _Grid, ctypes.c_int, vp,
+                                        ctypes.c_int, ctypes.c_int, ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
+    lib.mmot_create_sharded.restype = ctypes.c_int
+    lib.mmot_nccl_unique_id.argtypes = [vp]
+    lib.mmot_nccl_unique_id.restype = ctypes.c_int
+    lib.mmot_shard_range.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
+                                     ctypes.POINTER(ctypes.c_int64)]
+    lib.mmot_shard_range.restype = None
+    dpp = ctypes.POINTER(ctypes.c_double)
+    lib.mmot_compose_rank_carries.argtypes = [ctypes.c_int, dpp, ctypes.c_int, ctypes.c_int, dpp, dpp]
+    lib.mmot_compose_rank_carries.restype = ctypes.c_int
     lib.mmot_marginal.argtypes = [vp, ctypes.c_int, vpp, vp]
     lib.mmot_marginal.restype = ctypes.c_int
     lib.mmot_sinkhorn.argtypes = [vp, vpp, ctypes.c_int, ctypes.c_double, vpp, ctypes.POINTER(_Report)]
@@ -116,6 +128,40 @@ def _ptr_array(ptrs: Sequence[int]):
     return arr
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for a sharded context (create on one rank, broadcast)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    st = lib.mmot_nccl_unique_id(buf)
+    if st != 0:
+        raise MMOTError(st, lib.mmot_last_error(None).decode())
+    return buf.raw
+
+
+def shard_range(N_global: int, rank: int, world: int):
+    """Grid chunk [lo, hi) owned by `rank` (host logic of the C ABI, no GPU needed)."""
+    lib = load_library()
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    lib.mmot_shard_range(int(N_global), int(rank), int(world), ctypes.byref(lo), ctypes.byref(hi))
+    return lo.value, hi.value
+
+
+def compose_rank_carries(l: int, ops_all, world: int, rank: int):
+    """Host reference of the sharded carry composition (C ABI, no GPU needed).
+    ops_all: float64 array [world][2][l * 2**(l-1)].  Returns (fin, bin) arrays of 2**(l-1)."""
+    import numpy as np
+    lib = load_library()
+    a = np.ascontiguousarray(ops_all, dtype=np.float64)
+    M = 1 << (l - 1)
+    fin, bin_ = np.zeros(M), np.zeros(M)
+    dp = ctypes.POINTER(ctypes.c_double)
+    st = lib.mmot_compose_rank_carries(int(l), a.ctypes.data_as(dp), int(world), int(rank), fin.ctypes.data_as(dp),
+                                       bin_.ctypes.data_as(dp))
+    if st != 0:
+        raise MMOTError(st, lib.mmot_last_error(None).decode())
+    return fin, bin_
+
+
 class Context:
     """One MMOT problem shape (l, N, eta, grid) with its device workspace.
 
@@ -125,7 +171,7 @@ class Context:
 
     def __init__(self, l: int, N: int, eta, grid=(0.0, 1.0), dtype: str = "f64",
                  repr: str = "log", check_every: int = 0, chunk: int = 0, stream=None,
-                 kernel: str = "auto", batch: Optional[int] = None):
+                 kernel: str = "auto", batch: Optional[int] = None, shard=None):
         """Single instance (eta: float), or a batched context (batch=B, eta: B per-instance
         values) whose array arguments are [B][N] planes (mmot_create_batched)."""
         import torch
@@ -142,7 +188,18 @@ class Context:
         kern = {"auto": 0, "two_walk": 1, "single_walk": 2}[kernel]
         opts = _Opts(int(check_every), 0, LOG if repr == "log" else LINEAR, int(chunk), kern)
         ctx = ctypes.c_void_p()
-        if self.batch is None:
+        self.shard = shard
+        if shard is not None:
+            rank, world, uid = shard
+            self.N_global = self.N
+            lo, hi = shard_range(self.N, rank, world)
+            self.N = hi - lo
+            idb = ctypes.create_string_buffer(bytes(uid), 128)
+            st = self._lib.mmot_create_sharded(self.l, self.N_global, float(eta), _Grid(*self.grid),
+                                               F64 if dtype == "f64" else F32, idb, int(rank), int(world),
+                                               ctypes.byref(opts), ctypes.c_void_p(self.stream.cuda_stream),
+                                               ctypes.byref(ctx))
+        elif self.batch is None:
             st = self._lib.mmot_create(self.l, self.N, self.eta, _Grid(*self.grid), F64 if dtype == "f64" else F32,
                                        ctypes.byref(opts), ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx))
         else:

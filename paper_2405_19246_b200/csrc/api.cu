@@ -1,6 +1,7 @@
 // api.cu -- the C ABI declared in include/mmot.h: argument validation, context workspace,
 // and the device-resident Sinkhorn driver (Algorithm 4).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -17,6 +18,10 @@ using mmot::Plan;
 
 namespace {
 
+struct ncclUniqueIdBytes {
+    char internal[128];
+};
+
 struct DevScalars {
     int stop;
     int status;
@@ -32,6 +37,40 @@ struct DevScalars {
 };
 
 char g_err[256] = "";
+
+// ---------------------------------------------------------------------------------------
+// NCCL, resolved at run time from the libnccl.so.2 already loaded in the process (PyTorch's)
+// or the system one, so the library never pins an NCCL version at link time.
+typedef int nccl_result;
+typedef void *nccl_comm;
+struct NcclApi {
+    bool tried = false, ok = false;
+    nccl_result (*GetUniqueId)(void *);
+    nccl_result (*CommInitRank)(nccl_comm *, int, ncclUniqueIdBytes, int);
+    nccl_result (*CommDestroy)(nccl_comm);
+    nccl_result (*AllGather)(const void *, void *, size_t, int, nccl_comm, cudaStream_t);
+    nccl_result (*AllReduce)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t);
+    const char *(*GetErrorString)(nccl_result);
+};
+NcclApi g_nccl;
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+
+bool nccl_load() {
+    if (g_nccl.tried) return g_nccl.ok;
+    g_nccl.tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    g_nccl.GetUniqueId = (nccl_result(*)(void *))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (nccl_result(*)(nccl_comm *, int, ncclUniqueIdBytes, int))dlsym(h, "ncclCommInitRank");
+    g_nccl.CommDestroy = (nccl_result(*)(nccl_comm))dlsym(h, "ncclCommDestroy");
+    g_nccl.AllGather = (nccl_result(*)(const void *, void *, size_t, int, nccl_comm, cudaStream_t))dlsym(h, "ncclAllGather");
+    g_nccl.AllReduce = (nccl_result(*)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclAllReduce");
+    g_nccl.GetErrorString = (const char *(*)(nccl_result))dlsym(h, "ncclGetErrorString");
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllGather && g_nccl.AllReduce &&
+                g_nccl.GetErrorString;
+    return g_nccl.ok;
+}
 
 }  // namespace
 
@@ -60,6 +99,13 @@ struct mmot_ctx {
     int64_t nchp = 0;                       // sw: chains rounded up to 32 (transposed row length)
     double *mu_t[mmot::kMaxL] = {nullptr};  // sw: marginals in the chain-transposed layout
     double *out_t = nullptr;                // sw: marginal output in the chain-transposed layout
+    // sharded contexts (mmot_create_sharded)
+    bool sharded = false;
+    int rank = 0, world = 1;
+    int64_t N_global = 0, lo = 0;
+    nccl_comm comm = nullptr;
+    double *shard_mem = nullptr;            // agg_send [2*SZ], agg_all [world*2*SZ], rank_car [2*M] (Dual-sized)
+    int exch_error = 0;
     // batched contexts (mmot_create_batched)
     bool batched = false;
     int64_t batch = 1;
@@ -159,6 +205,8 @@ void mmot_destroy(mmot_ctx *ctx) {
     cudaFree(ctx->ws);
     cudaFree(ctx->out_t);
     cudaFree(ctx->bat_mem);
+    cudaFree(ctx->shard_mem);
+    if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
     cudaFree(ctx->bat_int);
     cudaFree(ctx->bat_ptrs);
     if (ctx->bat_whost) cudaFreeHost(ctx->bat_whost);
@@ -504,6 +552,28 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
 }
 
 // ---------------------------------------------------------------------------------------
+// Sharded contexts: all-gather of the whole-shard operators ([2][SZ] elements of elem_bytes)
+// on the context stream (called from inside the scan, between up-sweep and down-sweep).
+static void shard_exchange(void *vctx, int elem_bytes, cudaStream_t s) {
+    mmot_ctx *c = static_cast<mmot_ctx *>(vctx);
+    const size_t SZ = (size_t)c->l * (1 << (c->l - 1));
+    const size_t n = 2 * SZ * (size_t)(elem_bytes / 8);
+    const nccl_result r = g_nccl.AllGather(c->shard_mem, c->shard_mem + 2 * SZ * 2, n, kNcclFloat64, c->comm, s);
+    if (r != 0 && !c->exch_error) {
+        c->exch_error = r;
+        set_err(c, "ncclAllGather: %s", g_nccl.GetErrorString(r));
+    }
+}
+
+// Sum a device double over the ranks (residual, cost) in place.
+static mmot_status shard_allreduce(mmot_ctx *c, double *dev) {
+    if (!c->sharded || c->world == 1) return MMOT_OK;
+    const nccl_result r = g_nccl.AllReduce(dev, dev, 1, kNcclFloat64, kNcclSum, c->comm, c->stream);
+    if (r != 0) { set_err(c, "ncclAllReduce: %s", g_nccl.GetErrorString(r)); return MMOT_ENCCL; }
+    return MMOT_OK;
+}
+
+// ---------------------------------------------------------------------------------------
 static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double *mu, double *out, int iter) {
     Plan p{};
     p.NB = c->l - 1;
@@ -530,6 +600,17 @@ static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double
     p.sw = c->sw ? 1 : 0;
     p.nchp = c->nchp;
     if (c->sw && mu) p.muk = c->mu_t[k];
+    if (c->sharded) {
+        const int M = 1 << (c->l - 1);
+        const size_t SZ = (size_t)c->l * M;  // (NB+1) * 2^NB, in Dual units below
+        p.exch = shard_exchange;
+        p.exch_ctx = c;
+        p.agg_send = c->shard_mem;
+        p.agg_all = c->shard_mem + 2 * SZ * 2;
+        p.rank_car = c->shard_mem + 2 * SZ * 2 + (size_t)c->world * 2 * SZ * 2;
+        p.world = c->world;
+        p.rank = c->rank;
+    }
     p.partial = c->partial;
     p.stop = &c->dsc->stop;
     p.status = &c->dsc->status;
@@ -620,6 +701,8 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
                 CK(c, mmot::launch_sum(c->partial, c->nchunks, &c->dsc->res_acc, 1.0, k > 0, &c->dsc->stop, c->stream,
                                        &c->launches));
             }
+            st = shard_allreduce(c, &c->dsc->res_acc);
+            if (st) return st;
             CK(c, mmot::launch_resid_finish(&c->dsc->res_acc, tol, t, &c->dsc->resid, &c->dsc->iters_done,
                                             &c->dsc->converged, &c->dsc->stop, c->stream, &c->launches));
         } else {
@@ -641,6 +724,7 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
     }
     st = sync_report(c);
     if (st) return st;
+    if (c->exch_error) return MMOT_ENCCL;
     const DevScalars &h = *c->hsc;
     if (rep) {
         rep->iters_done = h.iters_done;
@@ -747,6 +831,8 @@ mmot_status mmot_cost(mmot_ctx *c, const void *const *u, double *W) {
     Plan p = make_plan(c, k, lin, nullptr, nullptr, 0);
     CK(c, mmot::launch_product(p, mmot::MODE_COST, c->stream, &c->launches, prof_events(c, mmot::MODE_COST)));
     CK(c, mmot::launch_sum(c->partial, c->nchunks, &c->dsc->W, c->h, 0, &c->dsc->stop, c->stream, &c->launches));
+    st = shard_allreduce(c, &c->dsc->W);
+    if (st) return st;
     st = sync_report(c);
     if (st) return st;
     *W = c->hsc->W;
@@ -791,6 +877,87 @@ mmot_status mmot_init_uniform(mmot_ctx *c, void *const *u) {
         if (!u[q]) { set_err(c, "u[%d] is NULL", q); return MMOT_EINVAL; }
         CK(c, mmot::launch_fill(static_cast<double *>(u[q]), v, c->N * c->batch, c->stream, &c->launches));
     }
+    return MMOT_OK;
+}
+
+mmot_status mmot_nccl_unique_id(void *out) {
+    if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
+    if (!nccl_load()) { set_err(nullptr, "libnccl.so.2 not found"); return MMOT_ENCCL; }
+    const nccl_result r = g_nccl.GetUniqueId(out);
+    if (r != 0) { set_err(nullptr, "ncclGetUniqueId: %s", g_nccl.GetErrorString(r)); return MMOT_ENCCL; }
+    return MMOT_OK;
+}
+
+void mmot_shard_range(int64_t N_global, int rank, int world, int64_t *lo, int64_t *hi) {
+    if (lo) *lo = world > 0 ? (int64_t)((__int128)N_global * rank / world) : 0;
+    if (hi) *hi = world > 0 ? (int64_t)((__int128)N_global * (rank + 1) / world) : 0;
+}
+
+mmot_status mmot_compose_rank_carries(int l, const double *ops_all, int world, int rank, double *fin, double *bin) {
+    if (!ops_all || !fin || !bin || world < 1 || rank < 0 || rank >= world) { set_err(nullptr, "bad arguments"); return MMOT_EINVAL; }
+    switch (l - 1) {
+        case 1: mmot::compose_rank_carries<1, double>(ops_all, world, rank, fin, bin); break;
+        case 2: mmot::compose_rank_carries<2, double>(ops_all, world, rank, fin, bin); break;
+        case 3: mmot::compose_rank_carries<3, double>(ops_all, world, rank, fin, bin); break;
+        case 4: mmot::compose_rank_carries<4, double>(ops_all, world, rank, fin, bin); break;
+        case 5: mmot::compose_rank_carries<5, double>(ops_all, world, rank, fin, bin); break;
+        default: set_err(nullptr, "l=%d unsupported", l); return MMOT_EINVAL;
+    }
+    return MMOT_OK;
+}
+
+mmot_status mmot_create_sharded(int l, int64_t N_global, double eta, mmot_grid grid, mmot_dtype dt,
+                                const void *nccl_unique_id, int rank, int world, const mmot_opts *opts,
+                                void *cuda_stream, mmot_ctx **out) {
+    if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
+    *out = nullptr;
+    if (!nccl_unique_id || world < 1 || rank < 0 || rank >= world) { set_err(nullptr, "bad rank/world/id"); return MMOT_EINVAL; }
+    int64_t lo, hi;
+    mmot_shard_range(N_global, rank, world, &lo, &hi);
+    if (N_global < world) { set_err(nullptr, "N_global=%lld < world=%d", (long long)N_global, world); return MMOT_ESHAPE; }
+    // the shard's grid: same spacing h as the global grid, x_min shifted to the shard start
+    const double h = N_global > 1 ? (grid.x_max - grid.x_min) / (double)(N_global - 1) : 1.0;
+    mmot_grid g2{grid.x_min + lo * h, grid.x_min + (hi - 1) * h};
+    if (hi - lo == 1) g2.x_max = g2.x_min + h;  // a 1-point shard keeps the global h below
+    mmot_ctx *c = nullptr;
+    mmot_status st = mmot_create(l, hi - lo, eta, g2, dt, opts, cuda_stream, &c);
+    if (st) return st;
+    c->h = h;
+    for (int a = 0; a <= mmot::kMaxL; ++a) {
+        const int e = a <= l ? a * (l - a) : 0;
+        c->W.w[a] = a <= l ? exp(-(double)e * h / eta) : 0.0;
+    }
+    c->sharded = true;
+    c->rank = rank;
+    c->world = world;
+    c->N_global = N_global;
+    c->lo = lo;
+    c->grid = grid;
+    const size_t SZ = (size_t)l * (1 << (l - 1));
+    const size_t nd = (2 * SZ + (size_t)world * 2 * SZ + 2 * (1 << (l - 1))) * 2;  // Dual-sized
+    if (cudaMalloc(&c->shard_mem, nd * sizeof(double)) != cudaSuccess) {
+        set_err(c, "shard workspace allocation failed");
+        snprintf(g_err, sizeof g_err, "%s", c->err);
+        mmot_destroy(c);
+        return MMOT_ENOMEM;
+    }
+    if (!nccl_load()) {
+        set_err(c, "libnccl.so.2 not found");
+        snprintf(g_err, sizeof g_err, "%s", c->err);
+        mmot_destroy(c);
+        return MMOT_ENCCL;
+    }
+    ncclUniqueIdBytes id;
+    memcpy(id.internal, nccl_unique_id, sizeof id.internal);
+    const nccl_result r = g_nccl.CommInitRank(&c->comm, world, id, rank);
+    if (r != 0) {
+        set_err(c, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+        snprintf(g_err, sizeof g_err, "%s", c->err);
+        c->comm = nullptr;
+        mmot_destroy(c);
+        return MMOT_ENCCL;
+    }
+    *out = c;
     return MMOT_OK;
 }
 

@@ -30,6 +30,7 @@
 // parallel (hierarchical) scan over chunks.
 #pragma once
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 namespace mmot {
@@ -54,16 +55,16 @@ struct Dual {
     double v, d;
 };
 
-__device__ __forceinline__ double zero_of(double) { return 0.0; }
+__host__ __device__ __forceinline__ double zero_of(double) { return 0.0; }
 __device__ __forceinline__ Dual zero_of(Dual) { return Dual{0.0, 0.0}; }
-__device__ __forceinline__ double one_of(double) { return 1.0; }
+__host__ __device__ __forceinline__ double one_of(double) { return 1.0; }
 __device__ __forceinline__ Dual one_of(Dual) { return Dual{1.0, 0.0}; }
 
 // a * b
-__device__ __forceinline__ double mul(double a, double b) { return a * b; }
+__host__ __device__ __forceinline__ double mul(double a, double b) { return a * b; }
 __device__ __forceinline__ Dual mul(Dual a, Dual b) { return Dual{a.v * b.v, fma(a.d, b.v, a.v * b.d)}; }
 // acc + a * b
-__device__ __forceinline__ double mad(double a, double b, double acc) { return fma(a, b, acc); }
+__host__ __device__ __forceinline__ double mad(double a, double b, double acc) { return fma(a, b, acc); }
 __device__ __forceinline__ Dual mad(Dual a, Dual b, Dual acc) {
     return Dual{fma(a.v, b.v, acc.v), fma(a.d, b.v, fma(a.v, b.d, acc.d))};
 }
@@ -237,7 +238,7 @@ __device__ __forceinline__ void opx_store(const T (&G)[NB + 1][1 << NB], const T
 
 // out = Op(in):  out[S] = sum_{U subset S} in[U] * G[|U|][S\U]
 template <int NB, typename T>
-__device__ __forceinline__ void op_apply(const T (&G)[NB + 1][1 << NB], const T (&in)[1 << NB], T (&out)[1 << NB]) {
+__host__ __device__ __forceinline__ void op_apply(const T (&G)[NB + 1][1 << NB], const T (&in)[1 << NB], T (&out)[1 << NB]) {
 #pragma unroll
     for (int S = 0; S < (1 << NB); ++S) {
         T acc = zero_of(T{});
@@ -267,7 +268,7 @@ __device__ __forceinline__ void op_compose(const T (&A)[NB + 1][1 << NB], const 
 }
 
 template <int NB, typename T>
-__device__ __forceinline__ void op_load(T (&G)[NB + 1][1 << NB], const T *p) {
+__host__ __device__ __forceinline__ void op_load(T (&G)[NB + 1][1 << NB], const T *p) {
 #pragma unroll
     for (int c = 0; c <= NB; ++c)
 #pragma unroll
@@ -296,9 +297,36 @@ __device__ __forceinline__ void vec_store(const T (&v)[1 << NB], T *p) {
     for (int S = 0; S < (1 << NB); ++S) p[S] = v[S];
 }
 template <int NB, typename T>
-__device__ __forceinline__ void vec_unit(T (&v)[1 << NB]) {
+__host__ __device__ __forceinline__ void vec_unit(T (&v)[1 << NB]) {
 #pragma unroll
     for (int S = 0; S < (1 << NB); ++S) v[S] = (S == 0) ? one_of(T{}) : zero_of(T{});
+}
+
+// ---------------------------------------------------------------------------------------
+// Multi-GPU (sharded contexts): rank g owns a contiguous grid chunk; after the scan every rank
+// holds its whole-chunk prefix operator Gg and suffix operator Rg (the composition of all its
+// chain operators).  The carry entering rank g from the left is G_{g-1} o ... o G_0 (e_{}),
+// the one entering from the right is R_{g+1} o ... o R_{G-1} (e_{}).  `all` holds the gathered
+// [world][2][SZ] operators (prefix, suffix) in op_store layout.  Same code on host and device.
+template <int NB, typename T>
+__host__ __device__ inline void compose_rank_carries(const T *all, int world, int rank, T *fin, T *bin) {
+    constexpr int M = 1 << NB;
+    constexpr int SZ = (NB + 1) * M;
+    T cur[M], nxt[M], G[NB + 1][M];
+    vec_unit<NB, T>(cur);
+    for (int r = 0; r < rank; ++r) {
+        op_load<NB, T>(G, all + ((size_t)r * 2 + 0) * SZ);
+        op_apply<NB, T>(G, cur, nxt);
+        for (int S = 0; S < M; ++S) cur[S] = nxt[S];
+    }
+    for (int S = 0; S < M; ++S) fin[S] = cur[S];
+    vec_unit<NB, T>(cur);
+    for (int r = world - 1; r > rank; --r) {
+        op_load<NB, T>(G, all + ((size_t)r * 2 + 1) * SZ);
+        op_apply<NB, T>(G, cur, nxt);
+        for (int S = 0; S < M; ++S) cur[S] = nxt[S];
+    }
+    for (int S = 0; S < M; ++S) bin[S] = cur[S];
 }
 
 }  // namespace mmot

@@ -41,6 +41,13 @@ struct Plan {
     int sw;                          // 1: single-walk kernels (stable regime, see mmot_create); vectors are
                                      //    then in the chain-blocked layout ((c/32)*32P + t*32 + c%32)
     int64_t nchp;                    // chain count rounded up to 32 (transposed row length)
+    // sharded contexts (mmot_create_sharded): after the up-sweep the whole-shard operators are
+    // written to agg_send ([2][SZ]: prefix, suffix), exch() all-gathers them into agg_all
+    // ([world][2][SZ]) on the stream, and the carries entering the shard go to rank_car ([2][M])
+    void (*exch)(void *ctx, int elem_bytes, cudaStream_t s);
+    void *exch_ctx;
+    void *agg_send, *agg_all, *rank_car;
+    int world, rank;
     double *partial;                 // nchunks partial sums
     int *stop;                       // device flag: nonzero -> every kernel returns at once
     int *status;                     // device status (mmot_status) of the run

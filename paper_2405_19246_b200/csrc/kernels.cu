@@ -1100,6 +1100,11 @@ static void launch_apply(const Plan &p, int64_t /*nb*/, int /*tpb*/, cudaStream_
 
 // ---------------------------------------------------------------------------------------
 template <int NB, typename T>
+__global__ void k_compose(const T *all, int world, int rank, T *car) {
+    if (threadIdx.x == 0) compose_rank_carries<NB, T>(all, world, rank, car, car + (1 << NB));
+}
+
+template <int NB, typename T>
 static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *launches, cudaEvent_t *ev,
                               bool with_ops, bool next) {
     const int tpb = kWarpsPerCta * 32;
@@ -1128,6 +1133,7 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
     }
     if (ev) cudaEventRecord(ev[1], s);
     constexpr bool kWarpScan = NB <= 3 && sizeof(T) == sizeof(double);
+    const int top = p.nlev - 1;
     // up-sweep
     for (int i = 0; i + 1 < p.nlev; ++i) {
         const int64_t ng = p.nlev_n[i + 1];
@@ -1146,12 +1152,36 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
                                                p.nlev_n[i], p.stop);
         ++*launches;
     }
+    // sharded contexts: whole-shard operators (top level reduced to one), exchanged between the
+    // ranks, composed into the carries entering this shard (compose_rank_carries)
+    if (p.exch) {
+        if constexpr (kWarpScan) {
+            k_ops_reduce_w<NB><<<dim3(1, 2), 128, 0, s>>>(static_cast<const double *>(p.ops_f[top]),
+                                                          static_cast<const double *>(p.ops_b[top]),
+                                                          static_cast<double *>(p.agg_send),
+                                                          static_cast<double *>(p.agg_send) + OpShape<NB>::SZ,
+                                                          p.nlev_n[top], p.stop);
+        } else {
+            k_ops_reduce<NB, T><<<dim3(1, 2), 64, 0, s>>>(static_cast<const T *>(p.ops_f[top]),
+                                                         static_cast<const T *>(p.ops_b[top]),
+                                                         static_cast<T *>(p.agg_send),
+                                                         static_cast<T *>(p.agg_send) + OpShape<NB>::SZ,
+                                                         p.nlev_n[top], p.stop);
+        }
+        ++*launches;
+        p.exch(p.exch_ctx, (int)sizeof(T), s);
+        k_compose<NB, T><<<1, 1, 0, s>>>(static_cast<const T *>(p.agg_all), p.world, p.rank,
+                                         static_cast<T *>(p.rank_car));
+        ++*launches;
+    }
     // down-sweep
     for (int i = p.nlev - 1; i >= 0; --i) {
         const int64_t ng = (p.nlev_n[i] + kGroup - 1) / kGroup;
         dim3 grid((unsigned)((ng + 63) / 64), 2);
-        const T *gf = i + 1 < p.nlev ? static_cast<const T *>(p.car_f[i + 1]) : nullptr;
-        const T *gb = i + 1 < p.nlev ? static_cast<const T *>(p.car_b[i + 1]) : nullptr;
+        const T *gf = i + 1 < p.nlev ? static_cast<const T *>(p.car_f[i + 1])
+                                     : (p.exch ? static_cast<const T *>(p.rank_car) : nullptr);
+        const T *gb = i + 1 < p.nlev ? static_cast<const T *>(p.car_b[i + 1])
+                                     : (p.exch ? static_cast<const T *>(p.rank_car) + (1 << NB) : nullptr);
         if constexpr (kWarpScan) {
             dim3 gridw((unsigned)((ng + 3) / 4), 2);
             k_ops_down_w<NB><<<gridw, 128, 0, s>>>(static_cast<const double *>(p.ops_f[i]),
