@@ -297,6 +297,7 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
         } else {
             const int64_t target2 = 148 * 256;
             P = (N + target2 - 1) / target2;
+            if (NB >= 4) P = pmax;  // heavy operators: as few chains as the checkpoint store allows
             P = ((P + q - 1) / q) * q;
             P = std::max<int64_t>(q, std::min<int64_t>(P, pmax));
         }
@@ -307,10 +308,11 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
     // levels of the hierarchical operator scan
     int64_t n = c->nchunks;
     c->nlev = 0;
+    const int grp = mmot::group_of(NB);
     while (true) {
         c->nlev_n[c->nlev++] = n;
-        if (n <= mmot::kGroup || c->nlev == mmot::kMaxLevels) break;
-        n = (n + mmot::kGroup - 1) / mmot::kGroup;
+        if (n <= grp || c->nlev == mmot::kMaxLevels) break;
+        n = (n + grp - 1) / grp;
     }
     // workspace, sized for dual numbers (the cost) so every mode fits
     const int M = 1 << NB;
@@ -691,7 +693,7 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
             Plan p = make_plan(c, k, lin, mu[k], lin[k], t);
             CK(c, mmot::launch_product(p, mmot::MODE_UPD, c->stream, &c->launches, prof_events(c, mmot::MODE_UPD),
                                        ops_for != k, true));
-            ops_for = (k + 1) % l;
+            ops_for = l <= 5 ? (k + 1) % l : -1;  // l = 6: next-update operators are not fused (registers)
         }
         if (tol > 0 && (t % check_every == 0 || t == iters)) {
             for (int k = 0; k + 1 < l; ++k) {

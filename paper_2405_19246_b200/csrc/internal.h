@@ -14,7 +14,10 @@ enum Mode : int {
     MODE_COST = 3,  // partial[c] = sum phi_k * hatJ_k (duals)   (W)
 };
 
-constexpr int kGroup = 32;
+constexpr int kGroup = 32;  // operators per group of the hierarchical scan when NB <= 3 (one warp)
+// NB >= 4 composes a group sequentially in one thread (an op_compose of 2^NB-state operators is
+// heavy): smaller groups shorten that serial chain at the price of more levels.
+__host__ __device__ constexpr int group_of(int NB) { return NB <= 3 ? 32 : 8; }
 constexpr double kSwBound = 1.0;   // max P * max_a a(l-a) * h/eta for the single-walk kernels      // operators composed per thread in the hierarchical scan
 constexpr int kMaxLevels = 8;
 

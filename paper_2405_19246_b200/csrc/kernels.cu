@@ -86,9 +86,9 @@ __global__ void __launch_bounds__(64) k_ops_reduce(const T *in_f, const T *in_b,
     constexpr int M = 1 << NB;
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int dir = blockIdx.y;
-    const int64_t first = g * kGroup;
+    const int64_t first = g * group_of(NB);
     if (first >= n_in || *stop) return;
-    const int64_t last = min(n_in, first + kGroup) - 1;
+    const int64_t last = min(n_in, first + group_of(NB)) - 1;
     const T *in = dir == 0 ? in_f : in_b;
     T *out = dir == 0 ? out_f : out_b;
     T A[NB + 1][M], B[NB + 1][M], C[NB + 1][M];
@@ -125,9 +125,9 @@ __global__ void __launch_bounds__(64) k_ops_down(const T *ops_f, const T *ops_b,
     constexpr int M = 1 << NB;
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int dir = blockIdx.y;
-    const int64_t first = g * kGroup;
+    const int64_t first = g * group_of(NB);
     if (first >= n_in || *stop) return;
-    const int64_t last = min(n_in, first + kGroup) - 1;
+    const int64_t last = min(n_in, first + group_of(NB)) - 1;
     const T *ops = dir == 0 ? ops_f : ops_b;
     const T *gc = dir == 0 ? gcar_f : gcar_b;
     T *car = dir == 0 ? car_f : car_b;
@@ -153,6 +153,105 @@ __global__ void __launch_bounds__(64) k_ops_down(const T *ops_f, const T *ops_b,
             for (int S = 0; S < M; ++S) cur[S] = nxt[S];
             if (car_bi) vec_store<NB, T>(cur, car_bi + i * M);  // inclusive: suffix state at chain start
         }
+    }
+}
+
+// Block-cooperative variants of phase 2 for large operators (NB >= 4): a group of group_of(NB)
+// operators is staged in shared memory and every output entry (c, V) of a composition / every
+// state of an application is computed by its own thread, so the serial chain per group is
+// log2(group) compositions (reduce) or group applications of depth one (down).
+template <int NB>
+__device__ __forceinline__ bool opx_valid(int e) {  // entry e = c*M + V is a used operator entry
+    constexpr int M = 1 << NB;
+    return pc(e % M) <= NB - e / M;
+}
+
+template <int NB, typename T>
+__global__ void __launch_bounds__(128) k_ops_reduce_c(const T *in_f, const T *in_b, T *out_f, T *out_b, int64_t n_in,
+                                                       const int *stop) {
+    constexpr int M = 1 << NB;
+    constexpr int SZ = OpShape<NB>::SZ;
+    constexpr int GS = group_of(NB);
+    __shared__ T A[GS][SZ];
+    const int64_t g = blockIdx.x;
+    const int dir = blockIdx.y;
+    const int64_t first = g * GS;
+    if (first >= n_in || *stop) return;
+    const int cnt = (int)min((int64_t)GS, n_in - first);
+    const T *in = (dir == 0 ? in_f : in_b) + first * SZ;
+    for (int e = threadIdx.x; e < GS * SZ; e += blockDim.x) {
+        const int i = e / SZ, q = e % SZ;
+        A[i][q] = i < cnt && opx_valid<NB>(q) ? in[e] : ((q % M) == 0 && i >= cnt ? one_of(T{}) : zero_of(T{}));
+    }
+    __syncthreads();
+    for (int step = 1; step < GS; step <<= 1) {
+        // pairs (i, i + step), i a multiple of 2 step; prefix order applies member i first,
+        // suffix order applies member i + step first
+        T res[(GS * SZ + 127) / 128];
+        int nres = 0;
+        for (int e = threadIdx.x; e < (GS / (2 * step)) * SZ; e += blockDim.x) {
+            const int pr = e / SZ, q = e % SZ;
+            const int c = q / M, V = q % M;
+            const int i = pr * 2 * step;
+            const T *X = dir == 0 ? A[i] : A[i + step];      // applied first
+            const T *Y = dir == 0 ? A[i + step] : A[i];      // applied second
+            T acc = zero_of(T{});
+            if (pc(V) <= NB - c)
+                for (int U = V;; U = (U - 1) & V) {          // C_c[V] = sum_{U subset V} X_c[U] Y_{c+|U|}[V\U]
+                    acc = mad(X[c * M + U], Y[(c + pc(U)) * M + (V ^ U)], acc);
+                    if (U == 0) break;
+                }
+            res[nres++] = acc;
+        }
+        __syncthreads();
+        nres = 0;
+        for (int e = threadIdx.x; e < (GS / (2 * step)) * SZ; e += blockDim.x) {
+            const int pr = e / SZ, q = e % SZ;
+            A[pr * 2 * step][q] = res[nres++];
+        }
+        __syncthreads();
+    }
+    T *out = (dir == 0 ? out_f : out_b) + g * SZ;
+    for (int q = threadIdx.x; q < SZ; q += blockDim.x)
+        if (opx_valid<NB>(q)) out[q] = A[0][q];
+}
+
+template <int NB, typename T>
+__global__ void __launch_bounds__(64) k_ops_down_c(const T *ops_f, const T *ops_b, const T *gcar_f, const T *gcar_b,
+                                                    T *car_f, T *car_b, int64_t n_in, const int *stop, T *car_bi) {
+    constexpr int M = 1 << NB;
+    constexpr int SZ = OpShape<NB>::SZ;
+    constexpr int GS = group_of(NB);
+    __shared__ T G[GS][SZ];
+    __shared__ T cur[M];
+    const int64_t g = blockIdx.x;
+    const int dir = blockIdx.y;
+    const int64_t first = g * GS;
+    if (first >= n_in || *stop) return;
+    const int cnt = (int)min((int64_t)GS, n_in - first);
+    const T *ops = (dir == 0 ? ops_f : ops_b) + first * SZ;
+    for (int e = threadIdx.x; e < cnt * SZ; e += blockDim.x) G[e / SZ][e % SZ] = opx_valid<NB>(e % SZ) ? ops[e] : zero_of(T{});
+    const T *gc = dir == 0 ? gcar_f : gcar_b;
+    for (int S = threadIdx.x; S < M; S += blockDim.x) cur[S] = gc ? gc[g * M + S] : (S == 0 ? one_of(T{}) : zero_of(T{}));
+    __syncthreads();
+    T *car = dir == 0 ? car_f : car_b;
+    for (int t = 0; t < cnt; ++t) {
+        const int i = dir == 0 ? t : cnt - 1 - t;
+        T nx = zero_of(T{});
+        const int S = threadIdx.x;
+        if (S < M) {
+            car[(first + i) * M + S] = cur[S];
+            for (int U = S;; U = (U - 1) & S) {              // Op(cur)[S] = sum_{U subset S} cur[U] G_|U|[S\U]
+                nx = mad(cur[U], G[i][pc(U) * M + (S ^ U)], nx);
+                if (U == 0) break;
+            }
+        }
+        __syncthreads();
+        if (S < M) {
+            cur[S] = nx;
+            if (dir == 1 && car_bi) car_bi[(first + i) * M + S] = nx;  // inclusive (chain start)
+        }
+        __syncthreads();
     }
 }
 
@@ -1146,6 +1245,13 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
             ++*launches;
             continue;
         }
+        if constexpr (NB >= 4) {
+            k_ops_reduce_c<NB, T><<<dim3((unsigned)ng, 2), 128, 0, s>>>(
+                static_cast<const T *>(p.ops_f[i]), static_cast<const T *>(p.ops_b[i]), static_cast<T *>(p.ops_f[i + 1]),
+                static_cast<T *>(p.ops_b[i + 1]), p.nlev_n[i], p.stop);
+            ++*launches;
+            continue;
+        }
         dim3 grid((unsigned)((ng + 63) / 64), 2);
         k_ops_reduce<NB, T><<<grid, 64, 0, s>>>(static_cast<const T *>(p.ops_f[i]), static_cast<const T *>(p.ops_b[i]),
                                                static_cast<T *>(p.ops_f[i + 1]), static_cast<T *>(p.ops_b[i + 1]),
@@ -1161,6 +1267,12 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
                                                           static_cast<double *>(p.agg_send),
                                                           static_cast<double *>(p.agg_send) + OpShape<NB>::SZ,
                                                           p.nlev_n[top], p.stop);
+        } else if constexpr (NB >= 4) {
+            k_ops_reduce_c<NB, T><<<dim3(1, 2), 128, 0, s>>>(static_cast<const T *>(p.ops_f[top]),
+                                                            static_cast<const T *>(p.ops_b[top]),
+                                                            static_cast<T *>(p.agg_send),
+                                                            static_cast<T *>(p.agg_send) + OpShape<NB>::SZ,
+                                                            p.nlev_n[top], p.stop);
         } else {
             k_ops_reduce<NB, T><<<dim3(1, 2), 64, 0, s>>>(static_cast<const T *>(p.ops_f[top]),
                                                          static_cast<const T *>(p.ops_b[top]),
@@ -1176,7 +1288,7 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
     }
     // down-sweep
     for (int i = p.nlev - 1; i >= 0; --i) {
-        const int64_t ng = (p.nlev_n[i] + kGroup - 1) / kGroup;
+        const int64_t ng = (p.nlev_n[i] + group_of(NB) - 1) / group_of(NB);
         dim3 grid((unsigned)((ng + 63) / 64), 2);
         const T *gf = i + 1 < p.nlev ? static_cast<const T *>(p.car_f[i + 1])
                                      : (p.exch ? static_cast<const T *>(p.rank_car) : nullptr);
@@ -1194,6 +1306,13 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
             ++*launches;
             continue;
         }
+        if constexpr (NB >= 4) {
+            k_ops_down_c<NB, T><<<dim3((unsigned)ng, 2), 64, 0, s>>>(
+                static_cast<const T *>(p.ops_f[i]), static_cast<const T *>(p.ops_b[i]), gf, gb, static_cast<T *>(p.car_f[i]),
+                static_cast<T *>(p.car_b[i]), p.nlev_n[i], p.stop, i == 0 && p.sw ? static_cast<T *>(p.car_bi) : nullptr);
+            ++*launches;
+            continue;
+        }
         k_ops_down<NB, T><<<grid, 64, 0, s>>>(static_cast<const T *>(p.ops_f[i]), static_cast<const T *>(p.ops_b[i]),
                                              gf, gb, static_cast<T *>(p.car_f[i]), static_cast<T *>(p.car_b[i]),
                                              p.nlev_n[i], p.stop, i == 0 && p.sw ? static_cast<T *>(p.car_bi) : nullptr);
@@ -1203,8 +1322,9 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
     switch (mode) {
         case MODE_MARG: launch_apply<NB, T, MODE_MARG>(p, nb, tpb, s, launches); break;
         case MODE_UPD:
-            if (next) {
-                if constexpr (sizeof(T) == sizeof(double)) launch_apply<NB, T, MODE_UPD, true>(p, nb, tpb, s, launches);
+            if (next && NB <= 4) {
+                if constexpr (sizeof(T) == sizeof(double) && NB <= 4)
+                    launch_apply<NB, T, MODE_UPD, true>(p, nb, tpb, s, launches);
             } else {
                 launch_apply<NB, T, MODE_UPD>(p, nb, tpb, s, launches);
             }
