@@ -99,6 +99,12 @@ struct mmot_ctx {
     int64_t nchp = 0;                       // sw: chains rounded up to 32 (transposed row length)
     double *mu_t[mmot::kMaxL] = {nullptr};  // sw: marginals in the chain-transposed layout
     double *out_t = nullptr;                // sw: marginal output in the chain-transposed layout
+    // restricted next-update scan (single-walk contexts): second carry buffer + affine elements
+    bool rx = false;
+    void *rx_mem = nullptr;
+    void *carB_f = nullptr, *carB_bi = nullptr;
+    void *rxe_f[mmot::kMaxLevels] = {nullptr}, *rxe_b[mmot::kMaxLevels] = {nullptr};
+    void *rcar_f[mmot::kMaxLevels] = {nullptr}, *rcar_b[mmot::kMaxLevels] = {nullptr};
     // sharded contexts (mmot_create_sharded)
     bool sharded = false;
     int rank = 0, world = 1;
@@ -205,6 +211,7 @@ void mmot_destroy(mmot_ctx *ctx) {
     cudaFree(ctx->ws);
     cudaFree(ctx->out_t);
     cudaFree(ctx->bat_mem);
+    cudaFree(ctx->rx_mem);
     cudaFree(ctx->shard_mem);
     if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
     cudaFree(ctx->bat_int);
@@ -368,6 +375,35 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
             snprintf(g_err, sizeof g_err, "%s", c->err);
             mmot_destroy(c);
             return MMOT_ENOMEM;
+        }
+        // restricted next-update scan: a second set of level-0 carries and the affine elements
+        if (l >= 3 && l <= 5) {
+            const int MO = 1 << (NB - 1);
+            const size_t SZE = (size_t)(NB + 1) * MO;
+            size_t tot = 2 * (size_t)c->nchunks * M;  // carB_f, carB_bi
+            for (int i = 0; i < c->nlev; ++i) tot += 2 * (size_t)c->nlev_n[i] * (SZE + MO);
+            if (cudaMalloc(&c->rx_mem, tot * sizeof(double)) != cudaSuccess) {
+                set_err(c, "cudaMalloc of the restricted-scan workspace failed");
+                snprintf(g_err, sizeof g_err, "%s", c->err);
+                mmot_destroy(c);
+                return MMOT_ENOMEM;
+            }
+            double *q = static_cast<double *>(c->rx_mem);
+            c->carB_f = q;
+            q += (size_t)c->nchunks * M;
+            c->carB_bi = q;
+            q += (size_t)c->nchunks * M;
+            for (int i = 0; i < c->nlev; ++i) {
+                c->rxe_f[i] = q;
+                q += (size_t)c->nlev_n[i] * SZE;
+                c->rxe_b[i] = q;
+                q += (size_t)c->nlev_n[i] * SZE;
+                c->rcar_f[i] = q;
+                q += (size_t)c->nlev_n[i] * MO;
+                c->rcar_b[i] = q;
+                q += (size_t)c->nlev_n[i] * MO;
+            }
+            c->rx = getenv("MMOT_NO_RX") == nullptr;  // MMOT_NO_RX=1: full operator path (A/B runs)
         }
     } else if (c->opts.repr == MMOT_LOG) {
         for (int qq = 0; qq < l; ++qq) {
@@ -600,6 +636,12 @@ static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double
     }
     p.car_bi = c->car_bi;
     p.sw = c->sw ? 1 : 0;
+    for (int i = 0; i < c->nlev; ++i) {
+        p.rxe_f[i] = c->rxe_f[i];
+        p.rxe_b[i] = c->rxe_b[i];
+        p.rcar_f[i] = c->rcar_f[i];
+        p.rcar_b[i] = c->rcar_b[i];
+    }
     p.nchp = c->nchp;
     if (c->sw && mu) p.muk = c->mu_t[k];
     if (c->sharded) {
@@ -681,6 +723,12 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
     const int check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
     bool poll_pending = false;
     int ops_for = -1;  // bound set whose chain operators are currently in ops level 0
+    // restricted next-update scan: carries alternate between the context's level-0 arrays (0) and
+    // the second set (1); rx_ready = the previous update wrote this update's affine elements
+    const bool rx = c->rx && !c->sharded;
+    int cur = 0;
+    bool rx_ready = false;
+    void *cf[2] = {c->car_f[0], c->carB_f}, *cb[2] = {c->car_bi, c->carB_bi};
     for (int t = 1; t <= iters; ++t) {
         // asynchronous early exit: the device stop flag is polled without blocking
         if (poll_pending && cudaEventQuery(c->poll_ev) == cudaSuccess) {
@@ -691,15 +739,29 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
             // fused update: scan (+ operators only if not produced by the previous update),
             // apply phi_k <- mu_k / J_k and build the operators of update k+1 in the same walk
             Plan p = make_plan(c, k, lin, mu[k], lin[k], t);
+            if (rx) {
+                p.car_f[0] = cf[cur];
+                p.car_bi = cb[cur];
+                p.ncar_f = cf[1 - cur];
+                p.ncar_bi = cb[1 - cur];
+                p.nxr = 1;
+                p.rx_scan = rx_ready ? 1 : 0;
+            }
             CK(c, mmot::launch_product(p, mmot::MODE_UPD, c->stream, &c->launches, prof_events(c, mmot::MODE_UPD),
-                                       ops_for != k, true));
+                                       rx ? !rx_ready : ops_for != k, true));
             ops_for = l <= 5 ? (k + 1) % l : -1;  // l = 6: next-update operators are not fused (registers)
+            if (rx) {
+                rx_ready = true;
+                cur = 1 - cur;
+            }
         }
         if (tol > 0 && (t % check_every == 0 || t == iters)) {
             for (int k = 0; k + 1 < l; ++k) {
                 Plan p = make_plan(c, k, lin, mu[k], nullptr, t);
                 CK(c, mmot::launch_product(p, mmot::MODE_RES, c->stream, &c->launches, prof_events(c, mmot::MODE_RES)));
                 ops_for = -1;  // the residual products overwrote the chain operators
+                rx_ready = false;  // ... and the level-0 carries: the next update starts from a full scan
+                cur = 0;
                 CK(c, mmot::launch_sum(c->partial, c->nchunks, &c->dsc->res_acc, 1.0, k > 0, &c->dsc->stop, c->stream,
                                        &c->launches));
             }

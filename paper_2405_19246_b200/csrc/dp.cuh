@@ -329,4 +329,154 @@ __host__ __device__ inline void compose_rank_carries(const T *all, int world, in
     for (int S = 0; S < M; ++S) bin[S] = cur[S];
 }
 
+// ---------------------------------------------------------------------------------------
+// Restricted next-update scan (single-walk Sinkhorn updates).  Update k+1's bound slots are
+// (slot 1..NB-1 of update k, then the new phi_k).  Its states S' = U (U over the NB-1 "old"
+// slots) equal update k's states U << 1 exactly (same marginals, unchanged vectors), so only the
+// "new part" S' = U + {new} needs a scan, and it is affine in the carry:
+//   prefix  y_out = A'(y_in) + L,   suffix  z_start = A''(z_end) + M,
+// where A', A'' are operators of the (NB-1)-marginal DP on the old slots with shifts c = 1..NB
+// (entries G_c[V], c + |V| <= NB; A'' from the same walk by the prefix/suffix duality), and
+// L, M are accumulated along update k's walk from its exact states.
+// Element layout (SZE = (NB+1) * MO doubles): A[c-1][V] at (c-1)*MO + V, offset at NB*MO + U.
+// ---------------------------------------------------------------------------------------
+template <int NB>
+struct Rx {
+    static constexpr int NO = NB - 1;
+    static constexpr int MO = 1 << (NB - 1);
+    static constexpr int SZE = (NB + 1) * MO;
+};
+
+// L <- place_old(D L) + o * F_old   (F = update k's prefix state AFTER this point's step)
+template <int NB>
+__device__ __forceinline__ void rx_L_step(double (&L)[Rx<NB>::MO], const double *wt, const double (&f)[NB],
+                                          double o, const double (&F)[1 << NB]) {
+    constexpr int MO = Rx<NB>::MO;
+#pragma unroll
+    for (int U = 0; U < MO; ++U) L[U] *= wt[pc(U) + 1];
+#pragma unroll
+    for (int j = 0; j < NB - 1; ++j)
+#pragma unroll
+        for (int U = MO - 1; U >= 0; --U)
+            if ((U >> j) & 1) L[U] = fma(f[j + 1], L[U ^ (1 << j)], L[U]);
+#pragma unroll
+    for (int U = 0; U < MO; ++U) L[U] = fma(o, F[U << 1], L[U]);
+}
+
+// Running restricted operator Gr[c-1][V] (c = 1..NB, V over old slots, c+|V| <= NB); the diag
+// of the chain's first point is skipped (G~ convention of opx_*).
+template <int NB>
+__device__ __forceinline__ void rx_G_step(double (&G)[NB][Rx<NB>::MO], const double *wt, const double (&f)[NB], bool skip) {
+    constexpr int MO = Rx<NB>::MO;
+    if (!skip) {
+#pragma unroll
+        for (int c = 1; c <= NB; ++c)
+#pragma unroll
+            for (int V = 0; V < MO; ++V)
+                if (c + pc(V) <= NB) G[c - 1][V] *= wt[c + pc(V)];
+    }
+#pragma unroll
+    for (int c = 1; c <= NB; ++c)
+#pragma unroll
+        for (int j = 0; j < NB - 1; ++j)
+#pragma unroll
+            for (int V = MO - 1; V >= 0; --V)
+                if (((V >> j) & 1) && c + pc(V) <= NB) G[c - 1][V] = fma(f[j + 1], G[c - 1][V ^ (1 << j)], G[c - 1][V]);
+}
+
+// M += Pi_x s_x with Pi_x = suffix operator of [x0, x) (identity at the chain's first point,
+// else R_c[V] = w_c Gr_{l-c-|V|}[V]; l-c-|V| = NB-|R| for c = |U|+1, V = R\U) and
+// s_x[U] = o * Bo[U], Bo[U] = B[U << 1] (update k's suffix state at this point, before the
+// inverse step).
+template <int NB>
+__device__ __forceinline__ void rx_M_acc(double (&Mv)[Rx<NB>::MO], const double (&G)[NB][Rx<NB>::MO], const double *wt,
+                                         double o, const double (&Bo)[Rx<NB>::MO], bool first) {
+    constexpr int MO = Rx<NB>::MO;
+    if (first) {
+#pragma unroll
+        for (int R = 0; R < MO; ++R) Mv[R] = fma(o, Bo[R], Mv[R]);
+        return;
+    }
+    double ow[NB];
+#pragma unroll
+    for (int a = 1; a <= NB; ++a) ow[a - 1] = o * wt[a];
+    double sv[MO];
+#pragma unroll
+    for (int U = 0; U < MO; ++U) sv[U] = ow[pc(U)] * Bo[U];
+#pragma unroll
+    for (int R = 0; R < MO; ++R) {
+        double acc = Mv[R];
+#pragma unroll
+        for (int U = 0; U < MO; ++U)
+            if ((U & R) == U) acc = fma(G[NB - pc(R) - 1][R ^ U], sv[U], acc);
+        Mv[R] = acc;
+    }
+}
+
+// Chain-end elements: prefix (A'_c[V] = w_c Gr_c[V], offset L) and suffix (A''_c[V] =
+// w_c Gr_{l-c-|V|}[V], offset M).
+template <int NB>
+__device__ __forceinline__ void rx_store(const double (&G)[NB][Rx<NB>::MO], const double (&L)[Rx<NB>::MO],
+                                         const double (&Mv)[Rx<NB>::MO], const double *wt, double *ef, double *eb) {
+    constexpr int MO = Rx<NB>::MO;
+#pragma unroll
+    for (int c = 1; c <= NB; ++c)
+#pragma unroll
+        for (int V = 0; V < MO; ++V) {
+            const bool ok = c + pc(V) <= NB;
+            ef[(c - 1) * MO + V] = ok ? wt[c] * G[c - 1][V] : 0.0;
+            eb[(c - 1) * MO + V] = ok ? wt[c] * G[NB - c - pc(V)][V] : 0.0;
+        }
+#pragma unroll
+    for (int U = 0; U < MO; ++U) {
+        ef[NB * MO + U] = L[U];
+        eb[NB * MO + U] = Mv[U];
+    }
+}
+
+// Affine elements: identity, application to a new-part vector, composition (X first, then Y).
+template <int NB>
+__device__ __forceinline__ void rx_identity(double (&E)[Rx<NB>::SZE]) {
+    constexpr int MO = Rx<NB>::MO;
+#pragma unroll
+    for (int i = 0; i < Rx<NB>::SZE; ++i) E[i] = (i < NB * MO && i % MO == 0) ? 1.0 : 0.0;
+}
+template <int NB>
+__device__ __forceinline__ void rx_apply(const double (&E)[Rx<NB>::SZE], const double (&y)[Rx<NB>::MO],
+                                         double (&out)[Rx<NB>::MO]) {
+    constexpr int MO = Rx<NB>::MO;
+#pragma unroll
+    for (int S = 0; S < MO; ++S) {
+        double acc = E[NB * MO + S];
+#pragma unroll
+        for (int U = 0; U < MO; ++U)
+            if ((U & S) == U) acc = fma(y[U], E[pc(U) * MO + (S ^ U)], acc);
+        out[S] = acc;
+    }
+}
+template <int NB>
+__device__ __forceinline__ void rx_compose(const double (&X)[Rx<NB>::SZE], const double (&Y)[Rx<NB>::SZE],
+                                           double (&Z)[Rx<NB>::SZE]) {
+    constexpr int MO = Rx<NB>::MO;
+#pragma unroll
+    for (int c = 1; c <= NB; ++c)
+#pragma unroll
+        for (int V = 0; V < MO; ++V) {
+            double acc = 0.0;
+            if (c + pc(V) <= NB) {
+#pragma unroll
+                for (int U = 0; U < MO; ++U)
+                    if ((U & V) == U && c + pc(U) <= NB)
+                        acc = fma(X[(c - 1) * MO + U], Y[(c + pc(U) - 1) * MO + (V ^ U)], acc);
+            }
+            Z[(c - 1) * MO + V] = acc;
+        }
+    double xo[MO], yo[MO];
+#pragma unroll
+    for (int U = 0; U < MO; ++U) xo[U] = X[NB * MO + U];
+    rx_apply<NB>(Y, xo, yo);
+#pragma unroll
+    for (int U = 0; U < MO; ++U) Z[NB * MO + U] = yo[U];
+}
+
 }  // namespace mmot

@@ -47,6 +47,14 @@ struct Plan {
     // sharded contexts (mmot_create_sharded): after the up-sweep the whole-shard operators are
     // written to agg_send ([2][SZ]: prefix, suffix), exch() all-gathers them into agg_all
     // ([world][2][SZ]) on the stream, and the carries entering the shard go to rank_car ([2][M])
+    // restricted next-update scan (single-walk Sinkhorn, not sharded): nxr = 1 makes the update
+    // kernel write the affine elements of the next update (rxe_*[0]) and the old parts of the next
+    // carries (ncar_f, ncar_bi); rx_scan = 1 replaces the operator phase + full scan by the affine
+    // scan, which writes the new parts of car_f[0] / car_bi
+    int nxr, rx_scan;
+    void *rxe_f[kMaxLevels], *rxe_b[kMaxLevels];    // affine elements per level
+    void *rcar_f[kMaxLevels], *rcar_b[kMaxLevels];  // new-part carries per level (levels >= 1)
+    void *ncar_f, *ncar_bi;                         // next update's full carries (old parts)
     void (*exch)(void *ctx, int elem_bytes, cudaStream_t s);
     void *exch_ctx;
     void *agg_send, *agg_all, *rank_car;

@@ -875,7 +875,7 @@ __device__ __forceinline__ void sw_issue(double *sbuf, uint64_t *bar, const doub
     }
 }
 
-template <int NB, typename T, int MODE, bool NEXT>
+template <int NB, typename T, int MODE, bool NEXT, bool NXR = false>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply(Plan p) {
     using AV = ApplyVecs<NB, MODE>;
     constexpr int M = 1 << NB;
@@ -916,6 +916,27 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
     }
     T Gx[NEXT ? NB + 1 : 1][NEXT ? M : 1];
     if constexpr (NEXT) opx_identity<NB, T>(Gx);
+    // restricted next-update scan elements (dp.cuh Rx): L, running Gr, M; old parts of the carries
+    constexpr int MO = NXR ? Rx<NB>::MO : 1;
+    double rL[MO], rM[MO], rG[NXR ? NB : 1][MO];
+    if constexpr (NXR) {
+#pragma unroll
+        for (int U = 0; U < MO; ++U) {
+            rL[U] = 0.0;
+            rM[U] = 0.0;
+#pragma unroll
+            for (int c = 0; c < NB; ++c) rG[c][U] = U == 0 ? 1.0 : 0.0;
+        }
+        if (live) {
+            double *nf = static_cast<double *>(p.ncar_f) + c * M;
+            double *nb = static_cast<double *>(p.ncar_bi) + c * M;
+#pragma unroll
+            for (int U = 0; U < MO; ++U) {
+                nf[U] = value_of(F[U << 1]);
+                nb[U] = value_of(B[U << 1]);
+            }
+        }
+    }
     // the next-update operator step of point m is issued after the scans of point m+1
     // (software pipelining: the division of point m overlaps the scans of point m+1)
     double fprev[NB > 0 ? NB : 1], oprev = 0.0;
@@ -941,6 +962,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
             for (int b = 0; b < NB; ++b) f[b] = cur[(b * S + j) * 32 + lane];
             dp_diag<NB, T, true>(F, wt);
             dp_place<NB, T>(F, f);
+            double Bo[MO];
+            if constexpr (NXR) {
+#pragma unroll
+                for (int U = 0; U < MO; ++U) Bo[U] = value_of(B[U << 1]);
+            }
             dp_unplace<NB, T>(B, f);          // B := U_m = D B_{m+1}
             const T J = combine<NB, T>(F, B);
             dp_diag_inv<NB, T>(B, wi);        // B := B_{m+1}
@@ -969,6 +995,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
                 for (int b = 0; b < NB; ++b) fprev[b] = f[b];
                 oprev = o;
             }
+            if constexpr (NXR) {
+                if constexpr (sizeof(T) == sizeof(double)) {
+                    const bool first = j == 0 && s == 0;
+                    rx_M_acc<NB>(rM, rG, reinterpret_cast<const double *>(wt), o, Bo, first);
+                    rx_G_step<NB>(rG, reinterpret_cast<const double *>(wt), f, first);
+                    rx_L_step<NB>(rL, reinterpret_cast<const double *>(wt), f, o, reinterpret_cast<const double(&)[M]>(F));
+                }
+            }
         }
         have_prev = true;
         __syncwarp();  // every lane is done with this stage before it is refilled
@@ -982,6 +1016,135 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
         if (live)
             opx_store<NB, T>(Gx, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
                              static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+    }
+    if constexpr (NXR) {
+        if (live)
+            rx_store<NB>(rG, rL, rM, reinterpret_cast<const double *>(wt),
+                         static_cast<double *>(p.rxe_f[0]) + c * Rx<NB>::SZE,
+                         static_cast<double *>(p.rxe_b[0]) + c * Rx<NB>::SZE);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Affine scan of the restricted next-update elements (one warp per group of 32, shuffles).
+// ---------------------------------------------------------------------------------------
+template <int NB>
+__device__ __forceinline__ void rx_load(double (&E)[Rx<NB>::SZE], const double *src, int64_t i, int64_t n) {
+    if (i < n) {
+#pragma unroll
+        for (int q = 0; q < Rx<NB>::SZE; ++q) E[q] = src[i * Rx<NB>::SZE + q];
+    } else {
+        rx_identity<NB>(E);
+    }
+}
+template <int NB>
+__device__ __forceinline__ void rx_shfl(double (&D)[Rx<NB>::SZE], const double (&E)[Rx<NB>::SZE], int delta, int mode) {
+#pragma unroll
+    for (int q = 0; q < Rx<NB>::SZE; ++q)
+        D[q] = mode == 1 ? __shfl_up_sync(0xffffffffu, E[q], delta) : __shfl_down_sync(0xffffffffu, E[q], delta);
+}
+
+template <int NB>
+__global__ void __launch_bounds__(128) k_rx_reduce_w(const double *in_f, const double *in_b, double *out_f, double *out_b,
+                                                    int64_t n_in, const int *stop) {
+    constexpr int SZE = Rx<NB>::SZE;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t g = (int64_t)blockIdx.x * 4 + warp;
+    const int dir = blockIdx.y;
+    const int64_t first = g * 32;
+    if (first >= n_in || *stop) return;
+    double A[SZE], Bv[SZE], C[SZE];
+    rx_load<NB>(A, dir == 0 ? in_f : in_b, first + lane, n_in);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        rx_shfl<NB>(Bv, A, d, 2);
+        if (dir == 0) rx_compose<NB>(A, Bv, C);   // prefix: lower chain first
+        else rx_compose<NB>(Bv, A, C);            // suffix: higher chain first
+        if ((lane & (2 * d - 1)) == 0) {
+#pragma unroll
+            for (int q = 0; q < SZE; ++q) A[q] = C[q];
+        }
+    }
+    if (lane == 0) {
+        double *o = (dir == 0 ? out_f : out_b) + g * SZE;
+#pragma unroll
+        for (int q = 0; q < SZE; ++q) o[q] = A[q];
+    }
+}
+
+// Down-sweep: group carries gc (MO per group, nullptr = zero new part at the top), member carries
+// out: level >= 1 -> car (MO per member, exclusive in both directions); level 0 -> the full carry
+// arrays (stride M, new-part positions U | newbit): prefix exclusive, suffix inclusive.
+template <int NB>
+__global__ void __launch_bounds__(128) k_rx_down_w(const double *el_f, const double *el_b, const double *gc_f,
+                                                  const double *gc_b, double *car_f, double *car_b, int64_t n_in,
+                                                  const int *stop, double *full_f, double *full_bi) {
+    constexpr int SZE = Rx<NB>::SZE;
+    constexpr int MO = Rx<NB>::MO;
+    constexpr int M = 1 << NB;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t g = (int64_t)blockIdx.x * 4 + warp;
+    const int dir = blockIdx.y;
+    const int64_t first = g * 32;
+    if (first >= n_in || *stop) return;
+    double A[SZE], Bv[SZE], C[SZE];
+    rx_load<NB>(A, dir == 0 ? el_f : el_b, first + lane, n_in);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        rx_shfl<NB>(Bv, A, d, dir == 0 ? 1 : 2);
+        rx_compose<NB>(Bv, A, C);  // the earlier-applied part (from the shuffle) first
+        const bool take = dir == 0 ? lane >= d : lane + d < 32;
+        if (take) {
+#pragma unroll
+            for (int q = 0; q < SZE; ++q) A[q] = C[q];
+        }
+    }
+    const double *gc = dir == 0 ? gc_f : gc_b;
+    double cin[MO], out[MO], nb[MO];
+#pragma unroll
+    for (int U = 0; U < MO; ++U) cin[U] = gc ? gc[g * MO + U] : 0.0;
+    rx_apply<NB>(A, cin, out);
+#pragma unroll
+    for (int U = 0; U < MO; ++U)
+        nb[U] = dir == 0 ? __shfl_up_sync(0xffffffffu, out[U], 1) : __shfl_down_sync(0xffffffffu, out[U], 1);
+    const bool edge = dir == 0 ? lane == 0 : lane == 31;
+    const int64_t i = first + lane;
+    if (i < n_in) {
+        if (full_f) {  // level 0
+            constexpr int NEW = 1 << (NB - 1);
+            if (dir == 0) {
+#pragma unroll
+                for (int U = 0; U < MO; ++U) full_f[i * M + (U | NEW)] = edge ? cin[U] : nb[U];
+            } else {
+#pragma unroll
+                for (int U = 0; U < MO; ++U) full_bi[i * M + (U | NEW)] = out[U];
+            }
+        } else {
+            double *dst = (dir == 0 ? car_f : car_b) + i * MO;
+#pragma unroll
+            for (int U = 0; U < MO; ++U) dst[U] = edge ? cin[U] : nb[U];
+        }
+    }
+}
+
+template <int NB>
+static void launch_rx_scan(const Plan &p, cudaStream_t s, int64_t *launches) {
+    for (int i = 0; i + 1 < p.nlev; ++i) {
+        const int64_t ng = p.nlev_n[i + 1];
+        k_rx_reduce_w<NB><<<dim3((unsigned)((ng + 3) / 4), 2), 128, 0, s>>>(
+            static_cast<const double *>(p.rxe_f[i]), static_cast<const double *>(p.rxe_b[i]),
+            static_cast<double *>(p.rxe_f[i + 1]), static_cast<double *>(p.rxe_b[i + 1]), p.nlev_n[i], p.stop);
+        ++*launches;
+    }
+    for (int i = p.nlev - 1; i >= 0; --i) {
+        const int64_t ng = (p.nlev_n[i] + 31) / 32;
+        const double *gf = i + 1 < p.nlev ? static_cast<const double *>(p.rcar_f[i + 1]) : nullptr;
+        const double *gb = i + 1 < p.nlev ? static_cast<const double *>(p.rcar_b[i + 1]) : nullptr;
+        k_rx_down_w<NB><<<dim3((unsigned)((ng + 3) / 4), 2), 128, 0, s>>>(
+            static_cast<const double *>(p.rxe_f[i]), static_cast<const double *>(p.rxe_b[i]), gf, gb,
+            static_cast<double *>(p.rcar_f[i]), static_cast<double *>(p.rcar_b[i]), p.nlev_n[i], p.stop,
+            i == 0 ? static_cast<double *>(p.car_f[0]) : nullptr, i == 0 ? static_cast<double *>(p.car_bi) : nullptr);
+        ++*launches;
     }
 }
 
@@ -1144,17 +1307,17 @@ static constexpr size_t sw_smem() {
     return (size_t)kWarpsPerCta * kSwStages * ApplyVecs<NB, MODE>::NV * kSwS * 32 * sizeof(double);
 }
 
-template <int NB, typename T, int MODE, bool NEXT>
+template <int NB, typename T, int MODE, bool NEXT, bool NXR = false>
 static void launch_sw(const Plan &p, cudaStream_t s, int64_t *launches) {
     constexpr size_t sm = sw_smem<NB, MODE>();
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_sw_apply<NB, T, MODE, NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_sw_apply<NB, T, MODE, NEXT, NXR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         attr = true;
     }
     const int tpb = kWarpsPerCta * 32;
     const int64_t nb = (p.nchp + tpb - 1) / tpb;
-    k_sw_apply<NB, T, MODE, NEXT><<<(unsigned)nb, tpb, sm, s>>>(p);
+    k_sw_apply<NB, T, MODE, NEXT, NXR><<<(unsigned)nb, tpb, sm, s>>>(p);
     ++*launches;
 }
 
@@ -1183,7 +1346,15 @@ static void launch_apply(const Plan &p, int64_t /*nb*/, int /*tpb*/, cudaStream_
     const bool full_ok = p.P % slab_s(NB) == 0;
     const int64_t nfull = full_ok ? p.N / p.P : 0;
     if (p.sw) {
-        if constexpr (NB <= 4) launch_sw<NB, T, MODE, NEXT>(p, s, launches);
+        if constexpr (NB <= 4) {
+            if constexpr (NEXT && MODE == MODE_UPD && sizeof(T) == sizeof(double) && NB >= 2) {
+                if (p.nxr) {
+                    launch_sw<NB, T, MODE, false, true>(p, s, launches);
+                    return;
+                }
+            }
+            launch_sw<NB, T, MODE, NEXT>(p, s, launches);
+        }
         return;
     }
     if constexpr (NB <= 3 && sizeof(T) == sizeof(double)) {
@@ -1209,6 +1380,16 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
     const int tpb = kWarpsPerCta * 32;
     const int64_t nb = (p.nchunks + tpb - 1) / tpb;
     if (ev) cudaEventRecord(ev[0], s);
+    if constexpr (NB >= 2 && NB <= 4 && sizeof(T) == sizeof(double)) {
+        if (p.rx_scan && mode == MODE_UPD) {
+            if (ev) cudaEventRecord(ev[1], s);
+            launch_rx_scan<NB>(p, s, launches);
+            if (ev) cudaEventRecord(ev[2], s);
+            launch_apply<NB, T, MODE_UPD, true>(p, nb, tpb, s, launches);
+            if (ev) cudaEventRecord(ev[3], s);
+            return cudaGetLastError();
+        }
+    }
     if (with_ops && p.sw) {
         if constexpr (NB <= 4) {
             constexpr size_t sm = (size_t)kWarpsPerCta * kSwStages * NB * kSwS * 32 * sizeof(double);
