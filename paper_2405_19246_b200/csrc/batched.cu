@@ -32,7 +32,8 @@ namespace mmot {
 
 constexpr int kBS = 8;          // slab = checkpoint block (points per chain)
 constexpr int kBWarps = 4;      // warps (instances) per CTA
-constexpr int kRenorm = 48;     // lazy renormalisation threshold: |max exponent of a chain| (products of l mantissas stay far inside fp64)
+constexpr int kRenorm = 96;     // lazy renormalisation threshold: |max exponent of a chain| (products of l <= 5 mantissas stay below 2^480)
+static const int g_renorm = [] { const char *e = getenv("MMOT_BAT_RENORM"); return e ? atoi(e) : kRenorm; }();
 
 // exact 2^n as a double (0 below the normal range, inf above)
 __device__ __forceinline__ double pow2i(int n) {
@@ -95,6 +96,7 @@ struct BPlan {
     double *wout;                   // COST: [batch]
     int *status;                    // [batch] per-instance status (0 ok, EOVERFLOW)
     int *fail_iter;                 // [batch]
+    int renorm;                     // lazy renormalisation threshold (kRenorm)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -352,10 +354,26 @@ __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB 
     return emax;
 }
 
-// phit_k of this lane's chain *= 2^{-shift}
-__device__ void bat_rescale(double *v, int64_t x0, int64_t x1, int shift) {
-    const double sc = pow2i(-shift);
-    for (int64_t x = x0; x < x1; ++x) v[x] *= sc;
+// phit_k *= 2^{-shift_r} on every chain r whose lane asked for it (shift 0 = untouched); the
+// warp sweeps the instance's vector with coalesced accesses (lane i takes elements i, i+32, ...).
+__device__ void bat_rescale(double *v, int64_t N, int P, int shift, int lane) {
+    const bool any = __any_sync(0xffffffffu, shift != 0);
+    if (!any) return;
+    for (int64_t x0 = 0; x0 < N; x0 += 32 * 4) {
+        double t[4];
+        int sh[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t x = x0 + u * 32 + lane;
+            sh[u] = __shfl_sync(0xffffffffu, shift, (int)(x / P < 31 ? x / P : 31));
+            t[u] = (x < N && sh[u] != 0) ? v[x] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t x = x0 + u * 32 + lane;
+            if (x < N && sh[u] != 0) v[x] = scale2(t[u], -sh[u]);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -414,11 +432,10 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
                 if (b2 && fail < 0) fail = t;
                 bad |= b2;
                 int sh = shk;
-                if (emax > -1000000 && (emax > kRenorm || emax < -kRenorm)) {
-                    // (walk 2 ended with a __syncwarp after its last slab store: the chain is visible)
-                    bat_rescale(bp.phit[k] + inst * bp.N, x0, x1, emax);
-                    sh += emax;
-                }
+                const int resc = (emax > -1000000 && (emax > bp.renorm || emax < -bp.renorm)) ? emax : 0;
+                // (walk 2 ended with a __syncwarp after its last slab store: the vector is visible)
+                bat_rescale(bp.phit[k] + inst * bp.N, bp.N, bp.P, resc, lane);
+                sh += resc;
                 __syncwarp();
 #pragma unroll
                 for (int q = 0; q < L; ++q)
@@ -614,6 +631,7 @@ static BPlan to_bplan(const BatchArgs &a) {
     bp.wout = a.wout;
     bp.status = a.status;
     bp.fail_iter = a.fail_iter;
+    bp.renorm = g_renorm;
     return bp;
 }
 

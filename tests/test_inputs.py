@@ -32,3 +32,10 @@ def test_c1_floor_and_c5_etas():
     etas = mi.c5_etas(64)
     assert np.all((etas >= 1e-3) & (etas <= 1e-1))
     assert mi.c5_etas(4)[2] == mi.c5_etas(8)[2]
+
+
+def test_c5_batch_generator_matches_per_instance():
+    """The vectorised C5 generator (bench) gives bit-identical values to the per-instance one."""
+    a = mi.c5_batch_marginals(5, 3, 256, 5)
+    for i in range(3):
+        assert np.array_equal(a[:, i, :], mi.c5_marginals(5 + i, 256, 5))
