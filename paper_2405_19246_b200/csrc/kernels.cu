@@ -852,6 +852,22 @@ __device__ __forceinline__ void sw_issue(double *sbuf, uint64_t *bar, const doub
     }
 }
 
+template <int NB>
+__device__ __forceinline__ void rx_load(double (&E)[Rx<NB>::SZE], const double *src, int64_t i, int64_t n) {
+    if (i < n) {
+#pragma unroll
+        for (int q = 0; q < Rx<NB>::SZE; ++q) E[q] = src[i * Rx<NB>::SZE + q];
+    } else {
+        rx_identity<NB>(E);
+    }
+}
+template <int NB>
+__device__ __forceinline__ void rx_shfl(double (&D)[Rx<NB>::SZE], const double (&E)[Rx<NB>::SZE], int delta, int mode) {
+#pragma unroll
+    for (int q = 0; q < Rx<NB>::SZE; ++q)
+        D[q] = mode == 1 ? __shfl_up_sync(0xffffffffu, E[q], delta) : __shfl_down_sync(0xffffffffu, E[q], delta);
+}
+
 template <int NB, typename T, int MODE, bool NEXT, bool NXR = false>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply(Plan p) {
     using AV = ApplyVecs<NB, MODE>;
@@ -890,6 +906,45 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
     } else {
         vec_unit<NB, T>(F);
         vec_unit<NB, T>(B);
+    }
+    if constexpr (NXR) {
+        // level 0 of the restricted scan, fused: the new-part carries of this warp's 32 chains from
+        // the elements the previous update left in rxe_*[0] and the group carries of level 1
+        if (p.rx_scan) {
+            constexpr int SZE = Rx<NB>::SZE;
+            constexpr int MOn = Rx<NB>::MO;
+            constexpr int NEW = 1 << (NB - 1);
+            const int64_t g = chain0 / 32;
+#pragma unroll
+            for (int dir = 0; dir < 2; ++dir) {
+                double A[SZE], Bv[SZE], C[SZE];
+                rx_load<NB>(A, static_cast<const double *>(dir == 0 ? p.rxe_f[0] : p.rxe_b[0]), c, p.nchunks);
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    rx_shfl<NB>(Bv, A, d, dir == 0 ? 1 : 2);
+                    rx_compose<NB>(Bv, A, C);
+                    const bool take = dir == 0 ? lane >= d : lane + d < 32;
+                    if (take) {
+#pragma unroll
+                        for (int q = 0; q < SZE; ++q) A[q] = C[q];
+                    }
+                }
+                double cin[MOn], out[MOn];
+                const double *gc = p.nlev > 1 ? static_cast<const double *>(dir == 0 ? p.rcar_f[1] : p.rcar_b[1]) : nullptr;
+#pragma unroll
+                for (int U = 0; U < MOn; ++U) cin[U] = gc ? gc[g * MOn + U] : 0.0;
+                rx_apply<NB>(A, cin, out);
+#pragma unroll
+                for (int U = 0; U < MOn; ++U) {
+                    if (dir == 0) {
+                        const double up = __shfl_up_sync(0xffffffffu, out[U], 1);
+                        reinterpret_cast<double &>(F[U | NEW]) = lane == 0 ? cin[U] : up;  // exclusive prefix
+                    } else {
+                        reinterpret_cast<double &>(B[U | NEW]) = out[U];                   // inclusive suffix
+                    }
+                }
+            }
+        }
     }
     T Gx[NEXT ? NB + 1 : 1][NEXT ? M : 1];
     if constexpr (NEXT) opx_identity<NB, T>(Gx);
@@ -995,32 +1050,52 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
                              static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
     }
     if constexpr (NXR) {
-        if (live)
-            rx_store<NB>(rG, rL, rM, reinterpret_cast<const double *>(wt),
-                         static_cast<double *>(p.rxe_f[0]) + c * Rx<NB>::SZE,
-                         static_cast<double *>(p.rxe_b[0]) + c * Rx<NB>::SZE);
+        constexpr int SZE = Rx<NB>::SZE;
+        double ef[SZE], eb[SZE];
+        rx_store<NB>(rG, rL, rM, reinterpret_cast<const double *>(wt), ef, eb);
+        if (!live) {
+            rx_identity<NB>(ef);
+            rx_identity<NB>(eb);
+        } else {
+#pragma unroll
+            for (int q = 0; q < SZE; ++q) {
+                static_cast<double *>(p.rxe_f[0])[c * SZE + q] = ef[q];
+                static_cast<double *>(p.rxe_b[0])[c * SZE + q] = eb[q];
+            }
+        }
+        // level 0 -> 1 of the restricted scan, fused: shuffle-tree composition of the warp's 32
+        if (p.nlev > 1) {
+            double Bv[SZE], C[SZE];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                rx_shfl<NB>(Bv, ef, d, 2);
+                rx_compose<NB>(ef, Bv, C);
+                if ((lane & (2 * d - 1)) == 0) {
+#pragma unroll
+                    for (int q = 0; q < SZE; ++q) ef[q] = C[q];
+                }
+                rx_shfl<NB>(Bv, eb, d, 2);
+                rx_compose<NB>(Bv, eb, C);
+                if ((lane & (2 * d - 1)) == 0) {
+#pragma unroll
+                    for (int q = 0; q < SZE; ++q) eb[q] = C[q];
+                }
+            }
+            if (lane == 0) {
+                const int64_t g = chain0 / 32;
+#pragma unroll
+                for (int q = 0; q < SZE; ++q) {
+                    static_cast<double *>(p.rxe_f[1])[g * SZE + q] = ef[q];
+                    static_cast<double *>(p.rxe_b[1])[g * SZE + q] = eb[q];
+                }
+            }
+        }
     }
 }
 
 // ---------------------------------------------------------------------------------------
 // Affine scan of the restricted next-update elements (one warp per group of 32, shuffles).
 // ---------------------------------------------------------------------------------------
-template <int NB>
-__device__ __forceinline__ void rx_load(double (&E)[Rx<NB>::SZE], const double *src, int64_t i, int64_t n) {
-    if (i < n) {
-#pragma unroll
-        for (int q = 0; q < Rx<NB>::SZE; ++q) E[q] = src[i * Rx<NB>::SZE + q];
-    } else {
-        rx_identity<NB>(E);
-    }
-}
-template <int NB>
-__device__ __forceinline__ void rx_shfl(double (&D)[Rx<NB>::SZE], const double (&E)[Rx<NB>::SZE], int delta, int mode) {
-#pragma unroll
-    for (int q = 0; q < Rx<NB>::SZE; ++q)
-        D[q] = mode == 1 ? __shfl_up_sync(0xffffffffu, E[q], delta) : __shfl_down_sync(0xffffffffu, E[q], delta);
-}
-
 template <int NB>
 __global__ void __launch_bounds__(128) k_rx_reduce_w(const double *in_f, const double *in_b, double *out_f, double *out_b,
                                                     int64_t n_in, const int *stop) {
@@ -1104,16 +1179,18 @@ __global__ void __launch_bounds__(128) k_rx_down_w(const double *el_f, const dou
     }
 }
 
+// Levels >= 1 (level 0 is fused into the update kernels: reduce at the end of update k, down at
+// the start of update k+1).
 template <int NB>
 static void launch_rx_scan(const Plan &p, cudaStream_t s, int64_t *launches) {
-    for (int i = 0; i + 1 < p.nlev; ++i) {
+    for (int i = 1; i + 1 < p.nlev; ++i) {
         const int64_t ng = p.nlev_n[i + 1];
         k_rx_reduce_w<NB><<<dim3((unsigned)((ng + 3) / 4), 2), 128, 0, s>>>(
             static_cast<const double *>(p.rxe_f[i]), static_cast<const double *>(p.rxe_b[i]),
             static_cast<double *>(p.rxe_f[i + 1]), static_cast<double *>(p.rxe_b[i + 1]), p.nlev_n[i], p.stop);
         ++*launches;
     }
-    for (int i = p.nlev - 1; i >= 0; --i) {
+    for (int i = p.nlev - 1; i >= 1; --i) {
         const int64_t ng = (p.nlev_n[i] + 31) / 32;
         const double *gf = i + 1 < p.nlev ? static_cast<const double *>(p.rcar_f[i + 1]) : nullptr;
         const double *gb = i + 1 < p.nlev ? static_cast<const double *>(p.rcar_b[i + 1]) : nullptr;
