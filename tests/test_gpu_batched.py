@@ -114,26 +114,33 @@ def test_batched_cost_parity():
         assert abs(W[b] - W_ref) <= RTOL * abs(W_ref), (b, W[b], W_ref)
 
 
-def test_batched_c5_shape_sampled_instances():
-    """C5 shape (l=5, N=4096, per-instance eta, 3-component mixtures) at 64 instances; two
-    instances (smallest and largest eta) checked against the log-domain oracle after 3 sweeps."""
+def test_batched_c5_full_batch_sampled_instances():
+    """C5 at its full size and in the bench's launch configuration (8192 instances of l=5, N=4096,
+    per-instance eta, 3-component mixtures); three sampled instances (smallest, median and largest
+    eta) checked against the log-domain oracle after 3 sweeps: log phi and the marginals."""
     cfg = mmot_inputs.CONFIGS["C5"]
-    l, N, B, T = cfg.l, cfg.N, 64, 3
+    l, N, B, T = cfg.l, cfg.N, cfg.batch, 3
     etas = mmot_inputs.c5_etas(B)
-    mus = [mmot_inputs.c5_marginals(b, N, l) for b in range(B)]
-    mu_d = _planes([np.stack([mus[b][q] for b in range(B)]) for q in range(l)])
-    ctx = mm.Context(l, N, list(etas), batch=B)
+    mus_all = mmot_inputs.c5_batch_marginals(0, B, N, l)          # [l][B][N]
+    mu_d = [torch.from_numpy(mus_all[q]).to(DEV) for q in range(l)]
+    ctx = mm.Context(l, N, [float(e) for e in etas], batch=B)
     u = [torch.empty((B, N), dtype=torch.float64, device=DEV) for _ in range(l)]
     ctx.init_uniform(u)
     rep = ctx.sinkhorn(mu_d, T, 0.0, u)
-    assert rep["status"] == 0
-    g = np.stack([x.cpu().numpy() for x in u])
+    assert rep["status"] == 0 and rep["iters_done"] == T
+    picks = [int(np.argmin(etas)), int(np.argsort(etas)[B // 2]), int(np.argmax(etas))]
+    g = np.stack([x[picks].cpu().numpy() for x in u])               # [l][3][N]
+    marg = [ctx.marginal(k, u)[picks].cpu().numpy() for k in range(l)]
     ctx.close()
     h = mmot_inputs.grid_h(N)
-    for b in (int(np.argmin(etas)), int(np.argmax(etas))):
-        g_ref, _, _ = osk.sinkhorn(mus[b], h, etas[b], T, domain="log")
+    for j, b in enumerate(picks):
+        g_ref, _, _ = osk.sinkhorn(mus_all[:, b, :], h, float(etas[b]), T, domain="log")
         fin = np.isfinite(g_ref)
-        assert np.max(np.abs(g[:, b, :][fin] - g_ref[fin]) / np.maximum(1.0, np.abs(g_ref[fin]))) <= 1e-9, b
+        assert np.max(np.abs(g[:, j, :][fin] - g_ref[fin]) / np.maximum(1.0, np.abs(g_ref[fin]))) <= 1e-9, b
+        lw = np.array([-(a * (l - a)) * h / float(etas[b]) for a in range(l + 1)])
+        for k in range(l):
+            m_ref = np.exp(g_ref[k] + regions.marginal_product_log(list(g_ref), k, lw))
+            assert np.abs(marg[k][j] - m_ref).sum() / np.abs(m_ref).sum() <= 1e-10, (b, k)
 
 
 def test_batched_argument_errors():

@@ -97,6 +97,22 @@ def test_c3_fp64_reduced_lockstep(T):
         assert _l1rel(marg[k], m_ref[k]) <= 1e-10
 
 
+def test_c3_full_size_first_sweep():
+    """C3 at its full size (l=6, N=1e5, eta=1e-3) in the bench's launch configuration: one sweep
+    of six fused updates, compared with the oracle's first sweep (plain fp64 region chains,
+    which represent C3), marginals elementwise-L1 and log phi."""
+    cfg = mmot_inputs.CONFIGS["C3"]
+    mus = mmot_inputs.make_marginals("C3", 0)
+    h = mmot_inputs.grid_h(cfg.N)
+    rep, g, marg, W = _run_gpu(mus, cfg.eta, 1)
+    assert rep["status"] == 0 and rep["iters_done"] == 1
+    phis_ref, _, _ = osk.sinkhorn(mus, h, cfg.eta, 1, domain="plain")
+    assert np.max(np.abs(g - np.log(phis_ref))) <= 1e-9
+    m_ref = osk.marginals(phis_ref, h, cfg.eta)
+    for k in range(cfg.l):
+        assert _l1rel(marg[k], m_ref[k]) <= 1e-10, k
+
+
 def test_c4_shape_reduced_lockstep():
     """C4 recipe (l=4, eta=1e-4, smoothed random field) at N=2e5, 3 sweeps."""
     N = 200_000
