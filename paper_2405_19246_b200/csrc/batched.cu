@@ -47,6 +47,11 @@ __device__ __forceinline__ double scale2(double x, int n) {
     const int h = n / 2;
     return (x * pow2i(h)) * pow2i(n - h);
 }
+// 2^n with n clamped to the normal range (branch-free)
+__device__ __forceinline__ double pow2c(int n) {
+    n = max(-1022, min(1023, n));
+    return __longlong_as_double((long long)(n + 1023) << 52);
+}
 // floor(log2 x) of a positive normal double; very negative for 0 / denormals
 __device__ __forceinline__ int ilog2d(double x) {
     const int e = (int)((__double_as_longlong(x) >> 52) & 0x7ff);
@@ -69,11 +74,14 @@ __device__ __forceinline__ void vec_shift(T (&v)[1 << NB], const int (&d)[NB > 0
 #pragma unroll
         for (int b = 0; b < NB; ++b)
             if ((S >> b) & 1) n += d[b];
+        // branch-free exact 2^n in two factors (|n| up to ~2000 without forming 0 / inf early)
+        const int h1 = n >> 1;
+        const double a1 = pow2c(h1), a2 = pow2c(n - h1);
         if constexpr (sizeof(T) == sizeof(double)) {
-            v[S] = scale2(v[S], n);
+            v[S] = (v[S] * a1) * a2;
         } else {
-            reinterpret_cast<Dual &>(v[S]).v = scale2(reinterpret_cast<Dual &>(v[S]).v, n);
-            reinterpret_cast<Dual &>(v[S]).d = scale2(reinterpret_cast<Dual &>(v[S]).d, n);
+            reinterpret_cast<Dual &>(v[S]).v = (reinterpret_cast<Dual &>(v[S]).v * a1) * a2;
+            reinterpret_cast<Dual &>(v[S]).d = (reinterpret_cast<Dual &>(v[S]).d * a1) * a2;
         }
     }
 }
@@ -124,7 +132,7 @@ __device__ void bat_ops(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB +
         cp_async_wait<1>();
         __syncwarp();
         const double *cur = buf + (s & 1) * NB * TILE;
-#pragma unroll
+#pragma unroll 1
         for (int j = 0; j < S; ++j) {
             slab_f<NB, S>(f, cur, lane, j);
             opx_step<NB, T>(G, wt, f, s == 0 && j == 0);
@@ -176,6 +184,7 @@ __device__ void bat_carries(const T *ops, int k, const int (&E)[kMaxL], T (&Fin)
     int d[NB > 0 ? NB : 1];
 #pragma unroll
     for (int b = 0; b < NB; ++b) d[b] = Eb[b] - Enx[b];
+#pragma unroll 1
     for (int s = 0; s < 31; ++s) {
         op_apply<NB, T>(G, cur, y);
         vec_shift<NB, T>(y, d);
@@ -203,6 +212,7 @@ __device__ void bat_carries(const T *ops, int k, const int (&E)[kMaxL], T (&Fin)
     for (int b = 0; b < NB; ++b) d[b] = Eb[b] - Epv[b];
     vec_unit<NB, T>(cur);
     vec_unit<NB, T>(Bend);
+#pragma unroll 1
     for (int s = 31; s > 0; --s) {
         op_apply<NB, T>(G, cur, y);
         vec_shift<NB, T>(y, d);
@@ -248,7 +258,7 @@ __device__ void bat_walk1(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB
         cp_async_wait<1>();
         __syncwarp();
         const double *cur = buf + (t & 1) * NB * TILE;
-#pragma unroll
+#pragma unroll 1
         for (int jj = S - 1; jj >= 0; --jj) {
             slab_f<NB, S>(f, cur, lane, jj);
             dp_diag<NB, T, true>(st, wt);
@@ -298,7 +308,7 @@ __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB 
         T bend[M];
 #pragma unroll
         for (int S2 = 0; S2 < M; ++S2) bend[S2] = ck[(s * M + S2) * 32 + lane];
-#pragma unroll
+#pragma unroll 1
         for (int jb = 0; jb < QPS; ++jb) {
             T st[M];
 #pragma unroll
@@ -381,6 +391,9 @@ __device__ void bat_rescale(double *v, int64_t N, int P, int shift, int lane) {
 // Gauss-Seidel updates, all on device.
 template <int NB>
 __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
+    // The warps of a CTA run the phases of an update in lockstep (CTA barriers between phases),
+    // so only one phase's code is hot in the SM's instruction cache at a time: this kernel is
+    // instruction-fetch bound otherwise (ncu: "no instruction" was the top stall).
     using T = double;
     constexpr int L = NB + 1;
     constexpr int M = 1 << NB;
@@ -392,69 +405,80 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
     double *buf = smem + (size_t)warp * (2 * L + 1) * TILE;
     T *ops = bp.ops + slot * 2 * OpShape<NB>::SZ * 32;
     T *ck = bp.ckpt + slot * (int64_t)(bp.P / S) * M * 32;
-    const int64_t x0 = (int64_t)lane * bp.P, x1 = min(bp.N, x0 + bp.P);
-    for (int64_t inst = slot; inst < bp.batch; inst += bp.slots) {
+    for (int64_t base = (int64_t)blockIdx.x * kBWarps; base < bp.batch; base += bp.slots) {
+        const int64_t inst = base + warp;
+        const bool active = inst < bp.batch;
         T wt[NB + 2];
-        bweights<NB>(wt, bp.eta[inst], bp.h);
+        bweights<NB>(wt, active ? bp.eta[inst] : 1.0, bp.h);
         int E[kMaxL];
 #pragma unroll
-        for (int q = 0; q < kMaxL; ++q) E[q] = q < L ? bp.E[(inst * L + q) * 32 + lane] : 0;
-        int Sh[kMaxL];  // per marginal: exponent of E_q relative to -sum_{p != q} E_p (lazy renormalisation)
+        for (int q = 0; q < kMaxL; ++q) E[q] = (q < L && active) ? bp.E[(inst * L + q) * 32 + lane] : 0;
+        int Sh[kMaxL];  // per marginal: E_q = -sum_{p != q} E_p + Sh_q (lazy renormalisation)
 #pragma unroll
         for (int q = 0; q < kMaxL; ++q) {
             int s2 = 0;
 #pragma unroll
             for (int p = 0; p < L; ++p) s2 += E[p];
-            Sh[q] = q < L ? s2 : 0;  // E_q = -sum_{p != q} E_p + Sh_q  <=>  Sh_q = sum_p E_p
+            Sh[q] = q < L ? s2 : 0;
         }
         bool bad = false;
         int fail = -1;
-        bat_ops<NB, T>(bp, inst, 0, wt, buf, ops, lane);
-        for (int t = 1; t <= bp.iters && !__any_sync(0xffffffffu, bad); ++t) {
+        if (active) bat_ops<NB, T>(bp, inst, 0, wt, buf, ops, lane);
+        __syncthreads();
+        for (int t = 1; t <= bp.iters; ++t) {
+            const bool run = active && !__any_sync(0xffffffffu, bad);
             for (int k = 0; k < L; ++k) {
                 T F[M], B[M];
-                bat_carries<NB, T>(ops, k, E, F, B, lane);
-                bat_walk1<NB, T>(bp, inst, k, wt, B, buf, ck, lane);
+                if (run) {
+                    bat_carries<NB, T>(ops, k, E, F, B, lane);
+                }
+                __syncthreads();
+                if (run) bat_walk1<NB, T>(bp, inst, k, wt, B, buf, ck, lane);
+                __syncthreads();
                 int sumE = 0;
 #pragma unroll
                 for (int q = 0; q < L; ++q)
                     if (q != k) sumE += E[q];
-                double acc = 0.0;
-                bool b2 = false;
                 // phit_k is written as (mu_k / J~) * 2^{-sh_k}, sh_k = the shift chosen at the previous
-                // update of marginal k (lazy renormalisation: fp64 leaves ~2^900 of headroom, so the
-                // chain is rescaled only when its maximum exponent drifts beyond +-kRenorm)
+                // update of marginal k (lazy renormalisation: the chain is rescaled only when its
+                // maximum exponent drifts beyond +-renorm)
                 int shk = 0;
 #pragma unroll
                 for (int q = 0; q < L; ++q)
                     if (q == k) shk = Sh[q];
-                const int emax = bat_walk2<NB, T, MODE_UPD, 4>(bp, inst, k, wt, F, buf, ck, sumE, shk, acc, b2, lane);
-                if (b2 && fail < 0) fail = t;
-                bad |= b2;
-                int sh = shk;
-                const int resc = (emax > -1000000 && (emax > bp.renorm || emax < -bp.renorm)) ? emax : 0;
-                // (walk 2 ended with a __syncwarp after its last slab store: the vector is visible)
-                bat_rescale(bp.phit[k] + inst * bp.N, bp.N, bp.P, resc, lane);
-                sh += resc;
-                __syncwarp();
+                if (run) {
+                    double acc = 0.0;
+                    bool b2 = false;
+                    const int emax = bat_walk2<NB, T, MODE_UPD, 4>(bp, inst, k, wt, F, buf, ck, sumE, shk, acc, b2, lane);
+                    if (b2 && fail < 0) fail = t;
+                    bad |= b2;
+                    const int resc = (emax > -1000000 && (emax > bp.renorm || emax < -bp.renorm)) ? emax : 0;
+                    // (walk 2 ended with a __syncwarp after its last slab store: the vector is visible)
+                    bat_rescale(bp.phit[k] + inst * bp.N, bp.N, bp.P, resc, lane);
+                    __syncwarp();
 #pragma unroll
-                for (int q = 0; q < L; ++q)
-                    if (q == k) {
-                        E[q] = -sumE + sh;
-                        Sh[q] = sh;
-                    }
+                    for (int q = 0; q < L; ++q)
+                        if (q == k) {
+                            E[q] = -sumE + shk + resc;
+                            Sh[q] = shk + resc;
+                        }
+                }
+                __syncthreads();
                 // chain operators of the next update's bound set
-                bat_ops<NB, T>(bp, inst, (k + 1) % L, wt, buf, ops, lane);
+                if (run) bat_ops<NB, T>(bp, inst, (k + 1) % L, wt, buf, ops, lane);
+                __syncthreads();
             }
         }
+        if (active) {
 #pragma unroll
-        for (int q = 0; q < L; ++q) bp.E[(inst * L + q) * 32 + lane] = E[q];
-        const bool anybad = __any_sync(0xffffffffu, bad);
-        int fi = fail;
-        for (int o = 16; o > 0; o >>= 1) fi = max(fi, __shfl_down_sync(0xffffffffu, fi, o));
-        if (lane == 0) {
-            bp.status[inst] = anybad ? 6 : 0;
-            bp.fail_iter[inst] = anybad ? fi : -1;
+            for (int q = 0; q < L; ++q) bp.E[(inst * L + q) * 32 + lane] = E[q];
+            const bool anybad = __any_sync(0xffffffffu, bad);
+            int fi = fail;
+            for (int o = 16; o > 0; o >>= 1) fi = max(fi, __shfl_down_sync(0xffffffffu, fi, o));
+            if (lane == 0) {
+                bp.status[inst] = anybad ? 6 : 0;
+                bp.fail_iter[inst] = anybad ? fi : -1;
+            }
         }
     }
 }
