@@ -31,7 +31,7 @@
 namespace mmot {
 
 constexpr int kBS = 8;          // slab = checkpoint block (points per chain)
-constexpr int kBWarps = 4;      // warps (instances) per CTA
+constexpr int kBWarps = 8;      // warps (instances) per CTA (one CTA per SM, all in lockstep)
 constexpr int kRenorm = 96;     // lazy renormalisation threshold: |max exponent of a chain| (products of l <= 5 mantissas stay below 2^480)
 static const int g_renorm = [] { const char *e = getenv("MMOT_BAT_RENORM"); return e ? atoi(e) : kRenorm; }();
 
