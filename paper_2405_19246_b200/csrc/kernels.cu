@@ -184,30 +184,45 @@ __global__ void __launch_bounds__(128) k_ops_reduce_c(const T *in_f, const T *in
         A[i][q] = i < cnt && opx_valid<NB>(q) ? in[e] : ((q % M) == 0 && i >= cnt ? one_of(T{}) : zero_of(T{}));
     }
     __syncthreads();
+    constexpr int IT = (GS / 2 * SZ + 127) / 128;  // entries per thread at the widest step
+#pragma unroll
     for (int step = 1; step < GS; step <<= 1) {
         // pairs (i, i + step), i a multiple of 2 step; prefix order applies member i first,
         // suffix order applies member i + step first
-        T res[(GS * SZ + 127) / 128];
-        int nres = 0;
-        for (int e = threadIdx.x; e < (GS / (2 * step)) * SZ; e += blockDim.x) {
-            const int pr = e / SZ, q = e % SZ;
-            const int c = q / M, V = q % M;
-            const int i = pr * 2 * step;
-            const T *X = dir == 0 ? A[i] : A[i + step];      // applied first
-            const T *Y = dir == 0 ? A[i + step] : A[i];      // applied second
-            T acc = zero_of(T{});
-            if (pc(V) <= NB - c)
-                for (int U = V;; U = (U - 1) & V) {          // C_c[V] = sum_{U subset V} X_c[U] Y_{c+|U|}[V\U]
-                    acc = mad(X[c * M + U], Y[(c + pc(U)) * M + (V ^ U)], acc);
-                    if (U == 0) break;
+        const int lim = (GS / (2 * step)) * SZ;
+        T res[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int e = threadIdx.x + it * 128;
+            res[it] = zero_of(T{});
+            if (e < lim) {
+                const int pr = e / SZ, q = e % SZ;
+                const int c = q / M, V = q % M;
+                const int i = pr * 2 * step;
+                const T *X = dir == 0 ? A[i] : A[i + step];      // applied first
+                const T *Y = dir == 0 ? A[i + step] : A[i];      // applied second
+                if (pc(V) <= NB - c) {
+                    // C_c[V] = sum_{U subset V} X_c[U] Y_{c+|U|}[V\U]: 2^|V| terms, counted loop
+                    // (two accumulators, unrolled so the shared-memory loads run ahead)
+                    const int nt = 1 << pc(V);
+                    T a0 = zero_of(T{}), a1 = zero_of(T{});
+                    int U = V;
+#pragma unroll 4
+                    for (int t = 0; t < nt; ++t) {
+                        const T x = X[c * M + U], y = Y[(c + pc(U)) * M + (V ^ U)];
+                        if (t & 1) a1 = mad(x, y, a1);
+                        else a0 = mad(x, y, a0);
+                        U = (U - 1) & V;
+                    }
+                    res[it] = a0 + a1;
                 }
-            res[nres++] = acc;
+            }
         }
         __syncthreads();
-        nres = 0;
-        for (int e = threadIdx.x; e < (GS / (2 * step)) * SZ; e += blockDim.x) {
-            const int pr = e / SZ, q = e % SZ;
-            A[pr * 2 * step][q] = res[nres++];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int e = threadIdx.x + it * 128;
+            if (e < lim) A[(e / SZ) * 2 * step][e % SZ] = res[it];
         }
         __syncthreads();
     }
@@ -241,10 +256,18 @@ __global__ void __launch_bounds__(64) k_ops_down_c(const T *ops_f, const T *ops_
         const int S = threadIdx.x;
         if (S < M) {
             car[(first + i) * M + S] = cur[S];
-            for (int U = S;; U = (U - 1) & S) {              // Op(cur)[S] = sum_{U subset S} cur[U] G_|U|[S\U]
-                nx = mad(cur[U], G[i][pc(U) * M + (S ^ U)], nx);
-                if (U == 0) break;
+            // Op(cur)[S] = sum_{U subset S} cur[U] G_|U|[S\U]
+            const int nt = 1 << pc(S);
+            T a0 = zero_of(T{}), a1 = zero_of(T{});
+            int U = S;
+#pragma unroll 4
+            for (int t = 0; t < nt; ++t) {
+                const T x = cur[U], y = G[i][pc(U) * M + (S ^ U)];
+                if (t & 1) a1 = mad(x, y, a1);
+                else a0 = mad(x, y, a0);
+                U = (U - 1) & S;
             }
+            nx = a0 + a1;
         }
         __syncthreads();
         if (S < M) {
