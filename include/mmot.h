@@ -146,6 +146,14 @@ MMOT_API void mmot_shard_range(int64_t N_global, int rank, int world, int64_t *l
 MMOT_API mmot_status mmot_compose_rank_carries(int l, const double *ops_all, int world, int rank, double *fin,
                                                double *bin);
 
+/* Host reference of the composition sharded contexts run on device for the restricted
+ * next-update scan (single-walk Sinkhorn updates, l in 3..5; no GPU needed): elems_all =
+ * [world][2][l 2^(l-2)] gathered whole-shard affine elements (prefix, suffix; entry A_c[V] at
+ * (c-1) 2^(l-2) + V for c = 1..l-1, offsets at (l-1) 2^(l-2) + U), fin / bin = the 2^(l-2)
+ * new-part states entering shard `rank` from the left / right. */
+MMOT_API mmot_status mmot_compose_rank_affine(int l, const double *elems_all, int world, int rank, double *fin,
+                                              double *bin);
+
 /* m_k = phi_k * J_k(phi_{-k}) -- the k-th marginal of K . (phi_1 x ... x phi_l)
  * (P:1021), computed by the O(N) separated-summation scans.
  *   k in [0, l); u: host array of l device pointers (repr per opts, float64, length N each);

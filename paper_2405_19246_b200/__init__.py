@@ -13,7 +13,7 @@ import os
 from typing import List, Optional, Sequence
 
 __all__ = ["Context", "MMOTError", "lib_path", "load_library", "STATUS", "exported_symbols", "nccl_unique_id",
-           "shard_range", "compose_rank_carries"]
+           "shard_range", "compose_rank_carries", "compose_rank_affine"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libmmot.so")
@@ -82,6 +82,8 @@ def load_library():
     dpp = ctypes.POINTER(ctypes.c_double)
     lib.mmot_compose_rank_carries.argtypes = [ctypes.c_int, dpp, ctypes.c_int, ctypes.c_int, dpp, dpp]
     lib.mmot_compose_rank_carries.restype = ctypes.c_int
+    lib.mmot_compose_rank_affine.argtypes = [ctypes.c_int, dpp, ctypes.c_int, ctypes.c_int, dpp, dpp]
+    lib.mmot_compose_rank_affine.restype = ctypes.c_int
     lib.mmot_marginal.argtypes = [vp, ctypes.c_int, vpp, vp]
     lib.mmot_marginal.restype = ctypes.c_int
     lib.mmot_sinkhorn.argtypes = [vp, vpp, ctypes.c_int, ctypes.c_double, vpp, ctypes.POINTER(_Report)]
@@ -157,6 +159,22 @@ def compose_rank_carries(l: int, ops_all, world: int, rank: int):
     dp = ctypes.POINTER(ctypes.c_double)
     st = lib.mmot_compose_rank_carries(int(l), a.ctypes.data_as(dp), int(world), int(rank), fin.ctypes.data_as(dp),
                                        bin_.ctypes.data_as(dp))
+    if st != 0:
+        raise MMOTError(st, lib.mmot_last_error(None).decode())
+    return fin, bin_
+
+
+def compose_rank_affine(l: int, elems_all, world: int, rank: int):
+    """Host reference of the sharded restricted-scan composition (C ABI, no GPU needed).
+    elems_all: float64 array [world][2][l * 2**(l-2)].  Returns (fin, bin) arrays of 2**(l-2)."""
+    import numpy as np
+    lib = load_library()
+    a = np.ascontiguousarray(elems_all, dtype=np.float64)
+    MO = 1 << (l - 2)
+    fin, bin_ = np.zeros(MO), np.zeros(MO)
+    dp = ctypes.POINTER(ctypes.c_double)
+    st = lib.mmot_compose_rank_affine(int(l), a.ctypes.data_as(dp), int(world), int(rank), fin.ctypes.data_as(dp),
+                                      bin_.ctypes.data_as(dp))
     if st != 0:
         raise MMOTError(st, lib.mmot_last_error(None).decode())
     return fin, bin_

@@ -592,10 +592,9 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
 // ---------------------------------------------------------------------------------------
 // Sharded contexts: all-gather of the whole-shard operators ([2][SZ] elements of elem_bytes)
 // on the context stream (called from inside the scan, between up-sweep and down-sweep).
-static void shard_exchange(void *vctx, int elem_bytes, cudaStream_t s) {
+static void shard_exchange(void *vctx, size_t n, cudaStream_t s) {
     mmot_ctx *c = static_cast<mmot_ctx *>(vctx);
     const size_t SZ = (size_t)c->l * (1 << (c->l - 1));
-    const size_t n = 2 * SZ * (size_t)(elem_bytes / 8);
     const nccl_result r = g_nccl.AllGather(c->shard_mem, c->shard_mem + 2 * SZ * 2, n, kNcclFloat64, c->comm, s);
     if (r != 0 && !c->exch_error) {
         c->exch_error = r;
@@ -725,7 +724,7 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
     int ops_for = -1;  // bound set whose chain operators are currently in ops level 0
     // restricted next-update scan: carries alternate between the context's level-0 arrays (0) and
     // the second set (1); rx_ready = the previous update wrote this update's affine elements
-    const bool rx = c->rx && !c->sharded;
+    const bool rx = c->rx && (!c->sharded || c->nlev >= 2);
     int cur = 0;
     bool rx_ready = false;
     void *cf[2] = {c->car_f[0], c->carB_f}, *cb[2] = {c->car_bi, c->carB_bi};
@@ -966,6 +965,17 @@ mmot_status mmot_compose_rank_carries(int l, const double *ops_all, int world, i
         case 4: mmot::compose_rank_carries<4, double>(ops_all, world, rank, fin, bin); break;
         case 5: mmot::compose_rank_carries<5, double>(ops_all, world, rank, fin, bin); break;
         default: set_err(nullptr, "l=%d unsupported", l); return MMOT_EINVAL;
+    }
+    return MMOT_OK;
+}
+
+mmot_status mmot_compose_rank_affine(int l, const double *elems_all, int world, int rank, double *fin, double *bin) {
+    if (!elems_all || !fin || !bin || world < 1 || rank < 0 || rank >= world) { set_err(nullptr, "bad arguments"); return MMOT_EINVAL; }
+    switch (l - 1) {
+        case 2: mmot::compose_rank_affine<2>(elems_all, world, rank, fin, bin); break;
+        case 3: mmot::compose_rank_affine<3>(elems_all, world, rank, fin, bin); break;
+        case 4: mmot::compose_rank_affine<4>(elems_all, world, rank, fin, bin); break;
+        default: set_err(nullptr, "l=%d unsupported (3..5)", l); return MMOT_EINVAL;
     }
     return MMOT_OK;
 }

@@ -479,4 +479,39 @@ __device__ __forceinline__ void rx_compose(const double (&X)[Rx<NB>::SZE], const
     for (int U = 0; U < MO; ++U) Z[NB * MO + U] = yo[U];
 }
 
+// Sharded contexts with the restricted scan: gathered whole-shard affine elements
+// all = [world][2][SZE] (prefix, suffix); new-part carries entering shard `rank`:
+//   fin = E_{rank-1} o ... o E_0 (0),   bin = E_{rank+1} o ... o E_{world-1} (0)
+// (the new part of e_{} is zero).  Same code on host and device.
+template <int NB>
+__host__ __device__ inline void compose_rank_affine(const double *all, int world, int rank, double *fin, double *bin) {
+    constexpr int MO = Rx<NB>::MO;
+    constexpr int SZE = Rx<NB>::SZE;
+    double y[MO], z[MO];
+    for (int U = 0; U < MO; ++U) y[U] = 0.0;
+    for (int r = 0; r < rank; ++r) {
+        const double *E = all + ((size_t)r * 2 + 0) * SZE;
+        for (int S = 0; S < MO; ++S) {
+            double acc = E[NB * MO + S];
+            for (int U = 0; U < MO; ++U)
+                if ((U & S) == U) acc += y[U] * E[pc(U) * MO + (S ^ U)];
+            z[S] = acc;
+        }
+        for (int U = 0; U < MO; ++U) y[U] = z[U];
+    }
+    for (int U = 0; U < MO; ++U) fin[U] = y[U];
+    for (int U = 0; U < MO; ++U) y[U] = 0.0;
+    for (int r = world - 1; r > rank; --r) {
+        const double *E = all + ((size_t)r * 2 + 1) * SZE;
+        for (int S = 0; S < MO; ++S) {
+            double acc = E[NB * MO + S];
+            for (int U = 0; U < MO; ++U)
+                if ((U & S) == U) acc += y[U] * E[pc(U) * MO + (S ^ U)];
+            z[S] = acc;
+        }
+        for (int U = 0; U < MO; ++U) y[U] = z[U];
+    }
+    for (int U = 0; U < MO; ++U) bin[U] = y[U];
+}
+
 }  // namespace mmot

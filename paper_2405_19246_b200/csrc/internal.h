@@ -55,7 +55,7 @@ struct Plan {
     void *rxe_f[kMaxLevels], *rxe_b[kMaxLevels];    // affine elements per level
     void *rcar_f[kMaxLevels], *rcar_b[kMaxLevels];  // new-part carries per level (levels >= 1)
     void *ncar_f, *ncar_bi;                         // next update's full carries (old parts)
-    void (*exch)(void *ctx, int elem_bytes, cudaStream_t s);
+    void (*exch)(void *ctx, size_t doubles_per_rank, cudaStream_t s);
     void *exch_ctx;
     void *agg_send, *agg_all, *rank_car;
     int world, rank;

@@ -1205,6 +1205,11 @@ __global__ void __launch_bounds__(128) k_rx_down_w(const double *el_f, const dou
 // Levels >= 1 (level 0 is fused into the update kernels: reduce at the end of update k, down at
 // the start of update k+1).
 template <int NB>
+__global__ void k_rx_compose(const double *all, int world, int rank, double *car) {
+    if (threadIdx.x == 0) compose_rank_affine<NB>(all, world, rank, car, car + Rx<NB>::MO);
+}
+
+template <int NB>
 static void launch_rx_scan(const Plan &p, cudaStream_t s, int64_t *launches) {
     for (int i = 1; i + 1 < p.nlev; ++i) {
         const int64_t ng = p.nlev_n[i + 1];
@@ -1213,10 +1218,25 @@ static void launch_rx_scan(const Plan &p, cudaStream_t s, int64_t *launches) {
             static_cast<double *>(p.rxe_f[i + 1]), static_cast<double *>(p.rxe_b[i + 1]), p.nlev_n[i], p.stop);
         ++*launches;
     }
+    // sharded contexts: whole-shard affine elements (top level reduced to one), all-gathered,
+    // composed into the new-part carries entering this shard
+    const int top = p.nlev - 1;
+    if (p.exch) {
+        k_rx_reduce_w<NB><<<dim3(1, 2), 128, 0, s>>>(
+            static_cast<const double *>(p.rxe_f[top]), static_cast<const double *>(p.rxe_b[top]),
+            static_cast<double *>(p.agg_send), static_cast<double *>(p.agg_send) + Rx<NB>::SZE, p.nlev_n[top], p.stop);
+        ++*launches;
+        p.exch(p.exch_ctx, 2 * (size_t)Rx<NB>::SZE, s);
+        k_rx_compose<NB><<<1, 1, 0, s>>>(static_cast<const double *>(p.agg_all), p.world, p.rank,
+                                        static_cast<double *>(p.rank_car));
+        ++*launches;
+    }
     for (int i = p.nlev - 1; i >= 1; --i) {
         const int64_t ng = (p.nlev_n[i] + 31) / 32;
-        const double *gf = i + 1 < p.nlev ? static_cast<const double *>(p.rcar_f[i + 1]) : nullptr;
-        const double *gb = i + 1 < p.nlev ? static_cast<const double *>(p.rcar_b[i + 1]) : nullptr;
+        const double *gf = i + 1 < p.nlev ? static_cast<const double *>(p.rcar_f[i + 1])
+                                          : (p.exch ? static_cast<const double *>(p.rank_car) : nullptr);
+        const double *gb = i + 1 < p.nlev ? static_cast<const double *>(p.rcar_b[i + 1])
+                                          : (p.exch ? static_cast<const double *>(p.rank_car) + Rx<NB>::MO : nullptr);
         k_rx_down_w<NB><<<dim3((unsigned)((ng + 3) / 4), 2), 128, 0, s>>>(
             static_cast<const double *>(p.rxe_f[i]), static_cast<const double *>(p.rxe_b[i]), gf, gb,
             static_cast<double *>(p.rcar_f[i]), static_cast<double *>(p.rcar_b[i]), p.nlev_n[i], p.stop,
@@ -1539,7 +1559,7 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
                                                          p.nlev_n[top], p.stop);
         }
         ++*launches;
-        p.exch(p.exch_ctx, (int)sizeof(T), s);
+        p.exch(p.exch_ctx, 2 * (size_t)OpShape<NB>::SZ * (sizeof(T) / sizeof(double)), s);
         k_compose<NB, T><<<1, 1, 0, s>>>(static_cast<const T *>(p.agg_all), p.world, p.rank,
                                          static_cast<T *>(p.rank_car));
         ++*launches;
