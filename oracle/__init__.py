@@ -26,6 +26,6 @@ Everything is plain fp64 and follows the paper (``P:n`` = line n of PAPER.md):
 * ``comonotone`` -- closed-form unregularised optimum W_0 of the 1-D pairwise
                  L1 MMOT (sanity pin: W_eta >= W_0).
 
-Parity status of every function is listed in DESIGN.md §2 ("pins").
+Every function and the tests that pin it are listed in DESIGN.md §2b; none is "parity unpinned".
 """
 from . import dense, paper3, regions, sinkhorn, comonotone  # noqa: F401
