@@ -376,7 +376,12 @@ def run_mmot(args, cfg):
     # roofline of the dominant kernel group: the fused Sinkhorn update (one product of mode
     # "update" = operator pass + scan + apply).  Algorithmic bytes per update = (l+1) N 8.
     n_upd = prof["mode_n"]["update"]
-    upd_ms = prof["mode_ms"]["update"] / max(n_upd, 1)
+    if n_upd > 0:
+        upd_ms = prof["mode_ms"]["update"] / n_upd
+    else:
+        # persistent kernel (small instances): all sweeps in one launch, no per-update events;
+        # the step time per update is an upper bound of the update time
+        upd_ms = ms / max(iters_done * l, 1)
     alg_bytes = (l + 1) * Nl * 8
     peak, peak_src = _peaks()
     achieved = alg_bytes / (upd_ms / 1e3) / 1e9

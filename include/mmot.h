@@ -79,7 +79,13 @@ typedef struct { double x_min, x_max; } mmot_grid;
  *   SINGLE_WALK: suffix states walked forward through the inverse recurrence step (each grid
  *         point read once); l <= 5.  Its rounding error grows like exp(P * max_a a(l-a) h/eta),
  *         so outside the bound above the caller accepts the accuracy loss. */
-typedef enum { MMOT_KERNEL_AUTO = 0, MMOT_KERNEL_TWO_WALK = 1, MMOT_KERNEL_SINGLE_WALK = 2 } mmot_kernel;
+typedef enum {
+    MMOT_KERNEL_AUTO = 0,
+    MMOT_KERNEL_TWO_WALK = 1,
+    MMOT_KERNEL_SINGLE_WALK = 2,
+    MMOT_KERNEL_PERSISTENT = 3  /* one warp per instance, all sweeps in one launch (the batched kernel,
+                                   batch = 1); AUTO picks it for l <= 5, N <= 4096, MMOT_F64, chunk = 0 */
+} mmot_kernel;
 
 typedef struct {
     int check_every;    /* residual cadence in sweeps; 0 = only when tol > 0, every sweep (default) */
@@ -113,8 +119,10 @@ MMOT_API mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, m
  *   dt: MMOT_F64 (MMOT_F32 -> EUNSUPPORTED in this build).  eta_host is copied.
  * Layouts for the compute calls on a batched context: every array argument is a plane of
  * `batch` consecutive N-vectors ([batch][N], instance-major); mmot_cost fills W[batch] (host);
- * mmot_sinkhorn runs exactly `iters` sweeps per instance (tol must be <= 0, else EUNSUPPORTED),
- * one warp per instance on device, and reports the first failing instance (if any).
+ * mmot_sinkhorn runs at most `iters` sweeps per instance, one warp per instance on device, each
+ * instance stopping at its own first residual <= tol (tol > 0; residual every check_every sweeps);
+ * the report gives the max sweeps done and max last residual over the instances, converged = all
+ * converged, and the first failing instance's status (if any).
  * Internally each instance's scalings carry one exponent per 1/32 of the grid and marginal,
  * so instances whose |log phi| exceeds the fp64 range (eta = 1e-3) stay representable. */
 MMOT_API mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *eta_host, mmot_grid grid,

@@ -203,7 +203,7 @@ class Context:
         self.repr = repr
         self.h = (self.grid[1] - self.grid[0]) / (self.N - 1) if self.N > 1 else 1.0
         self.stream = stream if stream is not None else torch.cuda.current_stream()
-        kern = {"auto": 0, "two_walk": 1, "single_walk": 2}[kernel]
+        kern = {"auto": 0, "two_walk": 1, "single_walk": 2, "persistent": 3}[kernel]
         opts = _Opts(int(check_every), 0, LOG if repr == "log" else LINEAR, int(chunk), kern)
         ctx = ctypes.c_void_p()
         self.shard = shard
@@ -250,7 +250,8 @@ class Context:
         """Launch plan: chain length P, number of chains, kernel family ("two_walk"/"single_walk")."""
         P, n, k = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
         self._check(self._lib.mmot_info(self._ctx, ctypes.byref(P), ctypes.byref(n), ctypes.byref(k)))
-        return dict(chain_len=P.value, nchains=n.value, kernel={1: "two_walk", 2: "single_walk"}[k.value])
+        return dict(chain_len=P.value, nchains=n.value,
+                    kernel={1: "two_walk", 2: "single_walk", 3: "persistent"}[k.value])
 
     @property
     def launches(self) -> int:

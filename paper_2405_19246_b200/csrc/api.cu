@@ -120,7 +120,8 @@ struct mmot_ctx {
     int *bat_int = nullptr;                 // E, status, fail_iter
     void **bat_ptrs = nullptr;              // device array of l pointers (u[] for import/export)
     double *bat_whost = nullptr;            // pinned [batch]
-    int *bat_shost = nullptr;               // pinned [2*batch]
+    int *bat_shost = nullptr;               // pinned [4*batch]: status, fail_iter, iters_done, converged
+    double *bat_rhost = nullptr;            // pinned [batch]: last residual
     double *stage_mu[mmot::kMaxL] = {nullptr};
     double *stage_u[mmot::kMaxL] = {nullptr};
     int *hstop = nullptr;       // pinned, async stop polling
@@ -195,9 +196,9 @@ int64_t mmot_launch_count(const mmot_ctx *ctx) { return ctx ? ctx->launches : 0;
 
 mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t *nchains, int *kernel) {
     if (!ctx) { set_err(nullptr, "NULL context"); return MMOT_EINVAL; }
-    if (chain_len) *chain_len = ctx->P;
-    if (nchains) *nchains = ctx->nchunks;
-    if (kernel) *kernel = ctx->sw ? MMOT_KERNEL_SINGLE_WALK : MMOT_KERNEL_TWO_WALK;
+    if (chain_len) *chain_len = ctx->batched ? ctx->ba.P : ctx->P;
+    if (nchains) *nchains = ctx->batched ? 32 * ctx->batch : ctx->nchunks;
+    if (kernel) *kernel = ctx->batched ? MMOT_KERNEL_PERSISTENT : (ctx->sw ? MMOT_KERNEL_SINGLE_WALK : MMOT_KERNEL_TWO_WALK);
     return MMOT_OK;
 }
 
@@ -218,6 +219,7 @@ void mmot_destroy(mmot_ctx *ctx) {
     cudaFree(ctx->bat_ptrs);
     if (ctx->bat_whost) cudaFreeHost(ctx->bat_whost);
     if (ctx->bat_shost) cudaFreeHost(ctx->bat_shost);
+    if (ctx->bat_rhost) cudaFreeHost(ctx->bat_rhost);
     for (int q = 0; q < mmot::kMaxL; ++q) {
         cudaFree(ctx->lin[q]);
         cudaFree(ctx->mu_t[q]);
@@ -245,12 +247,21 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
     }
     if (dt != MMOT_F64 && dt != MMOT_F32) { set_err(nullptr, "bad dtype"); return MMOT_EINVAL; }
     if (opts && (opts->check_every < 0 || opts->chunk < 0 || (opts->repr != MMOT_LOG && opts->repr != MMOT_LINEAR) ||
-                 opts->kernel < MMOT_KERNEL_AUTO || opts->kernel > MMOT_KERNEL_SINGLE_WALK)) {
+                 opts->kernel < MMOT_KERNEL_AUTO || opts->kernel > MMOT_KERNEL_PERSISTENT)) {
         set_err(nullptr, "bad opts");
         return MMOT_EINVAL;
     }
     if (l > MMOT_MAX_L) { set_err(nullptr, "l=%d > MMOT_MAX_L=%d in this build", l, MMOT_MAX_L); return MMOT_EUNSUPPORTED; }
     if (dt == MMOT_F32) { set_err(nullptr, "MMOT_F32 single-instance contexts are not implemented yet"); return MMOT_EUNSUPPORTED; }
+    // small instances: the persistent batched kernel with one instance (all sweeps in one launch,
+    // no per-update kernel latency)
+    const int kern = opts ? opts->kernel : MMOT_KERNEL_AUTO;
+    const int chunk = opts ? opts->chunk : 0;
+    if (kern == MMOT_KERNEL_PERSISTENT ||
+        (kern == MMOT_KERNEL_AUTO && chunk == 0 && l <= 5 && N <= 4096 && getenv("MMOT_NO_PERSISTENT") == nullptr)) {
+        if (l > 5) { set_err(nullptr, "the persistent kernel supports l <= 5"); return MMOT_EUNSUPPORTED; }
+        return mmot_create_batched(l, N, 1, &eta, grid, dt, opts, cuda_stream, out);
+    }
 
     mmot_ctx *c = new mmot_ctx();
     c->l = l;
@@ -477,13 +488,14 @@ mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *e
     const size_t nd = (size_t)batch                      // eta
                       + (size_t)l * batch * N            // phit
                       + (size_t)a.slots * (opsz + cksz) / sizeof(double)
-                      + (size_t)batch;                   // wout
-    const size_t ni = (size_t)batch * l * 32 + 2 * (size_t)batch;
+                      + 2 * (size_t)batch;               // wout, resid
+    const size_t ni = (size_t)batch * l * 32 + 4 * (size_t)batch;
     bool ok = cudaMalloc(&c->bat_mem, nd * sizeof(double)) == cudaSuccess &&
               cudaMalloc(&c->bat_int, ni * sizeof(int)) == cudaSuccess &&
               cudaMalloc(&c->bat_ptrs, 2 * mmot::kMaxL * sizeof(void *)) == cudaSuccess &&
               cudaMallocHost(&c->bat_whost, (size_t)batch * sizeof(double)) == cudaSuccess &&
-              cudaMallocHost(&c->bat_shost, 2 * (size_t)batch * sizeof(int)) == cudaSuccess &&
+              cudaMallocHost(&c->bat_shost, 4 * (size_t)batch * sizeof(int)) == cudaSuccess &&
+              cudaMallocHost(&c->bat_rhost, (size_t)batch * sizeof(double)) == cudaSuccess &&
               cudaMallocHost(&c->hsc, sizeof(DevScalars)) == cudaSuccess &&
               cudaMalloc(&c->ws, sizeof(DevScalars)) == cudaSuccess;
     if (!ok) {
@@ -505,9 +517,12 @@ mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *e
     a.ckpt = p;
     p += (size_t)a.slots * cksz / sizeof(double);
     a.wout = p;
+    a.resid = p + batch;
     a.E = c->bat_int;
     a.status = c->bat_int + (size_t)batch * l * 32;
     a.fail_iter = a.status + batch;
+    a.iters_done = a.status + 2 * batch;
+    a.converged = a.status + 3 * batch;
     if (cudaMemsetAsync(c->bat_mem, 0, nd * sizeof(double), c->stream) != cudaSuccess ||
         cudaMemsetAsync(c->bat_int, 0, ni * sizeof(int), c->stream) != cudaSuccess ||
         cudaMemsetAsync(c->dsc, 0, sizeof(DevScalars), c->stream) != cudaSuccess ||
@@ -545,7 +560,6 @@ static mmot_status bat_import(mmot_ctx *c, const void *const *u) {
 
 static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters, double tol, void *const *u,
                                 mmot_report *rep) {
-    if (tol > 0) { set_err(c, "batched contexts run a fixed number of sweeps (tol must be <= 0)"); return MMOT_EUNSUPPORTED; }
     mmot_status st = reset_scalars(c);
     if (st) return st;
     const int64_t n = c->batch * c->N;
@@ -568,20 +582,31 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
     mmot::BatchArgs a = c->ba;
     for (int q = 0; q < c->l; ++q) a.mu[q] = mu[q];
     a.iters = iters;
+    a.tol = tol;
+    a.check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
     CK(c, mmot::launch_batched(a, 0, c->stream, &c->launches));
     st = bat_upload_ptrs(c, const_cast<const void *const *>(u), 0);
     if (st) return st;
     CK(c, mmot::launch_bat_convert(c->ba, c->bat_ptrs, 0, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
-    CK(c, cudaMemcpyAsync(c->bat_shost, c->ba.status, 2 * (size_t)c->batch * sizeof(int), cudaMemcpyDeviceToHost,
+    CK(c, cudaMemcpyAsync(c->bat_shost, c->ba.status, 4 * (size_t)c->batch * sizeof(int), cudaMemcpyDeviceToHost,
+                          c->stream));
+    CK(c, cudaMemcpyAsync(c->bat_rhost, c->ba.resid, (size_t)c->batch * sizeof(double), cudaMemcpyDeviceToHost,
                           c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
-    int status = 0, fail = -1;
-    for (int64_t b = 0; b < c->batch && !status; ++b)
-        if (c->bat_shost[b]) { status = c->bat_shost[b]; fail = c->bat_shost[c->batch + b]; }
+    int status = 0, fail = -1, done = 0, conv = 1;
+    double res = 0.0;
+    const int64_t B = c->batch;
+    for (int64_t b = 0; b < B; ++b) {
+        if (c->bat_shost[b] && !status) { status = c->bat_shost[b]; fail = c->bat_shost[B + b]; }
+        done = std::max(done, c->bat_shost[2 * B + b]);
+        conv &= c->bat_shost[3 * B + b];
+        res = std::max(res, c->bat_rhost[b]);  // NaN (never computed) propagates as "not a number"
+        if (isnan(c->bat_rhost[b])) res = NAN;
+    }
     if (rep) {
-        rep->iters_done = status ? fail : iters;
-        rep->residual = NAN;
-        rep->converged = 0;
+        rep->iters_done = done;                      // max over instances
+        rep->residual = tol > 0 ? res : NAN;         // max over instances
+        rep->converged = tol > 0 && conv;            // all instances
         rep->status = status;
         rep->fail_iter = status ? fail : -1;
     }
@@ -863,7 +888,7 @@ mmot_status mmot_sinkhorn_host(mmot_ctx *c, const void *const *marginals_host, i
         mu[q] = c->stage_mu[q];
         ud[q] = c->stage_u[q];
     }
-    mmot_status st = sinkhorn_impl(c, mu, iters, tol, ud, rep);
+    mmot_status st = c->batched ? bat_sinkhorn(c, mu, iters, tol, ud, rep) : sinkhorn_impl(c, mu, iters, tol, ud, rep);
     for (int q = 0; q < c->l; ++q)
         CK(c, cudaMemcpyAsync(u_host[q], c->stage_u[q], bytes, cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));

@@ -105,6 +105,11 @@ struct BPlan {
     int *status;                    // [batch] per-instance status (0 ok, EOVERFLOW)
     int *fail_iter;                 // [batch]
     int renorm;                     // lazy renormalisation threshold (kRenorm)
+    double tol;                     // residual tolerance (<= 0: fixed sweeps)
+    int check_every;                // residual cadence (sweeps)
+    int *iters_done;                // [batch]
+    int *converged;                 // [batch]
+    double *resid;                  // [batch]
 };
 
 // ---------------------------------------------------------------------------------------
@@ -350,6 +355,10 @@ __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB 
                     if (nz) emax = max(emax, ilog2d(o));
                 } else if (MODE == MODE_MARG) {
                     obuf[lane * (S + 1) + jx] = scale2(vk * jv, e_true);
+                } else if (MODE == MODE_RES) {
+                    // |m_k - mu_k| (P:168 generalised); mu_k read directly (residual sweeps only)
+                    const int64_t x = x0 + (int64_t)s * S + jx;
+                    if (x < N) acc += fabs(scale2(vk * jv, e_true) - __ldg(bp.mu[k] + inst * N + x));
                 } else if (MODE == MODE_COST) {
                     if constexpr (sizeof(T) == sizeof(Dual)) acc += scale2(vk * reinterpret_cast<const Dual &>(J).d, e_true);
                 }
@@ -425,8 +434,11 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
         int fail = -1;
         if (active) bat_ops<NB, T>(bp, inst, 0, wt, buf, ops, lane);
         __syncthreads();
+        int done_it = 0;
+        bool conv = false;
+        double last_res = __longlong_as_double(0x7ff8000000000000ll);  // NaN: never computed
         for (int t = 1; t <= bp.iters; ++t) {
-            const bool run = active && !__any_sync(0xffffffffu, bad);
+            const bool run = active && !conv && !__any_sync(0xffffffffu, bad);
             for (int k = 0; k < L; ++k) {
                 T F[M], B[M];
                 if (run) {
@@ -468,6 +480,44 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
                 if (run) bat_ops<NB, T>(bp, inst, (k + 1) % L, wt, buf, ops, lane);
                 __syncthreads();
             }
+            if (active && run) done_it = t;
+            // residual Res_t = sum_{k < l-1} ||phi_k J_k - mu_k||_1 on the end-of-sweep vectors
+            // (Algorithm 1 line 7, generalised; A6); stop at the first Res <= tol
+            if (bp.tol > 0 && (t % bp.check_every == 0 || t == bp.iters)) {
+                double res = 0.0;
+                for (int k = 0; k + 1 < L; ++k) {
+                    if (k > 0) {
+                        if (run) bat_ops<NB, T>(bp, inst, k, wt, buf, ops, lane);
+                        __syncthreads();
+                    }
+                    T F[M], B[M];
+                    if (run) bat_carries<NB, T>(ops, k, E, F, B, lane);
+                    __syncthreads();
+                    if (run) bat_walk1<NB, T>(bp, inst, k, wt, B, buf, ck, lane);
+                    __syncthreads();
+                    if (run) {
+                        int sumE = 0, Ek = 0;
+#pragma unroll
+                        for (int q = 0; q < L; ++q) {
+                            if (q != k) sumE += E[q];
+                            else Ek = E[q];
+                        }
+                        double acc = 0.0;
+                        bool b2 = false;
+                        bat_walk2<NB, T, MODE_RES, 4>(bp, inst, k, wt, F, buf, ck, sumE, Ek, acc, b2, lane);
+                        res += acc;
+                    }
+                    __syncthreads();
+                }
+                if (run) {
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) res += __shfl_xor_sync(0xffffffffu, res, o);
+                    last_res = res;
+                    if (res <= bp.tol) conv = true;
+                    else bat_ops<NB, T>(bp, inst, 0, wt, buf, ops, lane);  // the next sweep starts at k = 0
+                }
+                __syncthreads();
+            }
         }
         if (active) {
 #pragma unroll
@@ -478,6 +528,9 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
             if (lane == 0) {
                 bp.status[inst] = anybad ? 6 : 0;
                 bp.fail_iter[inst] = anybad ? fi : -1;
+                bp.iters_done[inst] = done_it;
+                bp.converged[inst] = conv ? 1 : 0;
+                bp.resid[inst] = last_res;
             }
         }
     }
@@ -656,6 +709,11 @@ static BPlan to_bplan(const BatchArgs &a) {
     bp.status = a.status;
     bp.fail_iter = a.fail_iter;
     bp.renorm = g_renorm;
+    bp.tol = a.tol;
+    bp.check_every = a.check_every > 0 ? a.check_every : 1;
+    bp.iters_done = a.iters_done;
+    bp.converged = a.converged;
+    bp.resid = a.resid;
     return bp;
 }
 

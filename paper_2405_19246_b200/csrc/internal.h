@@ -106,6 +106,10 @@ struct BatchArgs {
     double *out;                 // [batch][N] (marginal)
     double *wout;                // [batch] (cost)
     int *status, *fail_iter;     // [batch]
+    double tol;                  // residual tolerance (<= 0: run exactly iters sweeps)
+    int check_every;             // residual cadence in sweeps
+    int *iters_done, *converged; // [batch]
+    double *resid;               // [batch] last residual (NaN if never computed)
 };
 int64_t bat_slots(int l);
 // what: 0 Sinkhorn (iters sweeps), 1 marginal k -> out, 2 cost -> wout

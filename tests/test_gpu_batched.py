@@ -150,11 +150,25 @@ def test_batched_argument_errors():
     with pytest.raises(mm.MMOTError) as e:
         mm.Context(6, 100, [0.1], batch=1)
     assert e.value.name == "MMOT_EUNSUPPORTED"
-    ctx = mm.Context(3, 50, [0.1, 0.2], batch=2)
-    mu = _planes([np.full((2, 50), 1 / 50.0)] * 3)
-    u = [torch.empty((2, 50), dtype=torch.float64, device=DEV) for _ in range(3)]
+
+
+
+def test_batched_tolerance_per_instance():
+    """Each instance stops at its own first residual <= tol, checked inside the launch."""
+    l, N = 3, 200
+    etas = [0.05, 0.02]
+    B = 2
+    h = mmot_inputs.grid_h(N)
+    mus = [np.stack([mmot_inputs.c2_marginals(b, N, l)[q] for q in range(l)]) for b in range(B)]
+    ctx = mm.Context(l, N, etas, batch=B, check_every=1)
+    u = [torch.empty((B, N), dtype=torch.float64, device=DEV) for _ in range(l)]
     ctx.init_uniform(u)
-    with pytest.raises(mm.MMOTError) as e:
-        ctx.sinkhorn(mu, 5, 1e-6, u)
-    assert e.value.name == "MMOT_EUNSUPPORTED"
+    rep = ctx.sinkhorn(_planes([np.stack([mus[b][q] for b in range(B)]) for q in range(l)]), 500, 1e-8, u)
+    g = np.stack([x.cpu().numpy() for x in u])
     ctx.close()
+    t_refs = []
+    for b in range(B):
+        g_ref, t_ref, res_ref = osk.sinkhorn(mus[b], h, etas[b], 500, tol=1e-8, domain="log")
+        t_refs.append(t_ref)
+        assert np.max(np.abs(g[:, b, :] - g_ref)) <= 1e-8, b
+    assert rep["converged"] and rep["iters_done"] == max(t_refs)

@@ -109,5 +109,8 @@ def test_auto_selects_single_walk_for_c4_shape():
     assert info["kernel"] == "single_walk"
     assert info["chain_len"] * _emax(cfg.l) * h / cfg.eta <= 1.0
     small = mm.Context(4, 1000, 0.01)
-    assert small.info["kernel"] == "two_walk"
+    assert small.info["kernel"] == "persistent"      # small instances: one warp, all sweeps per launch
     small.close()
+    mid = mm.Context(4, 20000, 0.01)
+    assert mid.info["kernel"] == "two_walk"
+    mid.close()

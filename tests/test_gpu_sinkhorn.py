@@ -25,9 +25,9 @@ def _dev(vs):
     return [torch.from_numpy(np.ascontiguousarray(v)).to(DEV) for v in vs]
 
 
-def _run_gpu(mus, eta, T, tol=0.0, repr_="log", check_every=0, chunk=0):
+def _run_gpu(mus, eta, T, tol=0.0, repr_="log", check_every=0, chunk=0, kernel="auto"):
     l, N = mus.shape
-    ctx = mm.Context(l, N, eta, repr=repr_, check_every=check_every, chunk=chunk)
+    ctx = mm.Context(l, N, eta, repr=repr_, check_every=check_every, chunk=chunk, kernel=kernel)
     u = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in range(l)]
     ctx.init_uniform(u)
     rep = ctx.sinkhorn(_dev(mus), T, tol, u)
@@ -171,9 +171,25 @@ def test_overflow_reported():
     mus = np.stack([(x < 0.3).astype(float), (x > 0.7).astype(float), np.ones(N)])
     mus /= mus.sum(axis=1, keepdims=True)
     with pytest.raises(mm.MMOTError) as ei:
-        _run_gpu(mus, 1e-4, 50)
+        _run_gpu(mus, 1e-4, 50, kernel="two_walk")
     assert ei.value.name == "MMOT_EOVERFLOW"
     assert ei.value.report["fail_iter"] == 1
+
+
+@pytest.mark.parametrize("kernel", ["two_walk", "persistent"])
+def test_c2_to_tolerance_both_kernels(kernel):
+    """C2 stop iteration and solution through both kernel families (the persistent one runs the
+    residual checks inside its single launch)."""
+    cfg = mmot_inputs.CONFIGS["C2"]
+    mus = mmot_inputs.make_marginals("C2", 0)
+    h = mmot_inputs.grid_h(cfg.N)
+    rep, g, marg, W = _run_gpu(mus, cfg.eta, cfg.iters, tol=cfg.tol, kernel=kernel)
+    g_ref, t_ref, res_ref = osk.sinkhorn(mus, h, cfg.eta, cfg.iters, tol=cfg.tol, domain="log")
+    assert rep["converged"] and rep["iters_done"] == t_ref, (rep, t_ref, res_ref)
+    assert rep["residual"] == pytest.approx(res_ref, rel=1e-4)
+    m_ref = osk.marginals(np.exp(g_ref), h, cfg.eta)
+    for k in range(cfg.l):
+        assert _l1rel(marg[k], m_ref[k]) <= 1e-10
 
 
 def test_argument_errors():
