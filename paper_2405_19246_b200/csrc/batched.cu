@@ -282,7 +282,7 @@ __device__ void bat_walk1(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB
 //   MODE_COST: acc += phi_k hatJ (true scale)
 template <int NB, typename T, int MODE, int Q>
 __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB + 2], T (&F)[1 << NB], double *buf,
-                         const T *ck, int sumE_bound, int Ek, double &acc, bool &bad, int lane) {
+                         const T *ck, int sumE_bound, int Ek, double &acc, bool &bad, int lane, bool res = false) {
     constexpr int M = 1 << NB;
     constexpr int S = kBS;
     constexpr int TILE = 32 * (S + 1);
@@ -292,15 +292,17 @@ __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB 
     const double *vecs[NV];
 #pragma unroll
     for (int b = 0; b < NB; ++b) vecs[b] = bp.phit[(k + 1 + b) % (NB + 1)] + inst * N;
-    vecs[NB] = MODE == MODE_UPD ? bp.mu[k] + inst * N : bp.phit[k] + inst * N;
+    vecs[NB] = (MODE == MODE_UPD && !res) ? bp.mu[k] + inst * N : bp.phit[k] + inst * N;
     double *outv = MODE == MODE_UPD ? bp.phit[k] + inst * N : (MODE == MODE_MARG ? bp.out + inst * N : nullptr);
     const int ns = bp.P / S;
     const int64_t x0 = (int64_t)lane * bp.P;
     double f[NB > 0 ? NB : 1];
     double *obuf = buf + 2 * NV * TILE;
     int emax = -1000000;
-    const int e_true = sumE_bound + Ek;  // exponent of phi_k J_k's chain scale (MARG / COST)
-    const bool shok = Ek >= -1022 && Ek <= 1022;
+    const int e_true = sumE_bound + Ek;  // exponent of phi_k J_k's chain scale (MARG / COST / residual)
+    // residual products run through the UPD instantiation (one code copy): phi_k is read from the
+    // stage slot that holds mu_k in updates, mu_k straight from global memory
+    const bool shok = Ek >= -1022 && Ek <= 1022 && !res;
     const double shsc = MODE == MODE_UPD && shok ? pow2i(-Ek) : 1.0;  // UPD: Ek = pending shift of phi_k
     slab_issue<S, NV>(buf, vecs, 0, bp.P, N, 0, lane);
     cp_async_commit();
@@ -345,7 +347,11 @@ __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB 
                 const T J = combine<NB, T>(F, H[i]);
                 const double jv = value_of(J);
                 const double vk = cur[(NB * 32 + lane) * (S + 1) + jx];  // mu_k (UPD) or phit_k
-                if (MODE == MODE_UPD) {
+                if (MODE == MODE_UPD && res) {
+                    // |m_k - mu_k| (P:168 generalised)
+                    const int64_t x = x0 + (int64_t)s * S + jx;
+                    if (x < N) acc += fabs(scale2(vk * jv, e_true) - __ldg(bp.mu[k] + inst * N + x));
+                } else if (MODE == MODE_UPD) {
                     const double q = div_nr1(vk, jv);
                     const bool nz = nonzero(vk);
                     const int64_t x = x0 + (int64_t)s * S + jx;
@@ -355,17 +361,13 @@ __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB 
                     if (nz) emax = max(emax, ilog2d(o));
                 } else if (MODE == MODE_MARG) {
                     obuf[lane * (S + 1) + jx] = scale2(vk * jv, e_true);
-                } else if (MODE == MODE_RES) {
-                    // |m_k - mu_k| (P:168 generalised); mu_k read directly (residual sweeps only)
-                    const int64_t x = x0 + (int64_t)s * S + jx;
-                    if (x < N) acc += fabs(scale2(vk * jv, e_true) - __ldg(bp.mu[k] + inst * N + x));
                 } else if (MODE == MODE_COST) {
                     if constexpr (sizeof(T) == sizeof(Dual)) acc += scale2(vk * reinterpret_cast<const Dual &>(J).d, e_true);
                 }
             }
         }
         __syncwarp();
-        if (MODE == MODE_UPD || MODE == MODE_MARG) {
+        if ((MODE == MODE_UPD && !res) || MODE == MODE_MARG) {
             slab_store<S>(obuf, outv, 0, 32, bp.P, N, s, lane);
             __syncwarp();
         }
@@ -432,91 +434,77 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
         }
         bool bad = false;
         int fail = -1;
-        if (active) bat_ops<NB, T>(bp, inst, 0, wt, buf, ops, lane);
-        __syncthreads();
         int done_it = 0;
         bool conv = false;
         double last_res = __longlong_as_double(0x7ff8000000000000ll);  // NaN: never computed
+        if (active) bat_ops<NB, T>(bp, inst, 0, wt, buf, ops, lane);
+        __syncthreads();
+        // One sweep = l update slots and, on check sweeps, l-1 residual slots
+        // (Res_t = sum_{k<l-1} ||phi_k J_k - mu_k||_1 on the end-of-sweep vectors, Algorithm 1
+        // line 7, P:168 generalised; stop at the first Res <= tol).  Every slot runs the same
+        // code (one copy of each phase: the kernel is register- and instruction-cache-bound); the
+        // chain operators of the next slot's bound set are built at the end of each slot.
         for (int t = 1; t <= bp.iters; ++t) {
             const bool run = active && !conv && !__any_sync(0xffffffffu, bad);
-            for (int k = 0; k < L; ++k) {
+            const bool check = bp.tol > 0 && (t % bp.check_every == 0 || t == bp.iters);
+            const int nslots = check ? 2 * L - 1 : L;
+            double res = 0.0;
+            for (int sl = 0; sl < nslots; ++sl) {
+                const bool upd = sl < L;
+                const int k = upd ? sl : sl - L;
                 T F[M], B[M];
-                if (run) {
-                    bat_carries<NB, T>(ops, k, E, F, B, lane);
-                }
+                if (run) bat_carries<NB, T>(ops, k, E, F, B, lane);
                 __syncthreads();
                 if (run) bat_walk1<NB, T>(bp, inst, k, wt, B, buf, ck, lane);
                 __syncthreads();
-                int sumE = 0;
+                int sumE = 0, Ek = 0, shk = 0;
 #pragma unroll
-                for (int q = 0; q < L; ++q)
+                for (int q = 0; q < L; ++q) {
                     if (q != k) sumE += E[q];
-                // phit_k is written as (mu_k / J~) * 2^{-sh_k}, sh_k = the shift chosen at the previous
-                // update of marginal k (lazy renormalisation: the chain is rescaled only when its
-                // maximum exponent drifts beyond +-renorm)
-                int shk = 0;
-#pragma unroll
-                for (int q = 0; q < L; ++q)
-                    if (q == k) shk = Sh[q];
+                    else {
+                        Ek = E[q];
+                        shk = Sh[q];
+                    }
+                }
                 if (run) {
                     double acc = 0.0;
                     bool b2 = false;
-                    const int emax = bat_walk2<NB, T, MODE_UPD, 4>(bp, inst, k, wt, F, buf, ck, sumE, shk, acc, b2, lane);
-                    if (b2 && fail < 0) fail = t;
-                    bad |= b2;
-                    const int resc = (emax > -1000000 && (emax > bp.renorm || emax < -bp.renorm)) ? emax : 0;
-                    // (walk 2 ended with a __syncwarp after its last slab store: the vector is visible)
-                    bat_rescale(bp.phit[k] + inst * bp.N, bp.N, bp.P, resc, lane);
-                    __syncwarp();
+                    // updates: phit_k is written as (mu_k / J~) * 2^{-sh_k}, sh_k = the shift chosen at
+                    // the previous update of marginal k (lazy renormalisation: rescaled only when the
+                    // chain's maximum exponent drifts beyond +-renorm)
+                    const int emax = bat_walk2<NB, T, MODE_UPD, 4>(bp, inst, k, wt, F, buf, ck, sumE, upd ? shk : Ek,
+                                                                   acc, b2, lane, !upd);
+                    if (upd) {
+                        if (b2 && fail < 0) fail = t;
+                        bad |= b2;
+                        const int resc = (emax > -1000000 && (emax > bp.renorm || emax < -bp.renorm)) ? emax : 0;
+                        // (walk 2 ended with a __syncwarp after its last slab store: the vector is visible)
+                        bat_rescale(bp.phit[k] + inst * bp.N, bp.N, bp.P, resc, lane);
+                        __syncwarp();
 #pragma unroll
-                    for (int q = 0; q < L; ++q)
-                        if (q == k) {
-                            E[q] = -sumE + shk + resc;
-                            Sh[q] = shk + resc;
-                        }
-                }
-                __syncthreads();
-                // chain operators of the next update's bound set
-                if (run) bat_ops<NB, T>(bp, inst, (k + 1) % L, wt, buf, ops, lane);
-                __syncthreads();
-            }
-            if (active && run) done_it = t;
-            // residual Res_t = sum_{k < l-1} ||phi_k J_k - mu_k||_1 on the end-of-sweep vectors
-            // (Algorithm 1 line 7, generalised; A6); stop at the first Res <= tol
-            if (bp.tol > 0 && (t % bp.check_every == 0 || t == bp.iters)) {
-                double res = 0.0;
-                for (int k = 0; k + 1 < L; ++k) {
-                    if (k > 0) {
-                        if (run) bat_ops<NB, T>(bp, inst, k, wt, buf, ops, lane);
-                        __syncthreads();
-                    }
-                    T F[M], B[M];
-                    if (run) bat_carries<NB, T>(ops, k, E, F, B, lane);
-                    __syncthreads();
-                    if (run) bat_walk1<NB, T>(bp, inst, k, wt, B, buf, ck, lane);
-                    __syncthreads();
-                    if (run) {
-                        int sumE = 0, Ek = 0;
-#pragma unroll
-                        for (int q = 0; q < L; ++q) {
-                            if (q != k) sumE += E[q];
-                            else Ek = E[q];
-                        }
-                        double acc = 0.0;
-                        bool b2 = false;
-                        bat_walk2<NB, T, MODE_RES, 4>(bp, inst, k, wt, F, buf, ck, sumE, Ek, acc, b2, lane);
+                        for (int q = 0; q < L; ++q)
+                            if (q == k) {
+                                E[q] = -sumE + shk + resc;
+                                Sh[q] = shk + resc;
+                            }
+                    } else {
                         res += acc;
                     }
-                    __syncthreads();
                 }
-                if (run) {
+                __syncthreads();
+                // chain operators of the next slot's bound set
+                const int nk = sl + 1 < nslots ? ((sl + 1) < L ? sl + 1 : sl + 1 - L) : 0;
+                if (run) bat_ops<NB, T>(bp, inst, nk, wt, buf, ops, lane);
+                __syncthreads();
+            }
+            if (run) {
+                done_it = t;
+                if (check) {
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) res += __shfl_xor_sync(0xffffffffu, res, o);
                     last_res = res;
                     if (res <= bp.tol) conv = true;
-                    else bat_ops<NB, T>(bp, inst, 0, wt, buf, ops, lane);  // the next sweep starts at k = 0
                 }
-                __syncthreads();
             }
         }
         if (active) {

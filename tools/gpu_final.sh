@@ -1,0 +1,18 @@
+#!/bin/bash
+# Round-end evidence: GPU tests, smoke, every config's bench line, C4 launch list + ncu of the
+# update kernel, C5 ncu of the persistent kernel (reduced probe), reference arm.
+mkdir -p gpurun_out/final
+O=gpurun_out/final
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+tail -2 $O/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
+timeout 600 python bench.py > $O/bench_c4.json 2> $O/bench_c4.err; echo "c4 rc=$?"
+timeout 600 python bench.py --impl reference > $O/bench_c4_ref.json 2> $O/bench_c4_ref.err; echo "c4 ref rc=$?"
+for c in C1 C2 C3 C5; do timeout 900 python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err; echo "$c rc=$?"; done
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+timeout 300 $CMD > $O/plain.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_c4.csv $CMD > $O/ncu_launch.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sw_apply -s 20 -c 1 -o $O/prof_c4 $CMD > $O/ncu_c4.log 2>&1
+timeout 300 python tools/c5_probe.py 1184 30 > $O/c5probe.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bat_sinkhorn -c 1 -o $O/prof_c5 python tools/c5_probe.py 1184 30 > $O/ncu_c5.log 2>&1
+echo done
