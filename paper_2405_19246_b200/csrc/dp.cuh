@@ -142,40 +142,6 @@ __device__ __forceinline__ void op_identity(T (&G)[NB + 1][1 << NB]) {
         for (int S = 0; S < (1 << NB); ++S) G[c][S] = (S == 0) ? one_of(T{}) : zero_of(T{});
 }
 
-// Advance all shifted DPs G_c by one grid point (weights wt[a] = w_a, a = 0..NB+1).
-template <int NB, typename T>
-__device__ __forceinline__ void op_step(T (&G)[NB + 1][1 << NB], const T *wt, const double (&f)[NB > 0 ? NB : 1]) {
-#pragma unroll
-    for (int c = 0; c <= NB; ++c) {
-        if (c == 0) dp_diag<NB, T, true>(G[c], wt + c, NB - c);
-        else dp_diag<NB, T>(G[c], wt + c, NB - c);
-        dp_place<NB, T>(G[c], f, NB - c);
-    }
-}
-
-// Right-multiply a suffix operator by one grid point, R <- R o step_x (step_x applied first).
-// A suffix operator maps B_{x1} -> B_{x0} = step_{x0}(step_{x0+1}(... step_{x1-1}(B_{x1}))),
-// so walking the chain LEFT TO RIGHT it grows on the right.  In matrix form
-// R o step_x = R o place_x o diag: place_x = prod_q (I + phi_q E_q) acts on the column index
-// U (G_c[V] += phi_q G_{c+1}[V\q] for q in V), then diag scales column U by w_{|U|}
-// (G_c[V] *= w_c).  Same operation count as the left-multiplied prefix step, which lets one
-// forward walk build both the prefix and the suffix operator of a chain.
-template <int NB, typename T>
-__device__ __forceinline__ void op_rstep(T (&G)[NB + 1][1 << NB], const T *wt, const double (&f)[NB > 0 ? NB : 1]) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
-#pragma unroll
-        for (int c = 0; c < NB; ++c)
-#pragma unroll
-            for (int V = 0; V < (1 << NB); ++V)
-                if (((V >> b) & 1) && pc(V) <= NB - c) G[c][V] = mads(f[b], G[c + 1][V ^ (1 << b)], G[c][V]);
-#pragma unroll
-    for (int c = 1; c <= NB; ++c)  // slice 0 scales by w_0 = 1
-#pragma unroll
-        for (int V = 0; V < (1 << NB); ++V)
-            if (pc(V) <= NB - c) G[c][V] = mul(wt[c], G[c][V]);
-}
-
 // ---------------------------------------------------------------------------------------
 // One walk for both chain operators (prefix/suffix duality).
 //
@@ -186,7 +152,7 @@ __device__ __forceinline__ void op_rstep(T (&G)[NB + 1][1 << NB], const T *wt, c
 //     R_c[V] = w_c * Gt_{l-c-|V|}[V]                     (l = NB+1; Gt_l[{}] = 1)
 // (exact identity of the two sums; pinned by the GPU parity tests and DESIGN.md §1).
 // Gt is needed on the extended range c + |V| <= l, slices c = 0..NB: one walk of ~2/3 the
-// cost of op_step + op_rstep.
+// cost of walking the prefix and the suffix operators separately.
 // ---------------------------------------------------------------------------------------
 template <int NB, typename T>
 __device__ __forceinline__ void opx_identity(T (&G)[NB + 1][1 << NB]) {

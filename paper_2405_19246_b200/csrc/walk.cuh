@@ -15,11 +15,6 @@ __device__ __forceinline__ void load_weights(T (&wt)[NB + 2], const Weights &W) 
     for (int a = 0; a <= NB + 1; ++a) load_weight(wt[a], W, a);
 }
 
-template <int NB>
-__device__ __forceinline__ void load_f(double (&f)[NB > 0 ? NB : 1], const Plan &p, int64_t x) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) f[b] = __ldg(p.bound[b] + x);
-}
 
 // ---------------------------------------------------------------------------------------
 // Warp-cooperative slab staging.  A warp owns 32 consecutive chains (chunks of P points,
@@ -81,17 +76,6 @@ __device__ __forceinline__ void slab_f(double (&f)[NB > 0 ? NB : 1], const doubl
     for (int b = 0; b < NB; ++b) f[b] = buf[(b * 32 + lane) * (S + 1) + j];
 }
 
-// mu / J with a Newton-refined reciprocal: no divide slow path, no branch.
-__device__ __forceinline__ double div_nr(double mu, double j) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(j));
-    double e = fma(-j, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-j, r, 1.0);
-    r = fma(r, e, r);
-    const double q = mu * r;
-    return fma(r, fma(-j, q, mu), q);
-}
 
 // mu / J with one Newton step on the reciprocal (relative error ~2^-46) and a residual
 // correction of the quotient, which squares that error: q' - mu/J = O(2^-92) + rounding.
