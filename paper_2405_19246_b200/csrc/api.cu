@@ -234,8 +234,18 @@ void mmot_destroy(mmot_ctx *ctx) {
     delete ctx;
 }
 
+static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype dt, const mmot_opts *opts,
+                                 void *cuda_stream, mmot_ctx **out, bool allow_persistent);
+
 mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype dt, const mmot_opts *opts,
                         void *cuda_stream, mmot_ctx **out) {
+    return create_single(l, N, eta, grid, dt, opts, cuda_stream, out, true);
+}
+
+// allow_persistent = false (shards of a sharded context): the persistent batched kernel has no
+// cross-rank exchange, so a shard always gets a scan-based kernel family.
+static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype dt, const mmot_opts *opts,
+                                 void *cuda_stream, mmot_ctx **out, bool allow_persistent) {
     if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
     *out = nullptr;
     if (l < 2 || l > 8) { set_err(nullptr, "l=%d outside [2,8]", l); return MMOT_EINVAL; }
@@ -257,8 +267,12 @@ mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype
     // no per-update kernel latency)
     const int kern = opts ? opts->kernel : MMOT_KERNEL_AUTO;
     const int chunk = opts ? opts->chunk : 0;
-    if (kern == MMOT_KERNEL_PERSISTENT ||
-        (kern == MMOT_KERNEL_AUTO && chunk == 0 && l <= 5 && N <= 4096 && getenv("MMOT_NO_PERSISTENT") == nullptr)) {
+    if (kern == MMOT_KERNEL_PERSISTENT && !allow_persistent) {
+        set_err(nullptr, "sharded contexts cannot use the persistent kernel");
+        return MMOT_EUNSUPPORTED;
+    }
+    if (kern == MMOT_KERNEL_PERSISTENT || (allow_persistent && kern == MMOT_KERNEL_AUTO && chunk == 0 && l <= 5 &&
+                                           N <= 4096 && getenv("MMOT_NO_PERSISTENT") == nullptr)) {
         if (l > 5) { set_err(nullptr, "the persistent kernel supports l <= 5"); return MMOT_EUNSUPPORTED; }
         return mmot_create_batched(l, N, 1, &eta, grid, dt, opts, cuda_stream, out);
     }
@@ -1019,7 +1033,7 @@ mmot_status mmot_create_sharded(int l, int64_t N_global, double eta, mmot_grid g
     mmot_grid g2{grid.x_min + lo * h, grid.x_min + (hi - 1) * h};
     if (hi - lo == 1) g2.x_max = g2.x_min + h;  // a 1-point shard keeps the global h below
     mmot_ctx *c = nullptr;
-    mmot_status st = mmot_create(l, hi - lo, eta, g2, dt, opts, cuda_stream, &c);
+    mmot_status st = create_single(l, hi - lo, eta, g2, dt, opts, cuda_stream, &c, false);
     if (st) return st;
     c->h = h;
     for (int a = 0; a <= mmot::kMaxL; ++a) {
@@ -1055,6 +1069,25 @@ mmot_status mmot_create_sharded(int l, int64_t N_global, double eta, mmot_grid g
         c->comm = nullptr;
         mmot_destroy(c);
         return MMOT_ENCCL;
+    }
+    // Every rank must run the same collective sequence with the same payloads: the kernel family
+    // and the scan mode, chosen from the local shard size, have to agree across ranks.
+    {
+        const double sig = (double)((c->sw ? 4 : 0) + (c->rx ? 2 : 0) + (c->nlev >= 2 ? 1 : 0));
+        std::vector<double> all((size_t)world);
+        double *d = c->shard_mem;
+        bool ok = cudaMemcpyAsync(d, &sig, sizeof sig, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
+                  g_nccl.AllGather(d, d + 1, 1, kNcclFloat64, c->comm, c->stream) == 0 &&
+                  cudaMemcpyAsync(all.data(), d + 1, (size_t)world * sizeof(double), cudaMemcpyDeviceToHost,
+                                  c->stream) == cudaSuccess &&
+                  cudaStreamSynchronize(c->stream) == cudaSuccess;
+        for (int r2 = 0; ok && r2 < world; ++r2) ok = all[r2] == sig;
+        if (!ok) {
+            set_err(c, "sharded context: ranks chose different kernel configurations (shard sizes too uneven)");
+            snprintf(g_err, sizeof g_err, "%s", c->err);
+            mmot_destroy(c);
+            return MMOT_ESHAPE;
+        }
     }
     *out = c;
     return MMOT_OK;

@@ -56,3 +56,25 @@ def test_sharded_world1_sinkhorn_lockstep():
     g_ref, _, res_ref = osk.sinkhorn(mus, h, eta, T, tol=1e-300, domain="log")
     assert np.max(np.abs(g - g_ref)) <= 1e-9
     assert rep["residual"] == pytest.approx(res_ref, rel=1e-8)
+
+
+def test_sharded_small_shard_uses_scan_kernel():
+    """A shard small enough for the persistent kernel still gets a scan-based family (the
+    persistent kernel has no cross-rank exchange); an explicit persistent request is refused."""
+    l, N, eta, T = 4, 1000, 0.05, 3
+    h = mmot_inputs.grid_h(N)
+    mus = np.stack(mmot_inputs.random_marginals(78, l, N))
+    uid = mm.nccl_unique_id()
+    ctx = mm.Context(l, N, eta, repr="log", shard=(0, 1, uid))
+    assert ctx.info["kernel"] in ("two_walk", "single_walk")
+    u = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in range(l)]
+    ctx.init_uniform(u)
+    rep = ctx.sinkhorn(_dev(mus), T, 0.0, u)
+    assert rep["status"] == 0
+    g = np.stack([x.cpu().numpy() for x in u])
+    ctx.close()
+    g_ref, _, _ = osk.sinkhorn(mus, h, eta, T, domain="log")
+    assert np.max(np.abs(g - g_ref)) <= 1e-9
+    with pytest.raises(mm.MMOTError) as e:
+        mm.Context(l, N, eta, shard=(0, 1, mm.nccl_unique_id()), kernel="persistent")
+    assert e.value.name == "MMOT_EUNSUPPORTED"
