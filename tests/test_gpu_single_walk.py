@@ -114,3 +114,36 @@ def test_auto_selects_single_walk_for_c4_shape():
     mid = mm.Context(4, 20000, 0.01)
     assert mid.info["kernel"] == "two_walk"
     mid.close()
+
+
+@pytest.mark.slow
+def test_c4_full_size_sweeps_match_two_walk_and_fix_last_marginal():
+    """C4 at its full size (l=4, N=1e8, eta=1e-4) through mmot_sinkhorn in the bench's launch
+    configuration (single-walk, restricted next-update scan), 2 sweeps, checked (a) against the
+    two-walk family, an independent kernel path, on every element, and (b) by the property that
+    holds at any size: the sweep's last update makes marginal l-1 exact, m_{l-1} = mu_{l-1}
+    (P:1029-1035), with m_{l-1} from the product path verified by test_marginal_parity_c4_full_size."""
+    cfg = mmot_inputs.CONFIGS["C4"]
+    l, N, eta, T = cfg.l, cfg.N, cfg.eta, 2
+    mus = mmot_inputs.make_marginals("C4", 0)
+    mu_d = _dev(mus)
+    del mus
+    g = {}
+    for fam in ("auto", "two_walk"):
+        ctx = mm.Context(l, N, eta, repr="log", kernel=fam)
+        if fam == "auto":
+            assert ctx.info["kernel"] == "single_walk"
+        u = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in range(l)]
+        ctx.init_uniform(u)
+        rep = ctx.sinkhorn(mu_d, T, 0.0, u)
+        assert rep["status"] == 0 and rep["iters_done"] == T
+        if fam == "auto":
+            m_last = ctx.marginal(l - 1, u)
+            rel = float((m_last - mu_d[l - 1]).abs().sum() / mu_d[l - 1].abs().sum())
+            assert rel <= RTOL, rel
+            del m_last
+        g[fam] = u
+        ctx.close()
+    for k in range(l):
+        d = float((g["auto"][k] - g["two_walk"][k]).abs().max())
+        assert d <= 1e-9, (k, d)
