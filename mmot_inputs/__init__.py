@@ -24,7 +24,7 @@ __all__ = [
     "Config", "CONFIGS", "config", "grid_h", "gaussian_bump", "mixture",
     "c1_marginals", "c2_marginals", "c3_marginals", "c4_marginals",
     "c5_marginals", "c5_etas", "c5_batch_marginals", "random_marginals", "random_positive",
-    "make_marginals",
+    "make_marginals", "ricker_marginals",
 ]
 
 
@@ -197,3 +197,19 @@ def make_marginals(name: str, instance: int = 0, N: Optional[int] = None) -> np.
     if name == "C5":
         return c5_marginals(instance, n, cfg.l)
     raise KeyError(name)
+
+
+def ricker_marginals(N: int = 100, taus=(0.0, 0.75, 1.5), delta: float = 1e-3, x_min: float = -2.0,
+                     x_max: float = 2.0, A: float = 1.0, F0: float = 1.0) -> np.ndarray:
+    """The paper's Ricker-wavelet marginals (§5.2), one per shift tau_j:
+    R(t) = A (1 - 2 pi^2 F0^2 t^2) exp(-pi^2 F0^2 t^2), f_j(t) = R(t - tau_j) on N uniform points of
+    [x_min, x_max], mu_j = (f_j^2 / ||f_j^2||_1 + delta) / (1 + L delta).  Deterministic (no draws).
+    Reading: ||.||_1 is the discrete sum and L = N, so every mu_j sums to one."""
+    t = np.linspace(x_min, x_max, N)
+    out = []
+    for tau in taus:
+        a = (math.pi * F0 * (t - tau)) ** 2
+        f = A * (1.0 - 2.0 * a) * np.exp(-a)
+        p = f * f / np.sum(f * f)
+        out.append((p + delta) / (1.0 + N * delta))
+    return np.stack(out)
