@@ -278,6 +278,57 @@ __global__ void __launch_bounds__(64) k_ops_down_c(const T *ops_f, const T *ops_
     }
 }
 
+// Warp-per-group down-sweep for NB >= 4 (fp64): the M <= 32 states of an application map onto the
+// lanes of one warp, so the group's GS sequential applications need only warp barriers; two
+// groups per 64-thread block (blockIdx.y = direction as in k_ops_down_c).
+template <int NB>
+__global__ void __launch_bounds__(64) k_ops_down_cw(const double *ops_f, const double *ops_b, const double *gcar_f,
+                                                     const double *gcar_b, double *car_f, double *car_b, int64_t n_in,
+                                                     const int *stop, double *car_bi) {
+    constexpr int M = 1 << NB;
+    constexpr int SZ = OpShape<NB>::SZ;
+    constexpr int GS = group_of(NB);
+    __shared__ double G[2][GS][SZ];
+    __shared__ double cur[2][M];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t g = (int64_t)blockIdx.x * 2 + w;
+    const int dir = blockIdx.y;
+    const int64_t first = g * GS;
+    if (first >= n_in || *stop) return;
+    const int cnt = (int)min((int64_t)GS, n_in - first);
+    const double *ops = (dir == 0 ? ops_f : ops_b) + first * SZ;
+    for (int e = lane; e < cnt * SZ; e += 32) G[w][e / SZ][e % SZ] = opx_valid<NB>(e % SZ) ? ops[e] : 0.0;
+    const double *gc = dir == 0 ? gcar_f : gcar_b;
+    if (lane < M) cur[w][lane] = gc ? gc[g * M + lane] : (lane == 0 ? 1.0 : 0.0);
+    __syncwarp();
+    double *car = dir == 0 ? car_f : car_b;
+    for (int t = 0; t < cnt; ++t) {
+        const int i = dir == 0 ? t : cnt - 1 - t;
+        double nx = 0.0;
+        if (lane < M) {
+            car[(first + i) * M + lane] = cur[w][lane];
+            // Op(cur)[S] = sum_{U subset S} cur[U] G_|U|[S\U]
+            const int nt = 1 << pc(lane);
+            double a0 = 0.0, a1 = 0.0;
+            int U = lane;
+#pragma unroll 4
+            for (int k = 0; k < nt; ++k) {
+                const double x = cur[w][U], y = G[w][i][pc(U) * M + (lane ^ U)];
+                if (k & 1) a1 = fma(x, y, a1);
+                else a0 = fma(x, y, a0);
+                U = (U - 1) & lane;
+            }
+            nx = a0 + a1;
+        }
+        __syncwarp();
+        if (lane < M) {
+            cur[w][lane] = nx;
+            if (dir == 1 && car_bi) car_bi[(first + i) * M + lane] = nx;  // inclusive (chain start)
+        }
+        __syncwarp();
+    }
+}
+
 // Warp-cooperative variants of phase 2 (fp64, NB <= 3): one warp per group of 32 operators;
 // the group is staged through shared memory (coalesced), then composed with a shuffle tree
 // (reduce) or a Kogge-Stone scan (down).  blockIdx.y selects the direction.
@@ -1581,6 +1632,15 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
                                                     static_cast<double *>(p.car_f[i]), static_cast<double *>(p.car_b[i]),
                                                     p.nlev_n[i], p.stop,
                                                     i == 0 && p.sw ? static_cast<double *>(p.car_bi) : nullptr);
+            ++*launches;
+            continue;
+        }
+        if constexpr (NB >= 4 && sizeof(T) == sizeof(double)) {
+            k_ops_down_cw<NB><<<dim3((unsigned)((ng + 1) / 2), 2), 64, 0, s>>>(
+                reinterpret_cast<const double *>(p.ops_f[i]), reinterpret_cast<const double *>(p.ops_b[i]),
+                reinterpret_cast<const double *>(gf), reinterpret_cast<const double *>(gb),
+                reinterpret_cast<double *>(p.car_f[i]), reinterpret_cast<double *>(p.car_b[i]), p.nlev_n[i], p.stop,
+                i == 0 && p.sw ? reinterpret_cast<double *>(p.car_bi) : nullptr);
             ++*launches;
             continue;
         }
