@@ -166,6 +166,111 @@ __device__ __forceinline__ bool opx_valid(int e) {  // entry e = c*M + V is a us
     return pc(e % M) <= NB - e / M;
 }
 
+// Term table of one composition C_c[V] = sum_{U subset V} X_c[U] Y_{c+|U|}[V\U] (NB >= 4): for
+// output entry q = c*M + V the terms start[q] .. start[q+1]-1, each a packed pair of offsets
+// (X offset | Y offset << 16) -- generated at compile time, staged in shared memory, so the
+// reduce kernel spends two loads and one FMA per term instead of the subset-enumeration
+// arithmetic.
+template <int NB>
+struct ComposeTab {
+    static constexpr int M = 1 << NB;
+    static constexpr int SZ = (NB + 1) * M;
+    static constexpr int count_terms() {
+        int n = 0;
+        for (int q = 0; q < SZ; ++q) {
+            const int c = q / M, V = q % M;
+            if (pc(V) <= NB - c) n += 1 << pc(V);
+        }
+        return n;
+    }
+    static constexpr int NT = count_terms();
+    unsigned pair[NT];
+    unsigned short start[SZ + 1];
+    constexpr ComposeTab() : pair(), start() {
+        int n = 0;
+        for (int q = 0; q < SZ; ++q) {
+            start[q] = (unsigned short)n;
+            const int c = q / M, V = q % M;
+            if (pc(V) > NB - c) continue;
+            int U = V;
+            for (int t = 0; t < (1 << pc(V)); ++t) {
+                pair[n++] = (unsigned)(c * M + U) | ((unsigned)((c + pc(U)) * M + (V ^ U)) << 16);
+                U = (U - 1) & V;
+            }
+        }
+        start[SZ] = (unsigned short)n;
+    }
+};
+template <int NB>
+__device__ const ComposeTab<NB> g_ctab = ComposeTab<NB>();
+
+// fp64 reduce for NB >= 4 through the term table (layout and semantics as k_ops_reduce_c).
+template <int NB>
+__global__ void __launch_bounds__(128) k_ops_reduce_t(const double *in_f, const double *in_b, double *out_f,
+                                                     double *out_b, int64_t n_in, const int *stop) {
+    constexpr int M = 1 << NB;
+    constexpr int SZ = OpShape<NB>::SZ;
+    constexpr int GS = group_of(NB);
+    constexpr int NT = ComposeTab<NB>::NT;
+    __shared__ double A[GS][SZ];
+    __shared__ unsigned tp[NT];
+    __shared__ unsigned short ts[SZ + 1];
+    const int64_t g = blockIdx.x;
+    const int dir = blockIdx.y;
+    const int64_t first = g * GS;
+    if (first >= n_in || *stop) return;
+    for (int t = threadIdx.x; t < NT; t += blockDim.x) tp[t] = g_ctab<NB>.pair[t];
+    for (int t = threadIdx.x; t <= SZ; t += blockDim.x) ts[t] = g_ctab<NB>.start[t];
+    const int cnt = (int)min((int64_t)GS, n_in - first);
+    const double *in = (dir == 0 ? in_f : in_b) + first * SZ;
+    for (int e = threadIdx.x; e < GS * SZ; e += blockDim.x) {
+        const int i = e / SZ, q = e % SZ;
+        A[i][q] = i < cnt && opx_valid<NB>(q) ? in[e] : ((q % M) == 0 && i >= cnt ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    constexpr int IT = (GS / 2 * SZ + 127) / 128;
+#pragma unroll
+    for (int step = 1; step < GS; step <<= 1) {
+        const int lim = (GS / (2 * step)) * SZ;
+        double res[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int e = threadIdx.x + it * 128;
+            res[it] = 0.0;
+            if (e < lim) {
+                const int pr = e / SZ, q = e % SZ;
+                const int i = pr * 2 * step;
+                const double *X = dir == 0 ? A[i] : A[i + step];  // applied first
+                const double *Y = dir == 0 ? A[i + step] : A[i];  // applied second
+                double a0 = 0.0, a1 = 0.0;
+                const int t0 = ts[q], t1 = ts[q + 1];
+                int t = t0;
+#pragma unroll 2
+                for (; t + 1 < t1; t += 2) {
+                    const unsigned p0 = tp[t], p1 = tp[t + 1];
+                    a0 = fma(X[p0 & 0xffffu], Y[p0 >> 16], a0);
+                    a1 = fma(X[p1 & 0xffffu], Y[p1 >> 16], a1);
+                }
+                if (t < t1) {
+                    const unsigned p0 = tp[t];
+                    a0 = fma(X[p0 & 0xffffu], Y[p0 >> 16], a0);
+                }
+                res[it] = a0 + a1;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int e = threadIdx.x + it * 128;
+            if (e < lim) A[(e / SZ) * 2 * step][e % SZ] = res[it];
+        }
+        __syncthreads();
+    }
+    double *out = (dir == 0 ? out_f : out_b) + g * SZ;
+    for (int q = threadIdx.x; q < SZ; q += blockDim.x)
+        if (opx_valid<NB>(q)) out[q] = A[0][q];
+}
+
 template <int NB, typename T>
 __global__ void __launch_bounds__(128) k_ops_reduce_c(const T *in_f, const T *in_b, T *out_f, T *out_b, int64_t n_in,
                                                        const int *stop) {
@@ -1571,6 +1676,14 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
                                                      static_cast<const double *>(p.ops_b[i]),
                                                      static_cast<double *>(p.ops_f[i + 1]),
                                                      static_cast<double *>(p.ops_b[i + 1]), p.nlev_n[i], p.stop);
+            ++*launches;
+            continue;
+        }
+        if constexpr (NB >= 4 && sizeof(T) == sizeof(double)) {
+            k_ops_reduce_t<NB><<<dim3((unsigned)ng, 2), 128, 0, s>>>(
+                reinterpret_cast<const double *>(p.ops_f[i]), reinterpret_cast<const double *>(p.ops_b[i]),
+                reinterpret_cast<double *>(p.ops_f[i + 1]), reinterpret_cast<double *>(p.ops_b[i + 1]), p.nlev_n[i],
+                p.stop);
             ++*launches;
             continue;
         }
