@@ -578,7 +578,9 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
     if (st) return st;
     const int64_t n = c->batch * c->N;
     for (int q = 0; q < c->l; ++q) {
-        CK(c, mmot::launch_check(mu[q], n, 0, &c->dsc->flags[q], &c->dsc->mass[q], c->stream, &c->launches));
+        // element checks over the whole batch; zero mass per instance (the smallest instance mass)
+        CK(c, mmot::launch_check(mu[q], n, 0, &c->dsc->flags[q], nullptr, c->stream, &c->launches));
+        CK(c, mmot::launch_bat_min_mass(mu[q], c->batch, c->N, &c->dsc->mass[q], c->stream, &c->launches));
         CK(c, mmot::launch_check(static_cast<const double *>(u[q]), n, c->opts.repr == MMOT_LOG ? 1 : 0,
                                  &c->dsc->flags[c->l + q], nullptr, c->stream, &c->launches));
     }

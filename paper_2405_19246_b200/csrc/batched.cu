@@ -646,6 +646,28 @@ __global__ void k_bat_export(BPlan bp, double *const *u, int is_log) {
     }
 }
 
+// Smallest per-instance mass of one marginal plane [batch][N] (EZEROMASS per instance):
+// one warp per instance, atomicMin on the bit pattern (order-preserving for non-negative
+// doubles; negative sums are reported as ENEGMASS by the element check first).
+__global__ void k_bat_min_mass(const double *mu, int64_t batch, int64_t N, double *mass) {
+    const int lane = threadIdx.x & 31;
+    const int64_t inst = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (inst >= batch) return;
+    double sum = 0.0;
+    for (int64_t x = lane; x < N; x += 32) sum += mu[inst * N + x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) atomicMin(reinterpret_cast<unsigned long long *>(mass), (unsigned long long)__double_as_longlong(fmax(sum, 0.0)));
+}
+
+cudaError_t launch_bat_min_mass(const double *mu, int64_t batch, int64_t N, double *mass, cudaStream_t s,
+                                int64_t *launches) {
+    cudaMemsetAsync(mass, 0x7f, sizeof(double), s);  // 1.4e306: larger than any mass
+    k_bat_min_mass<<<(unsigned)((batch + 3) / 4), 128, 0, s>>>(mu, batch, N, mass);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------------------
 template <int NB>
 static size_t bat_smem() {

@@ -112,6 +112,9 @@ struct BatchArgs {
     double *resid;               // [batch] last residual (NaN if never computed)
 };
 int64_t bat_slots(int l);
+// mass <- min over instances of sum_x mu[inst][x] (per-instance zero-mass check)
+cudaError_t launch_bat_min_mass(const double *mu, int64_t batch, int64_t N, double *mass, cudaStream_t s,
+                                int64_t *launches);
 // what: 0 Sinkhorn (iters sweeps), 1 marginal k -> out, 2 cost -> wout
 cudaError_t launch_batched(const BatchArgs &a, int what, cudaStream_t s, int64_t *launches);
 // u: DEVICE array of l device pointers; import: u -> (phit, E), else (phit, E) -> u

@@ -172,3 +172,24 @@ def test_batched_tolerance_per_instance():
         t_refs.append(t_ref)
         assert np.max(np.abs(g[:, b, :] - g_ref)) <= 1e-8, b
     assert rep["converged"] and rep["iters_done"] == max(t_refs)
+
+
+@pytest.mark.parametrize("bad,code", [("nan", "MMOT_ENONFINITE"), ("neg", "MMOT_ENEGMASS"), ("zero", "MMOT_EZEROMASS")])
+def test_batched_data_errors_per_instance(bad, code):
+    """Input errors in ONE instance of a batch are reported: a zero-mass marginal of a single
+    instance is EZEROMASS even though the batch as a whole has mass."""
+    l, N, B = 4, 300, 5
+    mus = np.stack([mmot_inputs.c2_marginals(b, N, l) for b in range(B)])  # [B][l][N]
+    if bad == "nan":
+        mus[3, 1, 17] = np.nan
+    elif bad == "neg":
+        mus[1, 2, 40] = -1e-6
+    else:
+        mus[2, 0, :] = 0.0
+    ctx = mm.Context(l, N, [0.05] * B, batch=B)
+    u = [torch.empty((B, N), dtype=torch.float64, device=DEV) for _ in range(l)]
+    ctx.init_uniform(u)
+    with pytest.raises(mm.MMOTError) as ei:
+        ctx.sinkhorn(_planes([mus[:, q, :] for q in range(l)]), 3, 0.0, u)
+    ctx.close()
+    assert ei.value.name == code
