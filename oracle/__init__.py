@@ -25,6 +25,8 @@ Everything is plain fp64 and follows the paper (``P:n`` = line n of PAPER.md):
                  residual (Algorithm 1 line 7 generalised), cost W.
 * ``comonotone`` -- closed-form unregularised optimum W_0 of the 1-D pairwise
                  L1 MMOT (sanity pin: W_eta >= W_0).
+* ``points``  -- non-uniform 1-D grids (footnote P:182): one decay per grid edge;
+                 brute force and the subset recursion with per-edge weights, Sinkhorn driver.
 
 Every function and the tests that pin it are listed in DESIGN.md §2b; none is "parity unpinned".
 """
