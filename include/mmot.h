@@ -128,6 +128,21 @@ MMOT_API mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, m
 MMOT_API mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *eta_host, mmot_grid grid,
                                          mmot_dtype dt, const mmot_opts *opts, void *cuda_stream, mmot_ctx **out);
 
+/* Non-uniform 1-D grids (the paper's footnote to the uniform-grid assumption, PAPER.md:182;
+ * SURVEY §8(f) NEXT-3).  x_host[N]: the grid points, finite and strictly increasing (copied).
+ * The L1 cost is c(i) = sum_{p<q} |x[i_p] - x[i_q]|; every grid edge e (between points e-1 and e)
+ * gets its own decay lambda_e = exp(-(x[e] - x[e-1]) / eta).  The contexts run on the persistent
+ * (batched) kernel family: opts->kernel must be MMOT_KERNEL_AUTO or MMOT_KERNEL_PERSISTENT
+ * (else EUNSUPPORTED); l in [2, 5]; all other arguments, layouts and the compute calls are those
+ * of mmot_create / mmot_create_batched (mmot_cost returns W = sum_i c(i) t(i) in x's units).
+ * Errors: EINVAL for a NULL / non-finite / non-increasing x_host, plus those of the uniform
+ * constructors. */
+MMOT_API mmot_status mmot_create_points(int l, int64_t N, double eta, const double *x_host, mmot_dtype dt,
+                                        const mmot_opts *opts, void *cuda_stream, mmot_ctx **out);
+MMOT_API mmot_status mmot_create_batched_points(int l, int64_t N, int64_t batch, const double *eta_host,
+                                                const double *x_host, mmot_dtype dt, const mmot_opts *opts,
+                                                void *cuda_stream, mmot_ctx **out);
+
 /* Create rank `rank`'s part of ONE instance sharded over `world` GPUs by contiguous grid
  * chunks (BASELINE C4 on 1/2/4/8 GPUs).  The rank owns global points
  * [lo, hi) = mmot_shard_range(N_global, rank, world) of every vector; all array arguments of

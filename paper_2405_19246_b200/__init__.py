@@ -71,6 +71,13 @@ def load_library():
     lib.mmot_create_batched.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
                                         _Grid, ctypes.c_int, ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
     lib.mmot_create_batched.restype = ctypes.c_int
+    lib.mmot_create_points.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
+                                       ctypes.c_int, ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
+    lib.mmot_create_points.restype = ctypes.c_int
+    lib.mmot_create_batched_points.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
+                                               ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.POINTER(_Opts), vp,
+                                               ctypes.POINTER(vp)]
+    lib.mmot_create_batched_points.restype = ctypes.c_int
     lib.mmot_create_sharded.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_double, _Grid, ctypes.c_int, vp,
                                         ctypes.c_int, ctypes.c_int, ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
     lib.mmot_create_sharded.restype = ctypes.c_int
@@ -189,9 +196,10 @@ class Context:
 
     def __init__(self, l: int, N: int, eta, grid=(0.0, 1.0), dtype: str = "f64",
                  repr: str = "log", check_every: int = 0, chunk: int = 0, stream=None,
-                 kernel: str = "auto", batch: Optional[int] = None, shard=None):
+                 kernel: str = "auto", batch: Optional[int] = None, shard=None, points=None):
         """Single instance (eta: float), or a batched context (batch=B, eta: B per-instance
-        values) whose array arguments are [B][N] planes (mmot_create_batched)."""
+        values) whose array arguments are [B][N] planes (mmot_create_batched).  points: N strictly
+        increasing grid coordinates for a non-uniform grid (mmot_create_points / _batched_points)."""
         import torch
         self._lib = load_library()
         if not torch.cuda.is_available():
@@ -217,6 +225,22 @@ class Context:
                                                F64 if dtype == "f64" else F32, idb, int(rank), int(world),
                                                ctypes.byref(opts), ctypes.c_void_p(self.stream.cuda_stream),
                                                ctypes.byref(ctx))
+        elif points is not None:
+            xs = [float(v) for v in points]
+            if len(xs) != self.N:
+                raise MMOTError(2, f"expected {self.N} grid points, got {len(xs)}")
+            self.grid = (xs[0], xs[-1])
+            self.h = None
+            xa = (ctypes.c_double * self.N)(*xs)
+            if self.batch is None:
+                st = self._lib.mmot_create_points(self.l, self.N, self.eta, xa, F64 if dtype == "f64" else F32,
+                                                  ctypes.byref(opts), ctypes.c_void_p(self.stream.cuda_stream),
+                                                  ctypes.byref(ctx))
+            else:
+                etas = (ctypes.c_double * self.batch)(*self.eta)
+                st = self._lib.mmot_create_batched_points(self.l, self.N, self.batch, etas, xa,
+                                                          F64 if dtype == "f64" else F32, ctypes.byref(opts),
+                                                          ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx))
         elif self.batch is None:
             st = self._lib.mmot_create(self.l, self.N, self.eta, _Grid(*self.grid), F64 if dtype == "f64" else F32,
                                        ctypes.byref(opts), ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(ctx))

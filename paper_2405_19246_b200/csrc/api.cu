@@ -117,6 +117,7 @@ struct mmot_ctx {
     int64_t batch = 1;
     mmot::BatchArgs ba{};
     double *bat_mem = nullptr;              // eta, phit, scratch, wout (one allocation)
+    double *pts_mem = nullptr;              // non-uniform grids: hx [ne], lambda [batch][ne]
     int *bat_int = nullptr;                 // E, status, fail_iter
     void **bat_ptrs = nullptr;              // device array of l pointers (u[] for import/export)
     double *bat_whost = nullptr;            // pinned [batch]
@@ -212,6 +213,7 @@ void mmot_destroy(mmot_ctx *ctx) {
     cudaFree(ctx->ws);
     cudaFree(ctx->out_t);
     cudaFree(ctx->bat_mem);
+    cudaFree(ctx->pts_mem);
     cudaFree(ctx->rx_mem);
     cudaFree(ctx->shard_mem);
     if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
@@ -548,6 +550,58 @@ mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *e
     }
     *out = c;
     return MMOT_OK;
+}
+
+// Non-uniform grid points (paper footnote P:182): batched context as above whose edge e (between
+// points e-1 and e) has its own length h_e = x[e] - x[e-1] and decay lambda_e = exp(-h_e / eta).
+mmot_status mmot_create_batched_points(int l, int64_t N, int64_t batch, const double *eta_host, const double *x_host,
+                                       mmot_dtype dt, const mmot_opts *opts, void *cuda_stream, mmot_ctx **out) {
+    if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
+    *out = nullptr;
+    if (!x_host || N < 1) { set_err(nullptr, "x_host must hold N >= 1 grid points"); return MMOT_EINVAL; }
+    for (int64_t i = 0; i < N; ++i)
+        if (!isfinite(x_host[i]) || (i > 0 && !(x_host[i] > x_host[i - 1]))) {
+            set_err(nullptr, "grid points must be finite and strictly increasing (index %lld)", (long long)i);
+            return MMOT_EINVAL;
+        }
+    if (opts && opts->kernel != MMOT_KERNEL_AUTO && opts->kernel != MMOT_KERNEL_PERSISTENT) {
+        set_err(nullptr, "non-uniform grids run on the persistent (batched) kernel family only");
+        return MMOT_EUNSUPPORTED;
+    }
+    mmot_grid g{x_host[0], N > 1 ? x_host[N - 1] : x_host[0] + 1.0};
+    mmot_ctx *c = nullptr;
+    mmot_status st = mmot_create_batched(l, N, batch, eta_host, g, dt, opts, cuda_stream, &c);
+    if (st) return st;
+    mmot::BatchArgs &a = c->ba;
+    const int64_t ne = 32 * (int64_t)a.P + 1;
+    std::vector<double> hx((size_t)ne, 0.0);
+    for (int64_t e = 1; e < N; ++e) hx[(size_t)e] = x_host[e] - x_host[e - 1];
+    if (cudaMalloc(&c->pts_mem, (size_t)(1 + batch) * ne * sizeof(double)) != cudaSuccess) {
+        set_err(c, "grid workspace allocation failed");
+        snprintf(g_err, sizeof g_err, "%s", c->err);
+        mmot_destroy(c);
+        return MMOT_ENOMEM;
+    }
+    double *dhx = c->pts_mem, *dlam = c->pts_mem + ne;
+    if (cudaMemcpyAsync(dhx, hx.data(), (size_t)ne * sizeof(double), cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+        mmot::launch_bat_lambda(dlam, dhx, a.eta, batch, ne, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess) {
+        set_err(c, "grid workspace init failed");
+        snprintf(g_err, sizeof g_err, "%s", c->err);
+        mmot_destroy(c);
+        return MMOT_ECUDA;
+    }
+    a.hx = dhx;
+    a.lam = dlam;
+    a.ne = ne;
+    *out = c;
+    return MMOT_OK;
+}
+
+mmot_status mmot_create_points(int l, int64_t N, double eta, const double *x_host, mmot_dtype dt, const mmot_opts *opts,
+                               void *cuda_stream, mmot_ctx **out) {
+    if (!(eta > 0) || !isfinite(eta)) { set_err(nullptr, "eta must be finite and > 0"); return MMOT_EINVAL; }
+    return mmot_create_batched_points(l, N, 1, &eta, x_host, dt, opts, cuda_stream, out);
 }
 
 }  // extern "C"

@@ -97,6 +97,10 @@ struct BPlan {
     const double *mu[kMaxL];        // [batch][N]
     double *ops;                    // scratch [slot][2][SZ][32]
     double *ckpt;                   // scratch [slot][P/kBS][M][32] (x2 for duals)
+    const double *lam;              // non-uniform grids: [batch][ne] lambda_e = exp(-h_e / eta) (else null)
+    const double *hx;               // non-uniform grids: [ne] edge lengths h_e (edge e between points e-1, e)
+    int64_t ne;                     // 32 P + 1 (edges 0 .. 32 P; 1 / 0 outside 1 .. N-1)
+    double hc;                      // cost factor: h (uniform: hatJ counts edges) or 1 (edge lengths in the tangent)
     int64_t slots;                  // resident warps (scratch slots)
     int iters;
     int k;                          // product mode: free marginal
@@ -112,10 +116,53 @@ struct BPlan {
     double *resid;                  // [batch]
 };
 
+// Non-uniform grids (paper footnote P:182): weights of edge e, w_a = lambda_e^{a(l-a)}, and for
+// duals the cost tangent a(l-a) h_e w_a (the edge's contribution to c(i) = sum_e h_e n(l-n)).
+template <int NB, typename T>
+__device__ __forceinline__ void pweights(T (&w)[NB + 2], const BPlan &bp, int64_t inst, int64_t e) {
+    constexpr int L = NB + 1;
+    const double lam = __ldg(bp.lam + inst * bp.ne + e);
+    double pw[L * L / 4 + 1];  // lambda^0 .. lambda^{max a(l-a)}
+    pw[0] = 1.0;
+#pragma unroll
+    for (int i = 1; i <= L * L / 4; ++i) pw[i] = pw[i - 1] * lam;
+    double he = 0.0;
+    if constexpr (sizeof(T) != sizeof(double)) he = __ldg(bp.hx + e);
+#pragma unroll
+    for (int a = 0; a <= NB + 1; ++a) {
+        const int ea = a <= L ? a * (L - a) : 0;
+        const double wa = a <= L ? pw[ea] : 0.0;
+        if constexpr (sizeof(T) == sizeof(double)) {
+            reinterpret_cast<double &>(w[a]) = wa;
+        } else {
+            reinterpret_cast<Dual &>(w[a]) = Dual{wa, (double)ea * he * wa};
+        }
+    }
+}
+
+// Chain operators under per-edge weights: prefix operator w_c(entry edge) Gt_c, suffix operator
+// w_c(exit edge) Gt_{l-c-|V|} (the duality of opx_store with the two boundary edges made explicit:
+// the chain's internal edges carry the same exponents in both, DESIGN.md §2 A20).
+template <int NB, typename T>
+__device__ __forceinline__ void opx_store_pts(const T (&G)[NB + 1][1 << NB], const T *win, const T *wout, T *pf, T *pb) {
+    constexpr int M = 1 << NB;
+#pragma unroll
+    for (int c = 0; c <= NB; ++c)
+#pragma unroll
+        for (int V = 0; V < M; ++V)
+            if (c + pc(V) <= NB) {
+                const int cp = NB + 1 - c - pc(V);
+                pf[c * M + V] = c == 0 ? G[0][V] : mul(win[c], G[c][V]);
+                const T r = cp > NB ? one_of(T{}) : G[cp][V];
+                pb[c * M + V] = c == 0 ? r : mul(wout[c], r);
+            }
+}
+
+
 // ---------------------------------------------------------------------------------------
 // Chain operator walk (extended operator, dp.cuh opx_*) of the bound set (k+1..k+NB mod l);
 // stores prefix op (dir 0) and suffix op (dir 1) of every lane into its slot's scratch.
-template <int NB, typename T>
+template <int NB, typename T, bool PTS>
 __device__ void bat_ops(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB + 2], double *buf, T *ops, int lane) {
     constexpr int M = 1 << NB;
     constexpr int S = kBS;
@@ -140,14 +187,27 @@ __device__ void bat_ops(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB +
 #pragma unroll 1
         for (int j = 0; j < S; ++j) {
             slab_f<NB, S>(f, cur, lane, j);
-            opx_step<NB, T>(G, wt, f, s == 0 && j == 0);
+            if constexpr (PTS) {
+                T wx[NB + 2];
+                pweights<NB, T>(wx, bp, inst, (int64_t)lane * bp.P + s * S + j);  // edge into the point
+                opx_step<NB, T>(G, wx, f, s == 0 && j == 0);
+            } else {
+                opx_step<NB, T>(G, wt, f, s == 0 && j == 0);
+            }
         }
         __syncwarp();
     }
     T pf[SZ], pb[SZ];
 #pragma unroll
     for (int i = 0; i < SZ; ++i) pf[i] = pb[i] = zero_of(T{});
-    opx_store<NB, T>(G, wt, pf, pb);
+    if constexpr (PTS) {
+        T win[NB + 2], wout[NB + 2];
+        pweights<NB, T>(win, bp, inst, (int64_t)lane * bp.P);             // entry edge of the chain
+        pweights<NB, T>(wout, bp, inst, (int64_t)(lane + 1) * bp.P);      // exit edge
+        opx_store_pts<NB, T>(G, win, wout, pf, pb);
+    } else {
+        opx_store<NB, T>(G, wt, pf, pb);
+    }
 #pragma unroll
     for (int i = 0; i < SZ; ++i) {
         ops[(0 * SZ + i) * 32 + lane] = pf[i];
@@ -239,7 +299,7 @@ __device__ void bat_carries(const T *ops, int k, const int (&E)[kMaxL], T (&Fin)
 
 // Walk 1 (right to left) from Bend: checkpoint B at every slab end x0 + (s+1) S, s = 0..ns-1
 // (the last one is Bend itself).  ck layout [s][M][32].
-template <int NB, typename T>
+template <int NB, typename T, bool PTS>
 __device__ void bat_walk1(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB + 2], T (&st)[1 << NB], double *buf,
                           T *ck, int lane) {
     constexpr int M = 1 << NB;
@@ -266,7 +326,13 @@ __device__ void bat_walk1(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB
 #pragma unroll 1
         for (int jj = S - 1; jj >= 0; --jj) {
             slab_f<NB, S>(f, cur, lane, jj);
-            dp_diag<NB, T, true>(st, wt);
+            if constexpr (PTS) {
+                T wx[NB + 2];
+                pweights<NB, T>(wx, bp, inst, (int64_t)lane * bp.P + s * S + jj + 1);  // edge to the right
+                dp_diag<NB, T, true>(st, wx);
+            } else {
+                dp_diag<NB, T, true>(st, wt);
+            }
             dp_place<NB, T>(st, f);
         }
         __syncwarp();
@@ -280,7 +346,7 @@ __device__ void bat_walk1(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB
 //   MODE_UPD : phit_k <- mu_k / J (provisional scale 2^{-sum_b E_b}), returns max exponent
 //   MODE_MARG: out = phi_k J (true scale)
 //   MODE_COST: acc += phi_k hatJ (true scale)
-template <int NB, typename T, int MODE, int Q>
+template <int NB, typename T, int MODE, int Q, bool PTS>
 __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB + 2], T (&F)[1 << NB], double *buf,
                          const T *ck, int sumE_bound, int Ek, double &acc, bool &bad, int lane, bool res = false) {
     constexpr int M = 1 << NB;
@@ -324,13 +390,25 @@ __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB 
 #pragma unroll
             for (int i = S - 1; i >= (jb + 1) * Q; --i) {
                 slab_f<NB, S>(f, cur, lane, i);
-                dp_diag<NB, T, true>(st, wt);
+                if constexpr (PTS) {
+                    T wx[NB + 2];
+                    pweights<NB, T>(wx, bp, inst, x0 + (int64_t)s * S + i + 1);
+                    dp_diag<NB, T, true>(st, wx);
+                } else {
+                    dp_diag<NB, T, true>(st, wt);
+                }
                 dp_place<NB, T>(st, f);
             }
             T H[Q][M];
 #pragma unroll
             for (int i = Q - 1; i >= 0; --i) {
-                dp_diag<NB, T, true>(st, wt);
+                if constexpr (PTS) {
+                    T wx[NB + 2];
+                    pweights<NB, T>(wx, bp, inst, x0 + (int64_t)s * S + jb * Q + i + 1);
+                    dp_diag<NB, T, true>(st, wx);
+                } else {
+                    dp_diag<NB, T, true>(st, wt);
+                }
 #pragma unroll
                 for (int S2 = 0; S2 < M; ++S2) H[i][S2] = st[S2];
                 if (i > 0) {
@@ -342,7 +420,13 @@ __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB 
             for (int i = 0; i < Q; ++i) {
                 const int jx = jb * Q + i;
                 slab_f<NB, S>(f, cur, lane, jx);
-                dp_diag<NB, T, true>(F, wt);
+                if constexpr (PTS) {
+                    T wx[NB + 2];
+                    pweights<NB, T>(wx, bp, inst, x0 + (int64_t)s * S + jx);
+                    dp_diag<NB, T, true>(F, wx);
+                } else {
+                    dp_diag<NB, T, true>(F, wt);
+                }
                 dp_place<NB, T>(F, f);
                 const T J = combine<NB, T>(F, H[i]);
                 const double jv = value_of(J);
@@ -400,7 +484,7 @@ __device__ void bat_rescale(double *v, int64_t N, int P, int shift, int lane) {
 // ---------------------------------------------------------------------------------------
 // Persistent Sinkhorn: each warp loops over instances; per instance `iters` sweeps of the l
 // Gauss-Seidel updates, all on device.
-template <int NB>
+template <int NB, bool PTS>
 __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
     // The warps of a CTA run the phases of an update in lockstep (CTA barriers between phases),
     // so only one phase's code is hot in the SM's instruction cache at a time: this kernel is
@@ -437,7 +521,7 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
         int done_it = 0;
         bool conv = false;
         double last_res = __longlong_as_double(0x7ff8000000000000ll);  // NaN: never computed
-        if (active) bat_ops<NB, T>(bp, inst, 0, wt, buf, ops, lane);
+        if (active) bat_ops<NB, T, PTS>(bp, inst, 0, wt, buf, ops, lane);
         __syncthreads();
         // One sweep = l update slots and, on check sweeps, l-1 residual slots
         // (Res_t = sum_{k<l-1} ||phi_k J_k - mu_k||_1 on the end-of-sweep vectors, Algorithm 1
@@ -455,7 +539,7 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
                 T F[M], B[M];
                 if (run) bat_carries<NB, T>(ops, k, E, F, B, lane);
                 __syncthreads();
-                if (run) bat_walk1<NB, T>(bp, inst, k, wt, B, buf, ck, lane);
+                if (run) bat_walk1<NB, T, PTS>(bp, inst, k, wt, B, buf, ck, lane);
                 __syncthreads();
                 int sumE = 0, Ek = 0, shk = 0;
 #pragma unroll
@@ -472,7 +556,7 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
                     // updates: phit_k is written as (mu_k / J~) * 2^{-sh_k}, sh_k = the shift chosen at
                     // the previous update of marginal k (lazy renormalisation: rescaled only when the
                     // chain's maximum exponent drifts beyond +-renorm)
-                    const int emax = bat_walk2<NB, T, MODE_UPD, 4>(bp, inst, k, wt, F, buf, ck, sumE, upd ? shk : Ek,
+                    const int emax = bat_walk2<NB, T, MODE_UPD, 4, PTS>(bp, inst, k, wt, F, buf, ck, sumE, upd ? shk : Ek,
                                                                    acc, b2, lane, !upd);
                     if (upd) {
                         if (b2 && fail < 0) fail = t;
@@ -494,7 +578,7 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
                 __syncthreads();
                 // chain operators of the next slot's bound set
                 const int nk = sl + 1 < nslots ? ((sl + 1) < L ? sl + 1 : sl + 1 - L) : 0;
-                if (run) bat_ops<NB, T>(bp, inst, nk, wt, buf, ops, lane);
+                if (run) bat_ops<NB, T, PTS>(bp, inst, nk, wt, buf, ops, lane);
                 __syncthreads();
             }
             if (run) {
@@ -525,7 +609,7 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
 }
 
 // One product of mode MARG (out = m_k) or COST (wout = W) for every instance.
-template <int NB, typename T, int MODE>
+template <int NB, typename T, int MODE, bool PTS>
 __global__ void __launch_bounds__(kBWarps * 32) k_bat_product(BPlan bp) {
     constexpr int L = NB + 1;
     constexpr int M = 1 << NB;
@@ -554,10 +638,10 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_product(BPlan bp) {
         int E[kMaxL];
 #pragma unroll
         for (int q = 0; q < kMaxL; ++q) E[q] = q < L ? bp.E[(inst * L + q) * 32 + lane] : 0;
-        bat_ops<NB, T>(bp, inst, k, wt, buf, ops, lane);
+        bat_ops<NB, T, PTS>(bp, inst, k, wt, buf, ops, lane);
         T F[M], B[M];
         bat_carries<NB, T>(ops, k, E, F, B, lane);
-        bat_walk1<NB, T>(bp, inst, k, wt, B, buf, ck, lane);
+        bat_walk1<NB, T, PTS>(bp, inst, k, wt, B, buf, ck, lane);
         int sumE = 0;
 #pragma unroll
         for (int q = 0; q < L; ++q)
@@ -568,10 +652,10 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_product(BPlan bp) {
             if (q == k) Ek = E[q];
         double acc = 0.0;
         bool bad = false;
-        bat_walk2<NB, T, MODE, (sizeof(T) == sizeof(double) ? 4 : 2)>(bp, inst, k, wt, F, buf, ck, sumE, Ek, acc, bad, lane);
+        bat_walk2<NB, T, MODE, (sizeof(T) == sizeof(double) ? 4 : 2), PTS>(bp, inst, k, wt, F, buf, ck, sumE, Ek, acc, bad, lane);
         if (MODE == MODE_COST) {
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-            if (lane == 0) bp.wout[inst] = bp.h * acc;
+            if (lane == 0) bp.wout[inst] = bp.hc * acc;
         }
     }
 }
@@ -683,10 +767,10 @@ int64_t bat_slots(int l) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kBWarps * 32, sm);
     };
     switch (NB) {
-        case 1: q(k_bat_sinkhorn<1>, bat_smem<1>()); break;
-        case 2: q(k_bat_sinkhorn<2>, bat_smem<2>()); break;
-        case 3: q(k_bat_sinkhorn<3>, bat_smem<3>()); break;
-        case 4: q(k_bat_sinkhorn<4>, bat_smem<4>()); break;
+        case 1: q(k_bat_sinkhorn<1, false>, bat_smem<1>()); break;
+        case 2: q(k_bat_sinkhorn<2, false>, bat_smem<2>()); break;
+        case 3: q(k_bat_sinkhorn<3, false>, bat_smem<3>()); break;
+        case 4: q(k_bat_sinkhorn<4, false>, bat_smem<4>()); break;
         default: n = 1;
     }
     cudaGetLastError();
@@ -711,6 +795,10 @@ static BPlan to_bplan(const BatchArgs &a) {
     bp.E = a.E;
     bp.ops = a.ops;
     bp.ckpt = a.ckpt;
+    bp.lam = a.lam;
+    bp.hx = a.hx;
+    bp.ne = a.ne;
+    bp.hc = a.lam ? 1.0 : a.h;
     bp.slots = a.slots;
     bp.iters = a.iters;
     bp.k = a.k;
@@ -727,38 +815,58 @@ static BPlan to_bplan(const BatchArgs &a) {
     return bp;
 }
 
-template <int NB>
+template <int NB, bool PTS>
 static cudaError_t bat_run(const BatchArgs &a, int what, cudaStream_t s, int64_t *launches) {
     const BPlan bp = to_bplan(a);
     const unsigned grid = (unsigned)((a.slots + kBWarps - 1) / kBWarps);
     const size_t sm = bat_smem<NB>();
-    static bool attr[4] = {false, false, false, false};
+    static bool attr[3] = {false, false, false};
     switch (what) {
         case 0:
-            if (!attr[0]) { cudaFuncSetAttribute(k_bat_sinkhorn<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[0] = true; }
-            k_bat_sinkhorn<NB><<<grid, kBWarps * 32, sm, s>>>(bp);
+            if (!attr[0]) { cudaFuncSetAttribute(k_bat_sinkhorn<NB, PTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[0] = true; }
+            k_bat_sinkhorn<NB, PTS><<<grid, kBWarps * 32, sm, s>>>(bp);
             break;
         case 1:
-            if (!attr[1]) { cudaFuncSetAttribute(k_bat_product<NB, double, MODE_MARG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[1] = true; }
-            k_bat_product<NB, double, MODE_MARG><<<grid, kBWarps * 32, sm, s>>>(bp);
+            if (!attr[1]) { cudaFuncSetAttribute(k_bat_product<NB, double, MODE_MARG, PTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[1] = true; }
+            k_bat_product<NB, double, MODE_MARG, PTS><<<grid, kBWarps * 32, sm, s>>>(bp);
             break;
         default:
-            if (!attr[2]) { cudaFuncSetAttribute(k_bat_product<NB, Dual, MODE_COST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[2] = true; }
-            k_bat_product<NB, Dual, MODE_COST><<<grid, kBWarps * 32, sm, s>>>(bp);
+            if (!attr[2]) { cudaFuncSetAttribute(k_bat_product<NB, Dual, MODE_COST, PTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[2] = true; }
+            k_bat_product<NB, Dual, MODE_COST, PTS><<<grid, kBWarps * 32, sm, s>>>(bp);
             break;
     }
     ++*launches;
     return cudaGetLastError();
 }
 
+template <int NB>
+static cudaError_t bat_run_any(const BatchArgs &a, int what, cudaStream_t s, int64_t *launches) {
+    return a.lam ? bat_run<NB, true>(a, what, s, launches) : bat_run<NB, false>(a, what, s, launches);
+}
+
 cudaError_t launch_batched(const BatchArgs &a, int what, cudaStream_t s, int64_t *launches) {
     switch (a.l - 1) {
-        case 1: return bat_run<1>(a, what, s, launches);
-        case 2: return bat_run<2>(a, what, s, launches);
-        case 3: return bat_run<3>(a, what, s, launches);
-        case 4: return bat_run<4>(a, what, s, launches);
+        case 1: return bat_run_any<1>(a, what, s, launches);
+        case 2: return bat_run_any<2>(a, what, s, launches);
+        case 3: return bat_run_any<3>(a, what, s, launches);
+        case 4: return bat_run_any<4>(a, what, s, launches);
         default: return cudaErrorInvalidValue;
     }
+}
+
+// lambda_e = exp(-h_e / eta_b) for every instance b and edge e (1 for edges outside the grid).
+__global__ void k_bat_lambda(double *lam, const double *hx, const double *eta, int64_t batch, int64_t ne) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= batch * ne) return;
+    const int64_t b = i / ne, e = i % ne;
+    const double h = hx[e];
+    lam[i] = h > 0.0 ? exp(-h / eta[b]) : 1.0;
+}
+
+cudaError_t launch_bat_lambda(double *lam, const double *hx, const double *eta, int64_t batch, int64_t ne, cudaStream_t s) {
+    const int64_t n = batch * ne;
+    k_bat_lambda<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(lam, hx, eta, batch, ne);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_bat_convert(const BatchArgs &a, void *const *u_dev_ptrs, int import, int is_log, cudaStream_t s,

@@ -101,6 +101,9 @@ struct BatchArgs {
     int *E;                      // device [batch][l][32] chain exponents
     const double *mu[kMaxL];     // device [batch][N]
     double *ops, *ckpt;          // scratch, sized by bat_scratch_bytes
+    const double *lam = nullptr; // non-uniform grids: [batch][ne] per-edge decays (null: uniform)
+    const double *hx = nullptr;  // non-uniform grids: [ne] edge lengths
+    int64_t ne = 0;              // edges per row: 32 P + 1
     int64_t slots;               // resident warps (= scratch slots)
     int iters, k;
     double *out;                 // [batch][N] (marginal)
@@ -112,6 +115,8 @@ struct BatchArgs {
     double *resid;               // [batch] last residual (NaN if never computed)
 };
 int64_t bat_slots(int l);
+// lam[b][e] = exp(-hx[e] / eta[b]) (1 where hx[e] = 0)
+cudaError_t launch_bat_lambda(double *lam, const double *hx, const double *eta, int64_t batch, int64_t ne, cudaStream_t s);
 // mass <- min over instances of sum_x mu[inst][x] (per-instance zero-mass check)
 cudaError_t launch_bat_min_mass(const double *mu, int64_t batch, int64_t N, double *mass, cudaStream_t s,
                                 int64_t *launches);

@@ -72,3 +72,15 @@ def test_batched_and_sharded_argument_errors(lib):
     assert lib.mmot_create_sharded(4, 100, 0.1, g, 0, uid, 2, 2, None, None, ctypes.byref(ctx)) == 1  # rank >= world
     assert lib.mmot_create_sharded(4, 100, 0.1, g, 0, None, 0, 1, None, None, ctypes.byref(ctx)) == 1  # no id
     assert ctx.value is None
+
+
+def test_points_argument_errors(lib):
+    """mmot_create_points validates the grid points on the host before any device work."""
+    ctx = ctypes.c_void_p()
+    bad = (ctypes.c_double * 4)(0.0, 0.5, 0.5, 1.0)      # not strictly increasing
+    assert lib.mmot_create_points(3, 4, 0.1, bad, 0, None, None, ctypes.byref(ctx)) == 1
+    nan = (ctypes.c_double * 3)(0.0, float("nan"), 1.0)
+    assert lib.mmot_create_points(3, 3, 0.1, nan, 0, None, None, ctypes.byref(ctx)) == 1
+    assert lib.mmot_create_points(3, 3, 0.1, None, 0, None, None, ctypes.byref(ctx)) == 1
+    ok = (ctypes.c_double * 3)(0.0, 0.2, 1.0)
+    assert lib.mmot_create_points(3, 3, -1.0, ok, 0, None, None, ctypes.byref(ctx)) == 1   # eta <= 0
