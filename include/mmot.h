@@ -131,10 +131,12 @@ MMOT_API mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const 
 /* Non-uniform 1-D grids (the paper's footnote to the uniform-grid assumption, PAPER.md:182;
  * SURVEY §8(f) NEXT-3).  x_host[N]: the grid points, finite and strictly increasing (copied).
  * The L1 cost is c(i) = sum_{p<q} |x[i_p] - x[i_q]|; every grid edge e (between points e-1 and e)
- * gets its own decay lambda_e = exp(-(x[e] - x[e-1]) / eta).  The contexts run on the persistent
- * (batched) kernel family: opts->kernel must be MMOT_KERNEL_AUTO or MMOT_KERNEL_PERSISTENT
- * (else EUNSUPPORTED); l in [2, 5]; all other arguments, layouts and the compute calls are those
- * of mmot_create / mmot_create_batched (mmot_cost returns W = sum_i c(i) t(i) in x's units).
+ * gets its own decay lambda_e = exp(-(x[e] - x[e-1]) / eta).  Kernel families: batched contexts
+ * and single instances with l <= 5, N <= 4096 (or opts->kernel = MMOT_KERNEL_PERSISTENT) run on the
+ * persistent kernel; larger single instances (l in [2, 6]) on the two-walk family
+ * (MMOT_KERNEL_SINGLE_WALK -> EUNSUPPORTED; batched contexts accept only AUTO / PERSISTENT).  All
+ * other arguments, layouts and the compute calls are those of mmot_create / mmot_create_batched
+ * (mmot_cost returns W = sum_i c(i) t(i) in x's units).
  * Errors: EINVAL for a NULL / non-finite / non-increasing x_host, plus those of the uniform
  * constructors. */
 MMOT_API mmot_status mmot_create_points(int l, int64_t N, double eta, const double *x_host, mmot_dtype dt,

@@ -118,6 +118,8 @@ struct mmot_ctx {
     mmot::BatchArgs ba{};
     double *bat_mem = nullptr;              // eta, phit, scratch, wout (one allocation)
     double *pts_mem = nullptr;              // non-uniform grids: hx [ne], lambda [batch][ne]
+    const double *pts_lam = nullptr;        // non-uniform grid, two-walk contexts: per-edge decays
+    const double *pts_hx = nullptr;         // ... and edge lengths
     int *bat_int = nullptr;                 // E, status, fail_iter
     void **bat_ptrs = nullptr;              // device array of l pointers (u[] for import/export)
     double *bat_whost = nullptr;            // pinned [batch]
@@ -600,8 +602,48 @@ mmot_status mmot_create_batched_points(int l, int64_t N, int64_t batch, const do
 
 mmot_status mmot_create_points(int l, int64_t N, double eta, const double *x_host, mmot_dtype dt, const mmot_opts *opts,
                                void *cuda_stream, mmot_ctx **out) {
+    if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
+    *out = nullptr;
     if (!(eta > 0) || !isfinite(eta)) { set_err(nullptr, "eta must be finite and > 0"); return MMOT_EINVAL; }
-    return mmot_create_batched_points(l, N, 1, &eta, x_host, dt, opts, cuda_stream, out);
+    const int kern = opts ? opts->kernel : MMOT_KERNEL_AUTO;
+    if (kern == MMOT_KERNEL_PERSISTENT || (kern == MMOT_KERNEL_AUTO && l <= 5 && N <= 4096))
+        return mmot_create_batched_points(l, N, 1, &eta, x_host, dt, opts, cuda_stream, out);
+    if (kern == MMOT_KERNEL_SINGLE_WALK) {
+        set_err(nullptr, "non-uniform grids run on the two-walk or persistent kernel families");
+        return MMOT_EUNSUPPORTED;
+    }
+    // larger instances: the two-walk family with per-edge decays
+    if (!x_host || N < 1) { set_err(nullptr, "x_host must hold N >= 1 grid points"); return MMOT_EINVAL; }
+    for (int64_t i = 0; i < N; ++i)
+        if (!isfinite(x_host[i]) || (i > 0 && !(x_host[i] > x_host[i - 1]))) {
+            set_err(nullptr, "grid points must be finite and strictly increasing (index %lld)", (long long)i);
+            return MMOT_EINVAL;
+        }
+    mmot_opts o2 = opts ? *opts : mmot_opts{0, 0, MMOT_LOG, 0, MMOT_KERNEL_AUTO};
+    o2.kernel = MMOT_KERNEL_TWO_WALK;
+    mmot_grid g{x_host[0], N > 1 ? x_host[N - 1] : x_host[0] + 1.0};
+    mmot_ctx *c = nullptr;
+    mmot_status st = create_single(l, N, eta, g, dt, &o2, cuda_stream, &c, false);
+    if (st) return st;
+    const int64_t ne = c->nchunks * c->P + 1;
+    std::vector<double> hv(2 * (size_t)ne, 0.0);  // [hx | lambda]
+    for (int64_t e = 0; e < ne; ++e) {
+        const double he = (e >= 1 && e < N) ? x_host[e] - x_host[e - 1] : 0.0;
+        hv[(size_t)e] = he;
+        hv[(size_t)(ne + e)] = he > 0.0 ? exp(-he / eta) : 1.0;
+    }
+    if (cudaMalloc(&c->pts_mem, 2 * (size_t)ne * sizeof(double)) != cudaSuccess ||
+        cudaMemcpyAsync(c->pts_mem, hv.data(), 2 * (size_t)ne * sizeof(double), cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess) {
+        set_err(c, "grid workspace allocation failed");
+        snprintf(g_err, sizeof g_err, "%s", c->err);
+        mmot_destroy(c);
+        return MMOT_ENOMEM;
+    }
+    c->pts_hx = c->pts_mem;
+    c->pts_lam = c->pts_mem + ne;
+    *out = c;
+    return MMOT_OK;
 }
 
 }  // extern "C"
@@ -749,6 +791,8 @@ static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double
         p.world = c->world;
         p.rank = c->rank;
     }
+    p.lam = c->pts_lam;
+    p.hx = c->pts_hx;
     p.partial = c->partial;
     p.stop = &c->dsc->stop;
     p.status = &c->dsc->status;
@@ -843,7 +887,8 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
             }
             CK(c, mmot::launch_product(p, mmot::MODE_UPD, c->stream, &c->launches, prof_events(c, mmot::MODE_UPD),
                                        rx ? !rx_ready : ops_for != k, true));
-            ops_for = l <= 5 ? (k + 1) % l : -1;  // l = 6: next-update operators are not fused (registers)
+            // l = 6 / non-uniform grids: next-update operators are not fused
+            ops_for = (l <= 5 && !c->pts_lam) ? (k + 1) % l : -1;
             if (rx) {
                 rx_ready = true;
                 cur = 1 - cur;
@@ -988,7 +1033,9 @@ mmot_status mmot_cost(mmot_ctx *c, const void *const *u, double *W) {
     const int k = c->l - 1;
     Plan p = make_plan(c, k, lin, nullptr, nullptr, 0);
     CK(c, mmot::launch_product(p, mmot::MODE_COST, c->stream, &c->launches, prof_events(c, mmot::MODE_COST)));
-    CK(c, mmot::launch_sum(c->partial, c->nchunks, &c->dsc->W, c->h, 0, &c->dsc->stop, c->stream, &c->launches));
+    // uniform grids: hatJ counts crossed edges (W = h <phi, hatJ>); non-uniform: the duals carry h_e
+    CK(c, mmot::launch_sum(c->partial, c->nchunks, &c->dsc->W, c->pts_lam ? 1.0 : c->h, 0, &c->dsc->stop, c->stream,
+                           &c->launches));
     st = shard_allreduce(c, &c->dsc->W);
     if (st) return st;
     st = sync_report(c);

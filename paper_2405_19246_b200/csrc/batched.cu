@@ -116,46 +116,10 @@ struct BPlan {
     double *resid;                  // [batch]
 };
 
-// Non-uniform grids (paper footnote P:182): weights of edge e, w_a = lambda_e^{a(l-a)}, and for
-// duals the cost tangent a(l-a) h_e w_a (the edge's contribution to c(i) = sum_e h_e n(l-n)).
+// Non-uniform grids (paper footnote P:182): weights of edge e of instance inst (walk.cuh).
 template <int NB, typename T>
 __device__ __forceinline__ void pweights(T (&w)[NB + 2], const BPlan &bp, int64_t inst, int64_t e) {
-    constexpr int L = NB + 1;
-    const double lam = __ldg(bp.lam + inst * bp.ne + e);
-    double pw[L * L / 4 + 1];  // lambda^0 .. lambda^{max a(l-a)}
-    pw[0] = 1.0;
-#pragma unroll
-    for (int i = 1; i <= L * L / 4; ++i) pw[i] = pw[i - 1] * lam;
-    double he = 0.0;
-    if constexpr (sizeof(T) != sizeof(double)) he = __ldg(bp.hx + e);
-#pragma unroll
-    for (int a = 0; a <= NB + 1; ++a) {
-        const int ea = a <= L ? a * (L - a) : 0;
-        const double wa = a <= L ? pw[ea] : 0.0;
-        if constexpr (sizeof(T) == sizeof(double)) {
-            reinterpret_cast<double &>(w[a]) = wa;
-        } else {
-            reinterpret_cast<Dual &>(w[a]) = Dual{wa, (double)ea * he * wa};
-        }
-    }
-}
-
-// Chain operators under per-edge weights: prefix operator w_c(entry edge) Gt_c, suffix operator
-// w_c(exit edge) Gt_{l-c-|V|} (the duality of opx_store with the two boundary edges made explicit:
-// the chain's internal edges carry the same exponents in both, DESIGN.md §2 A20).
-template <int NB, typename T>
-__device__ __forceinline__ void opx_store_pts(const T (&G)[NB + 1][1 << NB], const T *win, const T *wout, T *pf, T *pb) {
-    constexpr int M = 1 << NB;
-#pragma unroll
-    for (int c = 0; c <= NB; ++c)
-#pragma unroll
-        for (int V = 0; V < M; ++V)
-            if (c + pc(V) <= NB) {
-                const int cp = NB + 1 - c - pc(V);
-                pf[c * M + V] = c == 0 ? G[0][V] : mul(win[c], G[c][V]);
-                const T r = cp > NB ? one_of(T{}) : G[cp][V];
-                pb[c * M + V] = c == 0 ? r : mul(wout[c], r);
-            }
+    pweights_val<NB, T>(w, __ldg(bp.lam + inst * bp.ne + e), sizeof(T) == sizeof(double) ? 0.0 : __ldg(bp.hx + e));
 }
 
 

@@ -202,6 +202,24 @@ __device__ __forceinline__ void opx_store(const T (&G)[NB + 1][1 << NB], const T
             }
 }
 
+// Chain operators under per-edge weights: prefix operator w_c(entry edge) Gt_c, suffix operator
+// w_c(exit edge) Gt_{l-c-|V|} (the duality of opx_store with the two boundary edges made explicit:
+// the chain's internal edges carry the same exponents in both, DESIGN.md §2 A20).
+template <int NB, typename T>
+__device__ __forceinline__ void opx_store_pts(const T (&G)[NB + 1][1 << NB], const T *win, const T *wout, T *pf, T *pb) {
+    constexpr int M = 1 << NB;
+#pragma unroll
+    for (int c = 0; c <= NB; ++c)
+#pragma unroll
+        for (int V = 0; V < M; ++V)
+            if (c + pc(V) <= NB) {
+                const int cp = NB + 1 - c - pc(V);
+                pf[c * M + V] = c == 0 ? G[0][V] : mul(win[c], G[c][V]);
+                const T r = cp > NB ? one_of(T{}) : G[cp][V];
+                pb[c * M + V] = c == 0 ? r : mul(wout[c], r);
+            }
+}
+
 // out = Op(in):  out[S] = sum_{U subset S} in[U] * G[|U|][S\U]
 template <int NB, typename T>
 __host__ __device__ __forceinline__ void op_apply(const T (&G)[NB + 1][1 << NB], const T (&in)[1 << NB], T (&out)[1 << NB]) {

@@ -64,6 +64,8 @@ struct Plan {
     int *status;                     // device status (mmot_status) of the run
     int *fail_iter;                  // device: sweep index of the first failure
     int iter;                        // current sweep index (for fail_iter)
+    const double *lam = nullptr;     // non-uniform grid: per-edge decays [nchunks P + 1] (null: uniform)
+    const double *hx = nullptr;      // non-uniform grid: edge lengths (cost duals)
 };
 
 // Enqueue one product (ops -> scan -> apply) of `mode` on `s`.  Returns the number of

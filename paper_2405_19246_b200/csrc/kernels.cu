@@ -32,7 +32,24 @@ static const bool g_no_tmem = [] { const char *e = getenv("MMOT_NO_TMEM"); retur
 // ---------------------------------------------------------------------------------------
 constexpr int kWarpsPerCta = 4;
 
+// Non-uniform grids: weights of grid edge e (between points e-1 and e) from the context's arrays.
 template <int NB, typename T>
+__device__ __forceinline__ void pweights_plan(T (&w)[NB + 2], const Plan &p, int64_t e) {
+    pweights_val<NB, T>(w, __ldg(p.lam + e), sizeof(T) == sizeof(double) ? 0.0 : __ldg(p.hx + e));
+}
+// dp_diag with the uniform weights, or those of edge e on a non-uniform grid
+template <int NB, typename T, bool PTS>
+__device__ __forceinline__ void diag_e(T (&st)[1 << NB], const T (&wt)[NB + 2], const Plan &p, int64_t e) {
+    if constexpr (PTS) {
+        T w[NB + 2];
+        pweights_plan<NB, T>(w, p, e);
+        dp_diag<NB, T, true>(st, w);
+    } else {
+        dp_diag<NB, T, true>(st, wt);
+    }
+}
+
+template <int NB, typename T, bool PTS = false>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_ops(Plan p) {
     constexpr int M = 1 << NB;
     constexpr int S = slab_s(NB);
@@ -66,14 +83,29 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_ops(Plan p) {
             const int64_t x = x0 + (int64_t)s * S + j;
             if (x < x1) {
                 slab_f<NB, S>(f, cur, lane, j);
-                opx_step<NB, T>(G, wt, f, s == 0 && j == 0);
+                if constexpr (PTS) {
+                    T wx[NB + 2];
+                    pweights_plan<NB, T>(wx, p, x);  // edge into point x
+                    opx_step<NB, T>(G, wx, f, s == 0 && j == 0);
+                } else {
+                    opx_step<NB, T>(G, wt, f, s == 0 && j == 0);
+                }
             }
         }
         __syncwarp();
     }
-    if (c < p.nchunks)
-        opx_store<NB, T>(G, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
-                         static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+    if (c < p.nchunks) {
+        if constexpr (PTS) {
+            T win[NB + 2], wout[NB + 2];
+            pweights_plan<NB, T>(win, p, x0);           // entry edge of the chunk
+            pweights_plan<NB, T>(wout, p, x0 + p.P);    // exit edge (1 beyond the grid)
+            opx_store_pts<NB, T>(G, win, wout, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
+                                 static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+        } else {
+            opx_store<NB, T>(G, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
+                             static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -682,7 +714,7 @@ __device__ __forceinline__ void next_ops_step(T (&Gx)[NB + 1][1 << NB], const T 
 // FULL = every live lane owns a complete chain of P points (P % S == 0): no per-point bounds
 // predicates, compile-time checkpoint positions.  The ragged last chain (and tiny P) use
 // FULL = false.  Chains [cbeg, cend) are processed.
-template <int NB, typename T, int MODE, bool NEXT, bool FULL>
+template <int NB, typename T, int MODE, bool NEXT, bool FULL, bool PTS = false>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64_t cbeg, int64_t cend) {
     using AV = ApplyVecs<NB, MODE>;
     constexpr int M = 1 << NB;
@@ -746,7 +778,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64
             if (FULL) {
                 if (jj == 0 && s == 0) break;
                 slab_f<NB, S>(f, cur, lane, jj);
-                dp_diag<NB, T, true>(st, wt);
+                diag_e<NB, T, PTS>(st, wt, p, x0 + (int64_t)s * S + jj + 1);
                 dp_place<NB, T>(st, f);
                 if (jj % Q == 0) {
                     const int j = s * QPS + jj / Q - 1;
@@ -757,7 +789,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64
                 const int64_t x = x0 + (int64_t)s * S + jj;
                 if (x < x1 && x > x0) {
                     slab_f<NB, S>(f, cur, lane, jj);
-                    dp_diag<NB, T, true>(st, wt);
+                    diag_e<NB, T, PTS>(st, wt, p, x + 1);
                     dp_place<NB, T>(st, f);
                     if ((((int)(x - x0)) % Q) == 0) {
                         const int j = (int)((x - x0) / Q) - 1;
@@ -792,7 +824,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64
 #pragma unroll
                 for (int i = Q - 1; i >= 0; --i) {
                     if (FULL || i < len) {
-                        dp_diag<NB, T, true>(st, wt);
+                        diag_e<NB, T, PTS>(st, wt, p, base + i + 1);
 #pragma unroll
                         for (int S2 = 0; S2 < M; ++S2) H[i][S2] = st[S2];
                         if (i > 0) {
@@ -806,7 +838,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64
                     if (FULL || i < len) {
                         const int jx = jb * Q + i;
                         slab_f<NB, S>(f, cur, lane, jx);
-                        dp_diag<NB, T, true>(F, wt);
+                        diag_e<NB, T, PTS>(F, wt, p, base + i);
                         dp_place<NB, T>(F, f);
                         const T J = combine<NB, T>(F, H[i]);
                         const double o = epilogue<NB, T, MODE>(J, cur, lane, jx, acc, bad);
@@ -1522,19 +1554,19 @@ static size_t apply_smem() {
     return (size_t)kWarpsPerCta * (2 * ApplyVecs<NB, MODE>::NV + 1) * 32 * (slab_s(NB) + 1) * sizeof(double);
 }
 
-template <int NB, typename T, int MODE, bool NEXT, bool FULL>
+template <int NB, typename T, int MODE, bool NEXT, bool FULL, bool PTS = false>
 static void launch_apply_range(const Plan &p, int64_t cbeg, int64_t cend, cudaStream_t s, int64_t *launches) {
     if (cend <= cbeg) return;
     const size_t sm = apply_smem<NB, MODE>();
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_chunk_apply<NB, T, MODE, NEXT, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_chunk_apply<NB, T, MODE, NEXT, FULL, PTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sm);
         attr = true;
     }
     const int tpb = kWarpsPerCta * 32;
     const int64_t nb = (cend - cbeg + tpb - 1) / tpb;
-    k_chunk_apply<NB, T, MODE, NEXT, FULL><<<(unsigned)nb, tpb, sm, s>>>(p, cbeg, cend);
+    k_chunk_apply<NB, T, MODE, NEXT, FULL, PTS><<<(unsigned)nb, tpb, sm, s>>>(p, cbeg, cend);
     ++*launches;
 }
 
@@ -1598,6 +1630,14 @@ template <int NB, typename T, int MODE, bool NEXT = false>
 static void launch_apply(const Plan &p, int64_t /*nb*/, int /*tpb*/, cudaStream_t s, int64_t *launches) {
     const bool full_ok = p.P % slab_s(NB) == 0;
     const int64_t nfull = full_ok ? p.N / p.P : 0;
+    if (p.lam) {
+        // non-uniform grid (two-walk contexts only; no fused next-update operators)
+        if constexpr (!NEXT) {
+            launch_apply_range<NB, T, MODE, false, true, true>(p, 0, nfull, s, launches);
+            launch_apply_range<NB, T, MODE, false, false, true>(p, nfull, p.nchunks, s, launches);
+        }
+        return;
+    }
     if (p.sw) {
         if constexpr (NB <= 4) {
             if constexpr (NEXT && MODE == MODE_UPD && sizeof(T) == sizeof(double) && NB >= 2) {
@@ -1659,9 +1699,11 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k_chunk_ops<NB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            cudaFuncSetAttribute(k_chunk_ops<NB, T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             attr = true;
         }
-        k_chunk_ops<NB, T><<<(unsigned)nb, tpb, sm, s>>>(p);
+        if (p.lam) k_chunk_ops<NB, T, true><<<(unsigned)nb, tpb, sm, s>>>(p);
+        else k_chunk_ops<NB, T><<<(unsigned)nb, tpb, sm, s>>>(p);
         ++*launches;
     }
     if (ev) cudaEventRecord(ev[1], s);
@@ -1773,7 +1815,7 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
     switch (mode) {
         case MODE_MARG: launch_apply<NB, T, MODE_MARG>(p, nb, tpb, s, launches); break;
         case MODE_UPD:
-            if (next && NB <= 4) {
+            if (next && NB <= 4 && !p.lam) {
                 if constexpr (sizeof(T) == sizeof(double) && NB <= 4)
                     launch_apply<NB, T, MODE_UPD, true>(p, nb, tpb, s, launches);
             } else {

@@ -77,6 +77,28 @@ __device__ __forceinline__ void slab_f(double (&f)[NB > 0 ? NB : 1], const doubl
 }
 
 
+// Non-uniform grids (paper footnote P:182): the weights of one grid edge with decay lambda =
+// exp(-h_e / eta): w_a = lambda^{a(l-a)}, and for duals the cost tangent a(l-a) h_e w_a (the edge's
+// share of c(i) = sum_e h_e n(l-n)).
+template <int NB, typename T>
+__device__ __forceinline__ void pweights_val(T (&w)[NB + 2], double lam, double he) {
+    constexpr int L = NB + 1;
+    double pw[L * L / 4 + 1];  // lambda^0 .. lambda^{max a(l-a)}
+    pw[0] = 1.0;
+#pragma unroll
+    for (int i = 1; i <= L * L / 4; ++i) pw[i] = pw[i - 1] * lam;
+#pragma unroll
+    for (int a = 0; a <= NB + 1; ++a) {
+        const int ea = a <= L ? a * (L - a) : 0;
+        const double wa = a <= L ? pw[ea] : 0.0;
+        if constexpr (sizeof(T) == sizeof(double)) {
+            reinterpret_cast<double &>(w[a]) = wa;
+        } else {
+            reinterpret_cast<Dual &>(w[a]) = Dual{wa, (double)ea * he * wa};
+        }
+    }
+}
+
 // mu / J with one Newton step on the reciprocal (relative error ~2^-46) and a residual
 // correction of the quotient, which squares that error: q' - mu/J = O(2^-92) + rounding.
 __device__ __forceinline__ double div_nr1(double mu, double j) {

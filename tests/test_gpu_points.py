@@ -33,7 +33,7 @@ def test_points_marginals_and_cost(l, N):
     eta = 0.02
     phis = list(mmot_inputs.random_positive(200 + l, l, N))
     ctx = mm.Context(l, N, eta, repr="linear", points=x)
-    assert ctx.info["kernel"] == "persistent"
+    assert ctx.info["kernel"] == ("persistent" if N <= 4096 else "two_walk")
     u = _dev(phis)
     for k in range(l):
         got = ctx.marginal(k, u).cpu().numpy()
@@ -108,3 +108,40 @@ def test_uniform_points_equal_uniform_context():
     assert abs(a.cost(u) - b.cost(u)) <= RTOL * abs(b.cost(u))
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("l,N", [(3, 9000), (4, 20000), (6, 2500)])
+def test_points_two_walk_family(l, N):
+    """Instances above the persistent-kernel size run on the two-walk family with per-edge decays."""
+    x = _grid(500 + l, N)
+    eta = 0.01
+    phis = list(mmot_inputs.random_positive(600 + l, l, N))
+    ctx = mm.Context(l, N, eta, repr="linear", points=x)
+    assert ctx.info["kernel"] == "two_walk"
+    u = _dev(phis)
+    for k in (0, l - 1):
+        got = ctx.marginal(k, u).cpu().numpy()
+        want = phis[k] * points.product(phis, x, eta, k)
+        assert np.max(np.abs(got - want) / want) <= RTOL, k
+    W = ctx.cost(u)
+    ctx.close()
+    assert abs(W - points.cost(phis, x, eta)) <= RTOL * abs(W)
+
+
+def test_points_two_walk_sinkhorn_with_residual():
+    l, N, eta, T = 3, 6000, 0.02, 3
+    x = _grid(77, N)
+    mus = np.stack(mmot_inputs.random_marginals(78, l, N))
+    ctx = mm.Context(l, N, eta, repr="log", points=x, check_every=1)
+    assert ctx.info["kernel"] == "two_walk"
+    u = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in range(l)]
+    ctx.init_uniform(u)
+    rep = ctx.sinkhorn(_dev(mus), T, 1e-300, u)
+    assert rep["status"] == 0 and rep["iters_done"] == T
+    g = np.stack([v.cpu().numpy() for v in u])
+    ctx.close()
+    ref = points.sinkhorn(mus, x, eta, T)
+    assert np.max(np.abs(g - np.log(ref))) <= 1e-9
+    m = points.marginals(ref, x, eta)
+    res_ref = float(sum(np.abs(m[k] - mus[k]).sum() for k in range(l - 1)))
+    assert rep["residual"] == pytest.approx(res_ref, rel=1e-8)
