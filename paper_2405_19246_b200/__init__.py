@@ -215,6 +215,8 @@ class Context:
         opts = _Opts(int(check_every), 0, LOG if repr == "log" else LINEAR, int(chunk), kern)
         ctx = ctypes.c_void_p()
         self.shard = shard
+        if shard is not None and points is not None:
+            raise MMOTError(10, "sharded contexts support uniform grids only")
         if shard is not None:
             rank, world, uid = shard
             self.N_global = self.N

@@ -145,3 +145,36 @@ def test_points_two_walk_sinkhorn_with_residual():
     m = points.marginals(ref, x, eta)
     res_ref = float(sum(np.abs(m[k] - mus[k]).sum() for k in range(l - 1)))
     assert rep["residual"] == pytest.approx(res_ref, rel=1e-8)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 9])
+def test_points_tiny_grids(N):
+    l, eta = 3, 0.1
+    x = np.sort(np.random.default_rng(N).uniform(0, 1, N)) if N > 1 else np.array([0.25])
+    if N > 1:
+        x = np.unique(x)
+        assert len(x) == N
+    phis = list(mmot_inputs.random_positive(40 + N, l, N))
+    ctx = mm.Context(l, N, eta, repr="linear", points=x)
+    u = _dev(phis)
+    for k in range(l):
+        got = ctx.marginal(k, u).cpu().numpy()
+        want = phis[k] * points.product(phis, x, eta, k)
+        assert np.max(np.abs(got - want) / want) <= RTOL, k
+    W = ctx.cost(u)
+    ctx.close()
+    Wr = points.cost(phis, x, eta)
+    assert abs(W - Wr) <= RTOL * max(abs(Wr), 1e-300) or (Wr == 0.0 and W == 0.0)
+
+
+def test_points_rejects_single_walk_and_sharding_is_uniform_only():
+    x = np.linspace(0.0, 1.0, 100) ** 2
+    with pytest.raises(mm.MMOTError) as e:
+        mm.Context(3, 100, 0.1, points=x, kernel="single_walk")
+    assert e.value.name == "MMOT_EUNSUPPORTED"
+    ctx = mm.Context(3, 100, 0.1, points=x, kernel="two_walk")
+    assert ctx.info["kernel"] == "two_walk"
+    ctx.close()
+    with pytest.raises(mm.MMOTError) as e:
+        mm.Context(3, 100, 0.1, points=x, shard=(0, 1, mm.nccl_unique_id()))
+    assert e.value.name == "MMOT_EUNSUPPORTED"
