@@ -136,6 +136,8 @@ def oracle_batched_rate(cfg, n_inst: int = 2, sweeps: int = 2):
     t0 = time.perf_counter()
     for b in range(n_inst):
         mus = mmot_inputs.c5_marginals(b, cfg.N, cfg.l)
+        if cfg.dtype == "f32":
+            mus = mus.astype(np.float32).astype(np.float64)  # the fp32-rounded inputs of the GPU run
         osk.sinkhorn(mus, h, float(etas[b]), sweeps, domain="log")
     dt = time.perf_counter() - t0
     elems = n_inst * sweeps * cfg.l * cfg.l * cfg.N
@@ -197,8 +199,11 @@ def run_batched(args, cfg):
     B = b1 - b0
     etas = [float(e) for e in mmot_inputs.c5_etas(cfg.batch)[b0:b1]]
     mus_h = mmot_inputs.c5_batch_marginals(b0, B, N, l)            # [l][B][N] fp64, seeded
-    mus_d = [torch.from_numpy(mus_h[q]).to(dev) for q in range(l)]
-    ctx = mm.Context(l, N, etas, batch=B, repr="log")
+    io32 = cfg.dtype == "f32"  # C5 is an fp32 config: fp32 marginals in (MMOT_F32 I/O), fp64 scans
+    if io32:
+        mus_h = mus_h.astype(np.float32)
+    mus_d = [torch.from_numpy(np.ascontiguousarray(mus_h[q])).to(dev) for q in range(l)]
+    ctx = mm.Context(l, N, etas, batch=B, repr="log", dtype="f32" if io32 else "f64")
     u = [torch.empty((B, N), dtype=torch.float64, device=dev) for _ in range(l)]
     state = {}
     stream = ctx.stream
@@ -283,7 +288,7 @@ def run_batched(args, cfg):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e_ms = float(te.item())
         e2e = {"value": evals_all * l * N / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
-               "h2d_bytes_per_step": l * B * N * 8, "d2h_bytes_per_step": l * B * N * 8 + B * 8}
+               "h2d_bytes_per_step": l * B * N * mus_h.itemsize, "d2h_bytes_per_step": l * B * N * 8 + B * 8}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -291,6 +296,7 @@ def run_batched(args, cfg):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"C5: {cfg.batch} instances x (l={l}, N={N}), eta_b ~ logU[1e-3,1e-1], "
                                    f"T={T}, f64 arithmetic with per-chain exponents", "l": l, "N": N,
+                       "io_dtype": "f32 marginals (MMOT_F32 context), fp64 u[]" if io32 else "f64",
                        "batch": cfg.batch, "iters": T, "parallelism": f"instances sharded over {ws} GPU(s)",
                        "l2": "per-instance working set L2/SMEM resident; no flush (ALU-bound)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,

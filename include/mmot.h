@@ -105,7 +105,9 @@ typedef struct {
 
 /* Create a context for single instances of (l, N, eta) on `grid`.
  *   l in [2, MMOT_MAX_L], N >= 1, eta > 0 finite, x_max > x_min when N > 1.
- *   dt: arithmetic of the scans (MMOT_F64 implemented; MMOT_F32 -> EUNSUPPORTED in v0.1).
+ *   dt: element type of the marginals and of mmot_marginal's output (u[] is fp64 for both):
+ *       MMOT_F64 double; MMOT_F32 float (fp32 I/O: the scans run in fp64 on widened copies, so an
+ *       fp32 context reproduces the fp64 result of the fp32-rounded inputs).
  *   opts may be NULL (defaults).  cuda_stream: cudaStream_t (NULL = legacy default stream).
  * The per-edge weights w_a = lambda^{a(l-a)} = exp(-a(l-a) h/eta), a = 0..l, are computed
  * once in fp64 on the host (A15).  Allocates all workspace.
@@ -116,7 +118,7 @@ MMOT_API mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, m
 /* Create a context for `batch` independent instances of (l, N) on the same grid, instance b
  * with its own eta_host[b] (BASELINE C5: 8192 x (l=5, N=4096), eta ~ logU[1e-3, 1e-1]).
  *   l in [2, 5] in this build (EUNSUPPORTED above), N >= 1, batch >= 1, every eta finite > 0;
- *   dt: MMOT_F64 (MMOT_F32 -> EUNSUPPORTED in this build).  eta_host is copied.
+ *   dt: MMOT_F64 or MMOT_F32 (fp32 I/O, as for mmot_create).  eta_host is copied.
  * Layouts for the compute calls on a batched context: every array argument is a plane of
  * `batch` consecutive N-vectors ([batch][N], instance-major); mmot_cost fills W[batch] (host);
  * mmot_sinkhorn runs at most `iters` sweeps per instance, one warp per instance on device, each

@@ -209,6 +209,9 @@ class Context:
         self.eta = float(eta) if self.batch is None else [float(e) for e in eta]
         self.grid = (float(grid[0]), float(grid[1]))
         self.repr = repr
+        if dtype not in ("f64", "f32"):
+            raise MMOTError(1, f"dtype must be 'f64' or 'f32', got {dtype!r}")
+        self.dtype = dtype  # f32: float marginals / marginal outputs (fp32 I/O), fp64 scans; u[] stays float64
         self.h = (self.grid[1] - self.grid[0]) / (self.N - 1) if self.N > 1 else 1.0
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         kern = {"auto": 0, "two_walk": 1, "single_walk": 2, "persistent": 3}[kernel]
@@ -291,11 +294,15 @@ class Context:
         import torch
         if out is None:
             shape = (self.N,) if self.batch is None else (self.batch, self.N)
-            out = torch.empty(shape, dtype=torch.float64, device=u[0].device)
+            out = torch.empty(shape, dtype=torch.float32 if self.dtype == "f32" else torch.float64, device=u[0].device)
         self._check(self._lib.mmot_marginal(self._ctx, int(k), self._ptrs(u), ctypes.c_void_p(out.data_ptr())))
         return out
 
     def sinkhorn(self, marginals, iters: int, tol: float, u) -> dict:
+        import torch
+        want = torch.float32 if self.dtype == "f32" else torch.float64
+        if any(m.dtype != want for m in marginals) or any(x.dtype != torch.float64 for x in u):
+            raise MMOTError(2, f"marginals must be {want} and u float64 for a {self.dtype} context")
         rep = _Report()
         st = self._lib.mmot_sinkhorn(self._ctx, self._ptrs(marginals), int(iters), float(tol), self._ptrs(u),
                                      ctypes.byref(rep))

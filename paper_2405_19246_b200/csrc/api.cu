@@ -118,6 +118,8 @@ struct mmot_ctx {
     mmot::BatchArgs ba{};
     double *bat_mem = nullptr;              // eta, phit, scratch, wout (one allocation)
     double *pts_mem = nullptr;              // non-uniform grids: hx [ne], lambda [batch][ne]
+    double *f32_mem = nullptr;              // MMOT_F32 I/O: widened marginals [l][n] + output [n] (lazy)
+    float *f32_stage = nullptr;             // MMOT_F32 host calls: float staging [l][n] (lazy)
     const double *pts_lam = nullptr;        // non-uniform grid, two-walk contexts: per-edge decays
     const double *pts_hx = nullptr;         // ... and edge lengths
     int *bat_int = nullptr;                 // E, status, fail_iter
@@ -216,6 +218,8 @@ void mmot_destroy(mmot_ctx *ctx) {
     cudaFree(ctx->out_t);
     cudaFree(ctx->bat_mem);
     cudaFree(ctx->pts_mem);
+    cudaFree(ctx->f32_mem);
+    cudaFree(ctx->f32_stage);
     cudaFree(ctx->rx_mem);
     cudaFree(ctx->shard_mem);
     if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
@@ -266,7 +270,6 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
         return MMOT_EINVAL;
     }
     if (l > MMOT_MAX_L) { set_err(nullptr, "l=%d > MMOT_MAX_L=%d in this build", l, MMOT_MAX_L); return MMOT_EUNSUPPORTED; }
-    if (dt == MMOT_F32) { set_err(nullptr, "MMOT_F32 single-instance contexts are not implemented yet"); return MMOT_EUNSUPPORTED; }
     // small instances: the persistent batched kernel with one instance (all sweeps in one launch,
     // no per-update kernel latency)
     const int kern = opts ? opts->kernel : MMOT_KERNEL_AUTO;
@@ -480,7 +483,6 @@ mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *e
         return MMOT_EINVAL;
     }
     if (l > 5) { set_err(nullptr, "batched contexts support l <= 5 in this build"); return MMOT_EUNSUPPORTED; }
-    if (dt == MMOT_F32) { set_err(nullptr, "MMOT_F32 batched contexts are not implemented yet"); return MMOT_EUNSUPPORTED; }
     mmot_ctx *c = new mmot_ctx();
     c->l = l;
     c->N = N;
@@ -940,12 +942,46 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
     return (mmot_status)h.status;
 }
 
+// MMOT_F32 contexts take float marginals and write float marginal outputs; the scans run in fp64
+// on widened copies (on B200 an fp32 scan would need per-state exponents and issue
+// more instructions than the fp64 one).
+static int64_t io_elems(const mmot_ctx *c) { return c->N * (c->batched ? c->batch : 1); }
+static mmot_status f32_ensure(mmot_ctx *c) {
+    if (c->f32_mem) return MMOT_OK;
+    CK(c, cudaMalloc(&c->f32_mem, (size_t)(c->l + 1) * io_elems(c) * sizeof(double)));
+    return MMOT_OK;
+}
+static mmot_status f32_widen(mmot_ctx *c, const void *const *marginals, const double **mu) {
+    mmot_status st = f32_ensure(c);
+    if (st) return st;
+    const int64_t n = io_elems(c);
+    for (int q = 0; q < c->l; ++q) {
+        double *dst = c->f32_mem + (size_t)q * n;
+        CK(c, mmot::launch_convert(marginals[q], dst, n, 1, c->stream, &c->launches));
+        mu[q] = dst;
+    }
+    return MMOT_OK;
+}
+
 extern "C" {
+
+static mmot_status marginal_f64(mmot_ctx *c, int k, const void *const *u, void *out);
 
 mmot_status mmot_marginal(mmot_ctx *c, int k, const void *const *u, void *out) {
     if (!c || !u || !out) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
     if (k < 0 || k >= c->l) { set_err(c, "k=%d outside [0,%d)", k, c->l); return MMOT_EINVAL; }
     cudaSetDevice(c->device);
+    if (c->dt != MMOT_F32) return marginal_f64(c, k, u, out);
+    mmot_status st = f32_ensure(c);
+    if (st) return st;
+    double *o64 = c->f32_mem + (size_t)c->l * io_elems(c);
+    st = marginal_f64(c, k, u, o64);
+    if (st) return st;
+    CK(c, mmot::launch_convert(o64, out, io_elems(c), 0, c->stream, &c->launches));
+    return MMOT_OK;
+}
+
+static mmot_status marginal_f64(mmot_ctx *c, int k, const void *const *u, void *out) {
     if (c->batched) {
         mmot_status st = bat_import(c, u);
         if (st) return st;
@@ -979,6 +1015,10 @@ mmot_status mmot_sinkhorn(mmot_ctx *c, const void *const *marginals, int iters, 
         mu[q] = static_cast<const double *>(marginals[q]);
     }
     cudaSetDevice(c->device);
+    if (c->dt == MMOT_F32) {
+        mmot_status st = f32_widen(c, marginals, mu);
+        if (st) return st;
+    }
     if (c->batched) return bat_sinkhorn(c, mu, iters, tol, u, rep);
     return sinkhorn_impl(c, mu, iters, tol, u, rep);
 }
@@ -989,12 +1029,22 @@ mmot_status mmot_sinkhorn_host(mmot_ctx *c, const void *const *marginals_host, i
     if (!c || !marginals_host || !u_host) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
     if (iters < 0 || isnan(tol)) { set_err(c, "iters must be >= 0"); return MMOT_EINVAL; }
     cudaSetDevice(c->device);
-    const size_t bytes = (size_t)c->N * sizeof(double);
+    const size_t bytes = (size_t)io_elems(c) * sizeof(double);
+    const bool f32 = c->dt == MMOT_F32;
+    if (f32 && !c->f32_stage) CK(c, cudaMalloc(&c->f32_stage, (size_t)c->l * io_elems(c) * sizeof(float)));
     for (int q = 0; q < c->l; ++q) {
         if (!marginals_host[q] || !u_host[q]) { set_err(c, "NULL host pointer"); return MMOT_EINVAL; }
         if (!c->stage_mu[q]) CK(c, cudaMalloc(&c->stage_mu[q], bytes));
         if (!c->stage_u[q]) CK(c, cudaMalloc(&c->stage_u[q], bytes));
-        CK(c, cudaMemcpyAsync(c->stage_mu[q], marginals_host[q], bytes, cudaMemcpyHostToDevice, c->stream));
+        if (f32) {
+            // fp32 marginals cross PCIe as floats and are widened on the device
+            float *fs = c->f32_stage + (size_t)q * io_elems(c);
+            CK(c, cudaMemcpyAsync(fs, marginals_host[q], (size_t)io_elems(c) * sizeof(float), cudaMemcpyHostToDevice,
+                                  c->stream));
+            CK(c, mmot::launch_convert(fs, c->stage_mu[q], io_elems(c), 1, c->stream, &c->launches));
+        } else {
+            CK(c, cudaMemcpyAsync(c->stage_mu[q], marginals_host[q], bytes, cudaMemcpyHostToDevice, c->stream));
+        }
         CK(c, cudaMemcpyAsync(c->stage_u[q], u_host[q], bytes, cudaMemcpyHostToDevice, c->stream));
     }
     const double *mu[mmot::kMaxL];

@@ -129,6 +129,8 @@ cudaError_t launch_bat_convert(const BatchArgs &a, void *const *u_dev_ptrs, int 
                                int64_t *launches);
 
 // Elementwise helpers.
+// fp32 <-> fp64 (to_f64: float in -> double out, else double in -> float out)
+cudaError_t launch_convert(const void *in, void *out, int64_t n, int to_f64, cudaStream_t s, int64_t *launches);
 cudaError_t launch_exp(const double *in, double *out, int64_t n, cudaStream_t s, int64_t *launches);
 cudaError_t launch_log(const double *in, double *out, int64_t n, cudaStream_t s, int64_t *launches);
 cudaError_t launch_fill(double *out, double v, int64_t n, cudaStream_t s, int64_t *launches);

@@ -15,6 +15,7 @@
 //                      cost).
 // Everything is fp64 (double or dual numbers for the cost).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <math.h>
 #include <stdlib.h>
 
@@ -1919,6 +1920,24 @@ __global__ void k_check(const double *v, int64_t n, int allow_neg_inf, int *flag
         __syncthreads();
     }
     if (threadIdx.x == 0 && mass) atomicAdd(mass, sh[0]);
+}
+
+// fp32 I/O contexts (MMOT_F32): widen the caller's float marginals, narrow float outputs.
+__global__ void k_f32_to_f64(const float *__restrict__ in, double *__restrict__ out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (double)in[i];
+}
+__global__ void k_f64_to_f32(const double *__restrict__ in, float *__restrict__ out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (float)in[i];
+}
+cudaError_t launch_convert(const void *in, void *out, int64_t n, int to_f64, cudaStream_t s, int64_t *launches) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    if (to_f64) k_f32_to_f64<<<grid, 256, 0, s>>>(static_cast<const float *>(in), static_cast<double *>(out), n);
+    else k_f64_to_f32<<<grid, 256, 0, s>>>(static_cast<const double *>(in), static_cast<float *>(out), n);
+    ++*launches;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_check(const double *v, int64_t n, int allow_neg_inf, int *flags, double *mass,
