@@ -40,7 +40,7 @@ def _args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C3f", "C4", "C5"])
     ap.add_argument("--impl", default="mmot", choices=["mmot", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -158,6 +158,8 @@ def run_reference(args, cfg):
     else:
         n_sample = min(cfg.N, 10_000_000)
         mus = mmot_inputs.make_marginals(cfg.name, 0, None if cfg.N <= 2_000_000 else n_sample)
+        if cfg.dtype == "f32":
+            mus = mus.astype(np.float32).astype(np.float64)  # the fp32-rounded inputs of the GPU run
         for i in range(args.warmup + args.steps):
             r, dt = oracle_update_rate(cfg, mus, n_sample)
             if i >= args.warmup:
@@ -332,8 +334,12 @@ def run_mmot(args, cfg):
         shard = (rank, ws, obj[0])
         lo, hi = mm.shard_range(N, rank, ws)
         mus_h = np.ascontiguousarray(mus_h[:, lo:hi])
-    mus_d = [torch.from_numpy(m).to(dev) for m in mus_h]
-    ctx = mm.Context(l, N, cfg.eta, repr="log", check_every=1 if tol > 0 else 0, shard=shard)
+    io32 = cfg.dtype == "f32"  # C3f: fp32 marginals in (MMOT_F32 I/O), fp64 scans
+    if io32:
+        mus_h = mus_h.astype(np.float32)
+    mus_d = [torch.from_numpy(np.ascontiguousarray(m)).to(dev) for m in mus_h]
+    ctx = mm.Context(l, N, cfg.eta, repr="log", check_every=1 if tol > 0 else 0, shard=shard,
+                     dtype="f32" if io32 else "f64")
     Nl = ctx.N  # this rank's grid points
     u = [torch.empty(Nl, dtype=torch.float64, device=dev) for _ in range(l)]
     state = {}
@@ -426,7 +432,7 @@ def run_mmot(args, cfg):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e_ms = float(te.item())
         e2e = {"value": evals * l * N / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
-               "h2d_bytes_per_step": 2 * l * Nl * 8, "d2h_bytes_per_step": l * Nl * 8}
+               "h2d_bytes_per_step": l * Nl * (mus_h.itemsize + 8), "d2h_bytes_per_step": l * Nl * 8}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -442,6 +448,7 @@ def run_mmot(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": _workload(cfg), "l": l, "N": N, "eta": cfg.eta, "iters": T, "tol": tol,
+                       "io_dtype": "f32 marginals (MMOT_F32 context), fp64 u[]" if io32 else "f64",
                        "global_batch": 1,
                        "parallelism": (f"grid sharded over {ws} GPUs (contiguous chunks, NCCL all-gather of "
                                        f"whole-shard operators per update)") if ws > 1 else "single GPU",

@@ -8,7 +8,7 @@ tail -2 $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
 timeout 600 python bench.py > $O/bench_c4.json 2> $O/bench_c4.err; echo "c4 rc=$?"
 timeout 600 python bench.py --impl reference > $O/bench_c4_ref.json 2> $O/bench_c4_ref.err; echo "c4 ref rc=$?"
-for c in C1 C2 C3 C5; do timeout 900 python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err; echo "$c rc=$?"; done
+for c in C1 C2 C3 C3f C5; do timeout 900 python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err; echo "$c rc=$?"; done
 CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout 300 $CMD > $O/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_c4.csv $CMD > $O/ncu_launch.log 2>&1 && \
