@@ -85,3 +85,21 @@ def test_f64_batched_host_path_copies_every_instance():
     ctx.sinkhorn_host(mh, T, 0.0, uh)
     ctx.close()
     assert np.array_equal(g, np.stack([x.numpy() for x in uh]))
+
+
+def test_f32_sharded_world1_matches_f64():
+    l, N, eta, T = 4, 30000, 0.005, 2
+    mus = np.stack(mmot_inputs.random_marginals(31, l, N)).astype(np.float32)
+    res = {}
+    for dt in ("f32", "f64"):
+        ctx = mm.Context(l, N, eta, dtype=dt, shard=(0, 1, mm.nccl_unique_id()))
+        u = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in range(l)]
+        ctx.init_uniform(u)
+        src = mus if dt == "f32" else mus.astype(np.float64)
+        ctx.sinkhorn([torch.from_numpy(m).to(DEV) for m in src], T, 0.0, u)
+        res[dt] = (np.stack([x.cpu().numpy() for x in u]), ctx.marginal(1, u).cpu().numpy(), ctx.cost(u))
+        ctx.close()
+    assert np.max(np.abs(res["f32"][0] - res["f64"][0])) <= 1e-12 * max(1.0, np.abs(res["f64"][0]).max())
+    assert res["f32"][1].dtype == np.float32
+    assert np.array_equal(res["f32"][1], res["f64"][1].astype(np.float32))
+    assert res["f32"][2] == pytest.approx(res["f64"][2], rel=1e-12)
