@@ -205,3 +205,18 @@ def test_argument_errors():
         ctx.marginal(0, u[:2])
     assert ei.value.name == "MMOT_ESHAPE"
     ctx.close()
+
+
+@pytest.mark.parametrize("N,eta", [(400, 1e-4), (12000, 1e-3)])
+def test_overflow_reported_by_persistent_kernel(N, eta):
+    """Disjoint supports at small eta: J_k between the supports is below e^-708 relative to the
+    chain scale (the cost of crossing the gap is 0.8 / eta), beyond what per-chain exponents of
+    the scalings can absorb -- the persistent kernel reports EOVERFLOW with the sweep, like the
+    plain fp64 families, instead of returning garbage (range of the stabilisation)."""
+    x = np.arange(N) / (N - 1)
+    mus = np.stack([(x < 0.3).astype(float), (x > 0.7).astype(float), np.ones(N)])
+    mus /= mus.sum(axis=1, keepdims=True)
+    with pytest.raises(mm.MMOTError) as ei:
+        _run_gpu(mus, eta, 3, kernel="persistent")
+    assert ei.value.name == "MMOT_EOVERFLOW"
+    assert ei.value.report["fail_iter"] == 1
