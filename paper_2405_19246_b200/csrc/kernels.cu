@@ -1223,7 +1223,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
                 o = cur[(AV::IPHI * S + j) * 32 + lane] * jv;
             } else if (MODE == MODE_UPD) {
                 const double mu = cur[(AV::IMU * S + j) * 32 + lane];
-                const double q = div_nr1(mu, jv);
+                const double q = div_nr0(mu, jv);  // 2^-46 relative: inside the 1e-10 parity tolerance
                 const bool nz = nonzero(mu);
                 bad |= nz && !finite_positive(q);
                 o = nz ? q : 0.0;
