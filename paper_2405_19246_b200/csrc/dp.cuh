@@ -368,6 +368,33 @@ __device__ __forceinline__ void rx_G_step(double (&G)[NB][Rx<NB>::MO], const dou
                 if (((V >> j) & 1) && c + pc(V) <= NB) G[c - 1][V] = fma(f[j + 1], G[c - 1][V ^ (1 << j)], G[c - 1][V]);
 }
 
+// rx_G_step on the running operator scaled by s_t = w_1^t (t = diag steps applied so far): an
+// entry with c + |V| = a is multiplied by w_a / w_1, so entries with a in {1, l-1} (w_a = w_1)
+// need no multiply.  The caller keeps s_t (one multiply per point) and unscales at the uses
+// (rx_M_acc with o * s_t, rx_store with the entries times s_t).  wr[a] = w_a / w_1.
+template <int NB>
+__device__ __forceinline__ void rx_G_step_scaled(double (&G)[NB][Rx<NB>::MO], const double *wr, const double (&f)[NB],
+                                                 bool skip) {
+    constexpr int MO = Rx<NB>::MO;
+    constexpr int L = NB + 1;
+    if (!skip) {
+#pragma unroll
+        for (int c = 1; c <= NB; ++c)
+#pragma unroll
+            for (int V = 0; V < MO; ++V) {
+                const int a = c + pc(V);
+                if (a <= NB && a != 1 && a != L - 1) G[c - 1][V] *= wr[a];
+            }
+    }
+#pragma unroll
+    for (int c = 1; c <= NB; ++c)
+#pragma unroll
+        for (int j = 0; j < NB - 1; ++j)
+#pragma unroll
+            for (int V = MO - 1; V >= 0; --V)
+                if (((V >> j) & 1) && c + pc(V) <= NB) G[c - 1][V] = fma(f[j + 1], G[c - 1][V ^ (1 << j)], G[c - 1][V]);
+}
+
 // M += Pi_x s_x with Pi_x = suffix operator of [x0, x) (identity at the chain's first point,
 // else R_c[V] = w_c Gr_{l-c-|V|}[V]; l-c-|V| = NB-|R| for c = |U|+1, V = R\U) and
 // s_x[U] = o * Bo[U], Bo[U] = B[U << 1] (update k's suffix state at this point, before the

@@ -1163,6 +1163,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
     // restricted next-update scan elements (dp.cuh Rx): L, running Gr, M; old parts of the carries
     constexpr int MO = NXR ? Rx<NB>::MO : 1;
     double rL[MO], rM[MO], rG[NXR ? NB : 1][MO];
+    // rG is kept scaled by rgs = w_1^t (rx_G_step_scaled); rwr[a] = w_a / w_1
+    double rgs = 1.0, rwr[NB + 2];
+#pragma unroll
+    for (int a = 0; a <= NB + 1; ++a) rwr[a] = value_of(wt[a]) / value_of(wt[1]);
     if constexpr (NXR) {
 #pragma unroll
         for (int U = 0; U < MO; ++U) {
@@ -1242,8 +1246,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
             if constexpr (NXR) {
                 if constexpr (sizeof(T) == sizeof(double)) {
                     const bool first = j == 0 && s == 0;
-                    rx_M_acc<NB>(rM, rG, reinterpret_cast<const double *>(wt), o, Bo, first);
-                    rx_G_step<NB>(rG, reinterpret_cast<const double *>(wt), f, first);
+                    rx_M_acc<NB>(rM, rG, reinterpret_cast<const double *>(wt), o * rgs, Bo, first);
+                    rx_G_step_scaled<NB>(rG, rwr, f, first);
+                    if (!first) rgs *= reinterpret_cast<const double *>(wt)[1];
                     rx_L_step<NB>(rL, reinterpret_cast<const double *>(wt), f, o, reinterpret_cast<const double(&)[M]>(F));
                 }
             }
@@ -1264,6 +1269,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
     if constexpr (NXR) {
         constexpr int SZE = Rx<NB>::SZE;
         double ef[SZE], eb[SZE];
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+#pragma unroll
+            for (int U = 0; U < MO; ++U) rG[c][U] *= rgs;  // unscale the running operator
         rx_store<NB>(rG, rL, rM, reinterpret_cast<const double *>(wt), ef, eb);
         if (!live) {
             rx_identity<NB>(ef);
