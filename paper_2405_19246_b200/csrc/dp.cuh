@@ -424,6 +424,36 @@ __device__ __forceinline__ void rx_M_acc(double (&Mv)[Rx<NB>::MO], const double 
     }
 }
 
+// rx_M_acc on M scaled by 1/w_1 (unscale once at the chain end): the weights of the sources become
+// w_{|U|+1} / w_1 = wr[|U|+1], which is 1 for |U|+1 in {1, l-1}.
+template <int NB>
+__device__ __forceinline__ void rx_M_acc_scaled(double (&Mv)[Rx<NB>::MO], const double (&G)[NB][Rx<NB>::MO],
+                                                const double *wr, double w1inv, double o,
+                                                const double (&Bo)[Rx<NB>::MO], bool first) {
+    constexpr int MO = Rx<NB>::MO;
+    constexpr int L = NB + 1;
+    if (first) {
+        const double o1 = o * w1inv;
+#pragma unroll
+        for (int R = 0; R < MO; ++R) Mv[R] = fma(o1, Bo[R], Mv[R]);
+        return;
+    }
+    double ow[NB + 1];
+#pragma unroll
+    for (int a = 1; a <= NB; ++a) ow[a] = (a == 1 || a == L - 1) ? o : o * wr[a];
+    double sv[MO];
+#pragma unroll
+    for (int U = 0; U < MO; ++U) sv[U] = ow[pc(U) + 1] * Bo[U];
+#pragma unroll
+    for (int R = 0; R < MO; ++R) {
+        double acc = Mv[R];
+#pragma unroll
+        for (int U = 0; U < MO; ++U)
+            if ((U & R) == U) acc = fma(G[NB - pc(R) - 1][R ^ U], sv[U], acc);
+        Mv[R] = acc;
+    }
+}
+
 // Chain-end elements: prefix (A'_c[V] = w_c Gr_c[V], offset L) and suffix (A''_c[V] =
 // w_c Gr_{l-c-|V|}[V], offset M).
 template <int NB>

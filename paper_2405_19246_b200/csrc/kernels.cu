@@ -1167,6 +1167,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
     double rgs = 1.0, rwr[NB + 2];
 #pragma unroll
     for (int a = 0; a <= NB + 1; ++a) rwr[a] = value_of(wt[a]) / value_of(wt[1]);
+    const double rw1inv = 1.0 / value_of(wt[1]);
     if constexpr (NXR) {
 #pragma unroll
         for (int U = 0; U < MO; ++U) {
@@ -1246,7 +1247,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
             if constexpr (NXR) {
                 if constexpr (sizeof(T) == sizeof(double)) {
                     const bool first = j == 0 && s == 0;
-                    rx_M_acc<NB>(rM, rG, reinterpret_cast<const double *>(wt), o * rgs, Bo, first);
+                    rx_M_acc_scaled<NB>(rM, rG, rwr, rw1inv, o * rgs, Bo, first);  // rM kept as M / w_1
                     rx_G_step_scaled<NB>(rG, rwr, f, first);
                     if (!first) rgs *= reinterpret_cast<const double *>(wt)[1];
                     rx_L_step<NB>(rL, reinterpret_cast<const double *>(wt), f, o, reinterpret_cast<const double(&)[M]>(F));
@@ -1273,6 +1274,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
         for (int c = 0; c < NB; ++c)
 #pragma unroll
             for (int U = 0; U < MO; ++U) rG[c][U] *= rgs;  // unscale the running operator
+#pragma unroll
+        for (int U = 0; U < MO; ++U) rM[U] *= value_of(wt[1]);  // and the suffix offset
         rx_store<NB>(rG, rL, rM, reinterpret_cast<const double *>(wt), ef, eb);
         if (!live) {
             rx_identity<NB>(ef);
