@@ -71,7 +71,11 @@ def _workload(cfg):
 
 # ------------------------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms.  Started before the warm-up so the
+    sampler is running when the timed region starts; begin() marks the start of the timed region and
+    stop() keeps the rows taken after it.  A timed region shorter than the sampling period (C1) may
+    hold no row: then the last row before it (taken under the warm-up's load) is reported and
+    "window" says so."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -83,6 +87,26 @@ class ClockSampler:
                                        "-lms", "200", "-i", str(dev_index)], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+        self.mark = 0
+
+    def _rows(self):
+        self.f.flush()
+        rows = []
+        try:
+            for ln in open(self.f.name):
+                parts = [x.strip() for x in ln.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        return rows
+
+    def begin(self):
+        """Mark the start of the timed region (waits up to 2 s for the sampler's first row)."""
+        t0 = time.time()
+        while self.p is not None and not self._rows() and time.time() - t0 < 2.0:
+            time.sleep(0.02)
+        self.mark = len(self._rows())
 
     def stop(self):
         if self.p is None:
@@ -92,13 +116,13 @@ class ClockSampler:
             self.p.wait(timeout=5)
         except Exception:
             self.p.kill()
-        self.f.flush()
-        rows = []
-        for ln in open(self.f.name):
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
+        all_rows = self._rows()
         os.unlink(self.f.name)
+        rows = all_rows[self.mark:]
+        window = "timed region"
+        if not rows and all_rows:
+            rows = all_rows[self.mark - 1:self.mark] if self.mark > 0 else all_rows[:1]
+            window = "last sample before the timed region (region shorter than the 200 ms period)"
         if not rows:
             return None
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
@@ -106,7 +130,7 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "window": window}
 
 
 # ------------------------------------------------------------------------------------------
@@ -225,12 +249,13 @@ def run_batched(args, cfg):
         if ws > 1:
             dist.barrier()
 
+    clocks = ClockSampler(local)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local)
+    clocks.begin()
     launches0 = ctx.launches
     barrier()
     torch.cuda.synchronize()
@@ -354,13 +379,14 @@ def run_mmot(args, cfg):
         if ws > 1:
             dist.barrier()
 
+    clocks = ClockSampler(local)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     stream = ctx.stream
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local)
+    clocks.begin()
     ctx.profile(True)
     ctx.profile_read()
     launches0 = ctx.launches
