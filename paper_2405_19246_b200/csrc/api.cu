@@ -508,6 +508,7 @@ mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *e
     const size_t nd = (size_t)batch                      // eta
                       + (size_t)l * batch * N            // phit
                       + (size_t)a.slots * (opsz + cksz) / sizeof(double)
+                      + (size_t)a.slots * N                // deferred-residual save planes
                       + 2 * (size_t)batch;               // wout, resid
     const size_t ni = (size_t)batch * l * 32 + 4 * (size_t)batch;
     bool ok = cudaMalloc(&c->bat_mem, nd * sizeof(double)) == cudaSuccess &&
@@ -536,6 +537,8 @@ mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *e
     p += (size_t)a.slots * opsz / sizeof(double);
     a.ckpt = p;
     p += (size_t)a.slots * cksz / sizeof(double);
+    a.rsave = p;
+    p += (size_t)a.slots * N;
     a.wout = p;
     a.resid = p + batch;
     a.E = c->bat_int;

@@ -101,6 +101,7 @@ struct BPlan {
     const double *hx;               // non-uniform grids: [ne] edge lengths h_e (edge e between points e-1, e)
     int64_t ne;                     // 32 P + 1 (edges 0 .. 32 P; 1 / 0 outside 1 .. N-1)
     double hc;                      // cost factor: h (uniform: hatJ counts edges) or 1 (edge lengths in the tangent)
+    double *rsave;                  // [slot][N]: phit_0 before the update that closes a deferred residual
     int64_t slots;                  // resident warps (scratch slots)
     int iters;
     int k;                          // product mode: free marginal
@@ -312,7 +313,8 @@ __device__ void bat_walk1(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB
 //   MODE_COST: acc += phi_k hatJ (true scale)
 template <int NB, typename T, int MODE, int Q, bool PTS>
 __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB + 2], T (&F)[1 << NB], double *buf,
-                         const T *ck, int sumE_bound, int Ek, double &acc, bool &bad, int lane, bool res = false) {
+                         const T *ck, int sumE_bound, int Ek, double &acc, bool &bad, int lane, bool res = false,
+                         const double *oldv = nullptr, int e_old = 0) {
     constexpr int M = 1 << NB;
     constexpr int S = kBS;
     constexpr int TILE = 32 * (S + 1);
@@ -403,6 +405,9 @@ __device__ int bat_walk2(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB 
                     const double q = div_nr1(vk, jv);
                     const bool nz = nonzero(vk);
                     const int64_t x = x0 + (int64_t)s * S + jx;
+                    // deferred residual term of the previous sweep: |phi_k(old) J_k - mu_k| (the
+                    // bound vectors are that sweep's end-of-sweep vectors; a7, "free" k = 1 term)
+                    if (oldv && x < N) acc += fabs(scale2(oldv[x] * jv, sumE_bound + e_old) - vk);  // rewritten in-kernel: no __ldg
                     bad |= nz && x < N && !finite_positive(q);
                     const double o = nz ? (shok ? q * shsc : scale2(q, -Ek)) : 0.0;
                     obuf[lane * (S + 1) + jx] = o;
@@ -492,18 +497,35 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
         // line 7, P:168 generalised; stop at the first Res <= tol).  Every slot runs the same
         // code (one copy of each phase: the kernel is register- and instruction-cache-bound); the
         // chain operators of the next slot's bound set are built at the end of each slot.
+        // residual of a check sweep t < iters: the k = 0 term is taken inside sweep t+1's first update
+        // (same bound vectors), the other l-2 terms in residual slots at the end of sweep t; if the
+        // total meets tol, that first update is undone (phit_0 restored, exponents kept)
+        bool pend = false;
+        double pres = 0.0;
+        int pt = 0;
+        double *rsave = bp.rsave + slot * bp.N;
         for (int t = 1; t <= bp.iters; ++t) {
             const bool run = active && !conv && !__any_sync(0xffffffffu, bad);
             const bool check = bp.tol > 0 && (t % bp.check_every == 0 || t == bp.iters);
-            const int nslots = check ? 2 * L - 1 : L;
+            const bool defer = check && t < bp.iters;
+            const int nslots = L + (check ? (defer ? L - 2 : L - 1) : 0);
+            const int roff = defer ? 1 : 0;  // residual slot sl -> k = sl - L + roff
             double res = 0.0;
+            bool live = run;
             for (int sl = 0; sl < nslots; ++sl) {
                 const bool upd = sl < L;
-                const int k = upd ? sl : sl - L;
+                const int k = upd ? sl : sl - L + roff;
+                const bool close = upd && k == 0 && pend && live;  // this update closes sweep pt's residual
                 T F[M], B[M];
-                if (run) bat_carries<NB, T>(ops, k, E, F, B, lane);
+                if (live) bat_carries<NB, T>(ops, k, E, F, B, lane);
                 __syncthreads();
-                if (run) bat_walk1<NB, T, PTS>(bp, inst, k, wt, B, buf, ck, lane);
+                if (live) bat_walk1<NB, T, PTS>(bp, inst, k, wt, B, buf, ck, lane);
+                if (close) {
+                    // keep phit_0 of sweep pt (coalesced copy) for the residual and a possible undo
+                    const double *src = bp.phit[0] + inst * bp.N;
+                    for (int64_t x = lane; x < bp.N; x += 32) rsave[x] = src[x];
+                    __syncwarp();
+                }
                 __syncthreads();
                 int sumE = 0, Ek = 0, shk = 0;
 #pragma unroll
@@ -514,15 +536,34 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
                         shk = Sh[q];
                     }
                 }
-                if (run) {
+                if (live) {
                     double acc = 0.0;
                     bool b2 = false;
                     // updates: phit_k is written as (mu_k / J~) * 2^{-sh_k}, sh_k = the shift chosen at
                     // the previous update of marginal k (lazy renormalisation: rescaled only when the
                     // chain's maximum exponent drifts beyond +-renorm)
                     const int emax = bat_walk2<NB, T, MODE_UPD, 4, PTS>(bp, inst, k, wt, F, buf, ck, sumE, upd ? shk : Ek,
-                                                                   acc, b2, lane, !upd);
-                    if (upd) {
+                                                                        acc, b2, lane, !upd, close ? rsave : nullptr, Ek);
+                    bool undone = false;
+                    if (close) {
+                        double tot = acc;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+                        tot += pres;
+                        pend = false;
+                        last_res = tot;
+                        if (tot <= bp.tol) {
+                            // converged at sweep pt: undo this update
+                            double *dst = bp.phit[0] + inst * bp.N;
+                            for (int64_t x = lane; x < bp.N; x += 32) dst[x] = rsave[x];
+                            __syncwarp();
+                            conv = true;
+                            done_it = pt;
+                            live = false;
+                            undone = true;
+                        }
+                    }
+                    if (upd && !undone) {
                         if (b2 && fail < 0) fail = t;
                         bad |= b2;
                         const int resc = (emax > -1000000 && (emax > bp.renorm || emax < -bp.renorm)) ? emax : 0;
@@ -535,23 +576,29 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
                                 E[q] = -sumE + shk + resc;
                                 Sh[q] = shk + resc;
                             }
-                    } else {
+                    } else if (!upd) {
                         res += acc;
                     }
                 }
                 __syncthreads();
                 // chain operators of the next slot's bound set
-                const int nk = sl + 1 < nslots ? ((sl + 1) < L ? sl + 1 : sl + 1 - L) : 0;
-                if (run) bat_ops<NB, T, PTS>(bp, inst, nk, wt, buf, ops, lane);
+                const int nk = sl + 1 < nslots ? ((sl + 1) < L ? sl + 1 : sl + 1 - L + roff) : 0;
+                if (live) bat_ops<NB, T, PTS>(bp, inst, nk, wt, buf, ops, lane);
                 __syncthreads();
             }
-            if (run) {
+            if (live) {
                 done_it = t;
                 if (check) {
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) res += __shfl_xor_sync(0xffffffffu, res, o);
-                    last_res = res;
-                    if (res <= bp.tol) conv = true;
+                    if (defer) {
+                        pend = true;
+                        pres = res;
+                        pt = t;
+                    } else {
+                        last_res = res;
+                        if (res <= bp.tol) conv = true;
+                    }
                 }
             }
         }
@@ -759,6 +806,7 @@ static BPlan to_bplan(const BatchArgs &a) {
     bp.E = a.E;
     bp.ops = a.ops;
     bp.ckpt = a.ckpt;
+    bp.rsave = a.rsave;
     bp.lam = a.lam;
     bp.hx = a.hx;
     bp.ne = a.ne;

@@ -103,6 +103,7 @@ struct BatchArgs {
     int *E;                      // device [batch][l][32] chain exponents
     const double *mu[kMaxL];     // device [batch][N]
     double *ops, *ckpt;          // scratch, sized by bat_scratch_bytes
+    double *rsave = nullptr;     // [slots][N] scratch for the deferred residual (persistent kernel)
     const double *lam = nullptr; // non-uniform grids: [batch][ne] per-edge decays (null: uniform)
     const double *hx = nullptr;  // non-uniform grids: [ne] edge lengths
     int64_t ne = 0;              // edges per row: 32 P + 1
