@@ -453,8 +453,10 @@ __device__ void bat_rescale(double *v, int64_t N, int P, int shift, int lane) {
 // ---------------------------------------------------------------------------------------
 // Persistent Sinkhorn: each warp loops over instances; per instance `iters` sweeps of the l
 // Gauss-Seidel updates, all on device.
-template <int NB, bool PTS>
+template <int NB, bool PTS, bool CHK>
 __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
+    // CHK = false (tol <= 0, e.g. C5): no residual slots at all -- the residual and deferral code
+    // is compiled out, which keeps the walk registers of the fixed-sweep case unchanged
     // The warps of a CTA run the phases of an update in lockstep (CTA barriers between phases),
     // so only one phase's code is hot in the SM's instruction cache at a time: this kernel is
     // instruction-fetch bound otherwise (ncu: "no instruction" was the top stall).
@@ -506,7 +508,7 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
         double *rsave = bp.rsave + slot * bp.N;
         for (int t = 1; t <= bp.iters; ++t) {
             const bool run = active && !conv && !__any_sync(0xffffffffu, bad);
-            const bool check = bp.tol > 0 && (t % bp.check_every == 0 || t == bp.iters);
+            const bool check = CHK && bp.tol > 0 && (t % bp.check_every == 0 || t == bp.iters);
             const bool defer = check && t < bp.iters;
             const int nslots = L + (check ? (defer ? L - 2 : L - 1) : 0);
             const int roff = defer ? 1 : 0;  // residual slot sl -> k = sl - L + roff
@@ -778,10 +780,10 @@ int64_t bat_slots(int l) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kBWarps * 32, sm);
     };
     switch (NB) {
-        case 1: q(k_bat_sinkhorn<1, false>, bat_smem<1>()); break;
-        case 2: q(k_bat_sinkhorn<2, false>, bat_smem<2>()); break;
-        case 3: q(k_bat_sinkhorn<3, false>, bat_smem<3>()); break;
-        case 4: q(k_bat_sinkhorn<4, false>, bat_smem<4>()); break;
+        case 1: q(k_bat_sinkhorn<1, false, false>, bat_smem<1>()); break;
+        case 2: q(k_bat_sinkhorn<2, false, false>, bat_smem<2>()); break;
+        case 3: q(k_bat_sinkhorn<3, false, false>, bat_smem<3>()); break;
+        case 4: q(k_bat_sinkhorn<4, false, false>, bat_smem<4>()); break;
         default: n = 1;
     }
     cudaGetLastError();
@@ -835,8 +837,13 @@ static cudaError_t bat_run(const BatchArgs &a, int what, cudaStream_t s, int64_t
     static bool attr[3] = {false, false, false};
     switch (what) {
         case 0:
-            if (!attr[0]) { cudaFuncSetAttribute(k_bat_sinkhorn<NB, PTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[0] = true; }
-            k_bat_sinkhorn<NB, PTS><<<grid, kBWarps * 32, sm, s>>>(bp);
+            if (!attr[0]) {
+                cudaFuncSetAttribute(k_bat_sinkhorn<NB, PTS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                cudaFuncSetAttribute(k_bat_sinkhorn<NB, PTS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                attr[0] = true;
+            }
+            if (a.tol > 0) k_bat_sinkhorn<NB, PTS, true><<<grid, kBWarps * 32, sm, s>>>(bp);
+            else k_bat_sinkhorn<NB, PTS, false><<<grid, kBWarps * 32, sm, s>>>(bp);
             break;
         case 1:
             if (!attr[1]) { cudaFuncSetAttribute(k_bat_product<NB, double, MODE_MARG, PTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[1] = true; }
