@@ -15,4 +15,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sw_apply -s 20 -c 1 -o $O/prof_c4 $CMD > $O/ncu_c4.log 2>&1
 timeout 300 python tools/c5_probe.py 1184 30 > $O/c5probe.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bat_sinkhorn -c 1 -o $O/prof_c5 python tools/c5_probe.py 1184 30 > $O/ncu_c5.log 2>&1
+
+# summaries on the box (the reports themselves can exceed gpurun's 64 MiB copy-back limit)
+python tools/prof_summary.py $O/launches_c4.csv $O/prof_c4.ncu-rep > $O/summary_c4.txt 2>&1
+python tools/prof_summary.py $O/prof_c5.ncu-rep > $O/summary_c5.txt 2>&1
+ls -la $O/*.ncu-rep 2>/dev/null
+rm -f $O/prof_c5.ncu-rep
 echo done
