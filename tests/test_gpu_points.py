@@ -178,3 +178,21 @@ def test_points_rejects_single_walk_and_sharding_is_uniform_only():
     with pytest.raises(mm.MMOTError) as e:
         mm.Context(3, 100, 0.1, points=x, shard=(0, 1, mm.nccl_unique_id()))
     assert e.value.name == "MMOT_EUNSUPPORTED"
+
+
+@pytest.mark.parametrize("N", [600, 8000])
+def test_points_f32_io_matches_f64(N):
+    l, eta, T = 3, 0.02, 3
+    x = _grid(21, N)
+    mus = np.stack(mmot_inputs.random_marginals(22, l, N)).astype(np.float32)
+    res = {}
+    for dt in ("f32", "f64"):
+        ctx = mm.Context(l, N, eta, dtype=dt, points=x)
+        u = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in range(l)]
+        ctx.init_uniform(u)
+        src = mus if dt == "f32" else mus.astype(np.float64)
+        ctx.sinkhorn(_dev(src), T, 0.0, u)
+        res[dt] = (np.stack([v.cpu().numpy() for v in u]), ctx.marginal(0, u).cpu().numpy())
+        ctx.close()
+    assert np.max(np.abs(res["f32"][0] - res["f64"][0])) <= 1e-12 * max(1.0, np.abs(res["f64"][0]).max())
+    assert np.array_equal(res["f32"][1], res["f64"][1].astype(np.float32))
