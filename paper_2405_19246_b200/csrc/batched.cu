@@ -183,8 +183,13 @@ __device__ void bat_ops(const BPlan &bp, int64_t inst, int k, const T (&wt)[NB +
 
 // Carries of this update's bound set: Fin = prefix state entering the chain, Bend = suffix
 // state at the chain end (both in the chain's scale).  E[q] = this lane's chain exponents.
-template <int NB, typename T>
-__device__ void bat_carries(const T *ops, int k, const int (&E)[kMaxL], T (&Fin)[1 << NB], T (&Bend)[1 << NB], int lane) {
+template <int NB, typename T, bool FULLCH>
+__device__ void bat_carries(const T *ops, int k, const int (&E)[kMaxL], T (&Fin)[1 << NB], T (&Bend)[1 << NB], int lane,
+                            const BPlan &bp) {
+    // FULLCH: all 32 chains hold grid points (constant trip counts, the common case)
+    const int nch = FULLCH ? 32 : (int)((bp.N + bp.P - 1) / bp.P);
+    // nch = chains holding grid points (lanes >= nch walk only points beyond N): the carries need
+    // nch - 1 sequential steps per direction, not 31 (small N, C1)
     constexpr int M = 1 << NB;
     constexpr int SZ = OpShape<NB>::SZ;
     constexpr int L = NB + 1;
@@ -215,7 +220,7 @@ __device__ void bat_carries(const T *ops, int k, const int (&E)[kMaxL], T (&Fin)
 #pragma unroll
     for (int b = 0; b < NB; ++b) d[b] = Eb[b] - Enx[b];
 #pragma unroll 1
-    for (int s = 0; s < 31; ++s) {
+    for (int s = 0; s < nch - 1; ++s) {
         op_apply<NB, T>(G, cur, y);
         vec_shift<NB, T>(y, d);
 #pragma unroll
@@ -243,7 +248,7 @@ __device__ void bat_carries(const T *ops, int k, const int (&E)[kMaxL], T (&Fin)
     vec_unit<NB, T>(cur);
     vec_unit<NB, T>(Bend);
 #pragma unroll 1
-    for (int s = 31; s > 0; --s) {
+    for (int s = nch - 1; s > 0; --s) {
         op_apply<NB, T>(G, cur, y);
         vec_shift<NB, T>(y, d);
 #pragma unroll
@@ -519,7 +524,10 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_sinkhorn(BPlan bp) {
                 const int k = upd ? sl : sl - L + roff;
                 const bool close = upd && k == 0 && pend && live;  // this update closes sweep pt's residual
                 T F[M], B[M];
-                if (live) bat_carries<NB, T>(ops, k, E, F, B, lane);
+                if (live) {
+                    if (31 * (int64_t)bp.P < bp.N) bat_carries<NB, T, true>(ops, k, E, F, B, lane, bp);
+                    else bat_carries<NB, T, false>(ops, k, E, F, B, lane, bp);
+                }
                 __syncthreads();
                 if (live) bat_walk1<NB, T, PTS>(bp, inst, k, wt, B, buf, ck, lane);
                 if (close) {
@@ -653,7 +661,8 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bat_product(BPlan bp) {
         for (int q = 0; q < kMaxL; ++q) E[q] = q < L ? bp.E[(inst * L + q) * 32 + lane] : 0;
         bat_ops<NB, T, PTS>(bp, inst, k, wt, buf, ops, lane);
         T F[M], B[M];
-        bat_carries<NB, T>(ops, k, E, F, B, lane);
+        if (31 * (int64_t)bp.P < bp.N) bat_carries<NB, T, true>(ops, k, E, F, B, lane, bp);
+        else bat_carries<NB, T, false>(ops, k, E, F, B, lane, bp);
         bat_walk1<NB, T, PTS>(bp, inst, k, wt, B, buf, ck, lane);
         int sumE = 0;
 #pragma unroll
