@@ -109,6 +109,75 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_ops(Plan p) {
     }
 }
 
+// k_chunk_ops for NB = 5 (fp64, uniform grid) split by operator slice: the extended walk's slices
+// c = 0..NB never mix (diag scales G[c][V] by w_{c+|V|}, place stays inside slice c), so two
+// threads per chunk walk slices {0,1,2} and {3,4,5} (96 doubles each instead of 192, which spill);
+// the slices meet in shared memory for the store (the suffix operator reads slice l-c-|V|).
+constexpr int kOpsSplitChunks = 32;  // chunks per block (64 threads)
+template <int NB>
+__global__ void __launch_bounds__(2 * kOpsSplitChunks) k_chunk_ops_split(Plan p) {
+    constexpr int M = 1 << NB;
+    constexpr int L = NB + 1;
+    constexpr int HS = (NB + 1) / 2;  // slices per thread
+    __shared__ double Gs[kOpsSplitChunks][NB + 1][M];
+    const int ci = threadIdx.x >> 1, half = threadIdx.x & 1;
+    const int64_t c = (int64_t)blockIdx.x * kOpsSplitChunks + ci;
+    if (*p.stop) return;
+    double wt[NB + 2];
+    load_weights<NB, double>(wt, p.W);
+    double G[HS][M];
+#pragma unroll
+    for (int i = 0; i < HS; ++i)
+#pragma unroll
+        for (int V = 0; V < M; ++V) G[i][V] = V == 0 ? 1.0 : 0.0;
+    if (c < p.nchunks) {
+        const int64_t x0 = c * p.P, x1 = min(p.N, x0 + p.P);
+        for (int64_t x = x0; x < x1; ++x) {
+            double f[NB];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) f[b] = __ldg(p.bound[b] + x);
+            const bool skip = x == x0;
+#pragma unroll
+            for (int i = 0; i < HS; ++i) {
+                const int cc = half * HS + i;
+                if (!skip) {
+#pragma unroll
+                    for (int V = 0; V < M; ++V) {
+                        const int a = cc + pc(V);
+                        if (a < L && a > 0) G[i][V] *= wt[a];
+                    }
+                }
+#pragma unroll
+                for (int b = 0; b < NB; ++b)
+#pragma unroll
+                    for (int V = M - 1; V >= 0; --V)
+                        if (((V >> b) & 1) && cc + pc(V) <= L) G[i][V] = fma(f[b], G[i][V ^ (1 << b)], G[i][V]);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < HS; ++i)
+#pragma unroll
+        for (int V = 0; V < M; ++V) Gs[ci][half * HS + i][V] = G[i][V];
+    __syncthreads();
+    if (c >= p.nchunks) return;
+    double *pf = static_cast<double *>(p.ops_f[0]) + c * OpShape<NB>::SZ;
+    double *pb = static_cast<double *>(p.ops_b[0]) + c * OpShape<NB>::SZ;
+    // opx_store: prefix w_c Gt_c, suffix w_c Gt_{l-c-|V|} (this thread: slices half*HS ..)
+#pragma unroll
+    for (int i = 0; i < HS; ++i) {
+        const int cc = half * HS + i;
+#pragma unroll
+        for (int V = 0; V < M; ++V)
+            if (cc + pc(V) <= NB) {
+                const int cp = NB + 1 - cc - pc(V);
+                pf[cc * M + V] = cc == 0 ? Gs[ci][0][V] : wt[cc] * Gs[ci][cc][V];
+                const double r = cp > NB ? 1.0 : Gs[ci][cp][V];
+                pb[cc * M + V] = cc == 0 ? r : wt[cc] * r;
+            }
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // Phase 2a: compose groups of kGroup consecutive operators (dir 0: prefix order, dir 1:
 // suffix order, i.e. the last member is applied first).
@@ -1705,6 +1774,12 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
                 attr_sw = true;
             }
             k_sw_ops<NB, T><<<(unsigned)((p.nchp + tpb - 1) / tpb), tpb, sm, s>>>(p);
+            ++*launches;
+        }
+    } else if (with_ops && NB == 5 && sizeof(T) == sizeof(double) && !p.lam) {
+        if constexpr (NB == 5 && sizeof(T) == sizeof(double)) {
+            k_chunk_ops_split<NB><<<(unsigned)((p.nchunks + kOpsSplitChunks - 1) / kOpsSplitChunks), 2 * kOpsSplitChunks, 0,
+                                    s>>>(p);
             ++*launches;
         }
     } else if (with_ops) {
