@@ -66,7 +66,8 @@ typedef enum {
     MMOT_ECUDA = 7,        /* CUDA runtime error (see mmot_last_error)                    */
     MMOT_ENCCL = 8,        /* NCCL error (sharded contexts)                               */
     MMOT_ENOMEM = 9,       /* device allocation failed                                    */
-    MMOT_EUNSUPPORTED = 10 /* valid request this build does not implement                */
+    MMOT_EUNSUPPORTED = 10, /* valid request this build does not implement               */
+    MMOT_EPRECISION = 11   /* single-walk precision guard tripped on a sharded context     */
 } mmot_status;
 
 /* Uniform grid x_i = x_min + i h, i = 0..N-1 (endpoints included, A1). */
@@ -155,10 +156,32 @@ MMOT_API mmot_status mmot_create_batched_points(int l, int64_t N, int64_t batch,
  * mmot_nccl_unique_id on one rank, broadcast by the caller (e.g. torch.distributed).  Every
  * rank must make the same sequence of calls (each product performs one ncclAllGather of the
  * whole-shard prefix/suffix operators, ~2 (l) 2^(l-1) doubles per rank; residual and cost one
- * ncclAllReduce of a double).  Returns ENCCL if NCCL cannot be loaded or initialised. */
+ * ncclAllReduce of a double).  Returns ENCCL if NCCL cannot be loaded or initialised.
+ * Collective consistency: the data checks use the mass of the whole marginal, the status and
+ * stop flag are max-reduced over the ranks (after the checks, at every early-exit poll and at the
+ * end of a solve), and with tol > 0 the early exit is decided synchronously every 8 sweeps on the
+ * agreed flag, so all ranks leave the sweep loop together and report the same status.
+ * mmot_init_uniform fills log phi = -log N_global (the global problem's 1/N). */
 MMOT_API mmot_status mmot_create_sharded(int l, int64_t N_global, double eta, mmot_grid grid, mmot_dtype dt,
                                          const void *nccl_unique_id, int rank, int world, const mmot_opts *opts,
                                          void *cuda_stream, mmot_ctx **out);
+
+/* Virtual shards: an in-process group of `world` sharded contexts on ONE device, the device-side
+ * test mode of the sharded path (SURVEY §4 suite 4).  Each rank's context is created with
+ * mmot_create_sharded_virtual and driven by its own host thread on its own CUDA stream; the
+ * collectives of mmot_create_sharded (all-gather of the whole-shard operators, all-reduce of the
+ * residual / cost / data checks) become a host barrier plus cross-stream event waits and
+ * device-to-device copies, so the shard-boundary seeding, the carry composition with real
+ * predecessors and the partial reductions run exactly as on `world` GPUs (no kernel waits on
+ * another).  world in [1, 16].  The group must outlive its contexts; mmot_vgroup_destroy(NULL) is
+ * a no-op.  All ranks must make the same sequence of calls concurrently (a rank that fails to
+ * create leaves the others waiting, as with NCCL). */
+typedef struct mmot_vgroup mmot_vgroup;
+MMOT_API mmot_status mmot_vgroup_create(int world, mmot_vgroup **out);
+MMOT_API void mmot_vgroup_destroy(mmot_vgroup *group);
+MMOT_API mmot_status mmot_create_sharded_virtual(int l, int64_t N_global, double eta, mmot_grid grid, mmot_dtype dt,
+                                                 mmot_vgroup *group, int rank, const mmot_opts *opts,
+                                                 void *cuda_stream, mmot_ctx **out);
 
 /* 128-byte NCCL unique id for mmot_create_sharded (host memory). */
 MMOT_API mmot_status mmot_nccl_unique_id(void *out);
@@ -234,6 +257,16 @@ MMOT_API mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t 
 
 /* Kernel-launch counter: number of CUDA kernels this context has launched so far. */
 MMOT_API int64_t mmot_launch_count(const mmot_ctx *ctx);
+
+/* Single-walk precision guard.  The single-walk family walks suffix states forward
+ * through the subtractive inverse step; every product checks each chain's walked end state against
+ * the exact suffix carry of the next chain (componentwise relative error <= 1e-11, which bounds the
+ * error of every interior state).  If a check fails (scalings with large jumps, e.g. spanning
+ * 1e+-50 between neighbouring points), mmot_sinkhorn / mmot_marginal / mmot_cost redo the call on a
+ * two-walk context of the same problem before writing any output (single-walk mmot_marginal
+ * therefore synchronises the stream once), and sharded contexts return MMOT_EPRECISION on every
+ * rank.  Returns how many calls of this context were redone. */
+MMOT_API int64_t mmot_fallback_count(const mmot_ctx *ctx);
 
 /* Benchmark instrumentation.  While enabled, every tensor-vector product records CUDA events
  * on the context stream around its phases.  mmot_profile_read synchronises the stream and

@@ -12,7 +12,7 @@ import math
 import os
 from typing import List, Optional, Sequence
 
-__all__ = ["Context", "MMOTError", "lib_path", "load_library", "STATUS", "exported_symbols", "nccl_unique_id",
+__all__ = ["Context", "VirtualGroup", "MMOTError", "lib_path", "load_library", "STATUS", "exported_symbols", "nccl_unique_id",
            "shard_range", "compose_rank_carries", "compose_rank_affine"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -22,7 +22,7 @@ _lib = None
 STATUS = {
     0: "MMOT_OK", 1: "MMOT_EINVAL", 2: "MMOT_ESHAPE", 3: "MMOT_ENONFINITE", 4: "MMOT_ENEGMASS",
     5: "MMOT_EZEROMASS", 6: "MMOT_EOVERFLOW", 7: "MMOT_ECUDA", 8: "MMOT_ENCCL", 9: "MMOT_ENOMEM",
-    10: "MMOT_EUNSUPPORTED",
+    10: "MMOT_EUNSUPPORTED", 11: "MMOT_EPRECISION",
 }
 
 F64, F32 = 0, 1
@@ -81,6 +81,13 @@ def load_library():
     lib.mmot_create_sharded.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_double, _Grid, ctypes.c_int, vp,
                                         ctypes.c_int, ctypes.c_int, ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
     lib.mmot_create_sharded.restype = ctypes.c_int
+    lib.mmot_create_sharded_virtual.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_double, _Grid, ctypes.c_int,
+                                                vp, ctypes.c_int, ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
+    lib.mmot_create_sharded_virtual.restype = ctypes.c_int
+    lib.mmot_vgroup_create.argtypes = [ctypes.c_int, ctypes.POINTER(vp)]
+    lib.mmot_vgroup_create.restype = ctypes.c_int
+    lib.mmot_vgroup_destroy.argtypes = [vp]
+    lib.mmot_vgroup_destroy.restype = None
     lib.mmot_nccl_unique_id.argtypes = [vp]
     lib.mmot_nccl_unique_id.restype = ctypes.c_int
     lib.mmot_shard_range.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
@@ -114,6 +121,8 @@ def load_library():
     lib.mmot_info.restype = ctypes.c_int
     lib.mmot_launch_count.argtypes = [vp]
     lib.mmot_launch_count.restype = ctypes.c_int64
+    lib.mmot_fallback_count.argtypes = [vp]
+    lib.mmot_fallback_count.restype = ctypes.c_int64
     lib.mmot_profile_enable.argtypes = [vp, ctypes.c_int]
     lib.mmot_profile_enable.restype = ctypes.c_int
     dp = ctypes.POINTER(ctypes.c_double)
@@ -187,6 +196,31 @@ def compose_rank_affine(l: int, elems_all, world: int, rank: int):
     return fin, bin_
 
 
+class VirtualGroup:
+    """In-process group of `world` virtual shards on one device (mmot_vgroup_create): pass
+    ``shard=(rank, world, group)`` to Context from one host thread per rank."""
+
+    def __init__(self, world: int):
+        self._lib = load_library()
+        self.world = int(world)
+        g = ctypes.c_void_p()
+        st = self._lib.mmot_vgroup_create(self.world, ctypes.byref(g))
+        if st != 0:
+            raise MMOTError(st, self._lib.mmot_last_error(None).decode())
+        self._g = g
+
+    def close(self) -> None:
+        if getattr(self, "_g", None):
+            self._lib.mmot_vgroup_destroy(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
     """One MMOT problem shape (l, N, eta, grid) with its device workspace.
 
@@ -225,6 +259,15 @@ class Context:
             self.N_global = self.N
             lo, hi = shard_range(self.N, rank, world)
             self.N = hi - lo
+            if isinstance(uid, VirtualGroup):
+                st = self._lib.mmot_create_sharded_virtual(self.l, self.N_global, float(eta), _Grid(*self.grid),
+                                                           F64 if dtype == "f64" else F32, uid._g, int(rank),
+                                                           ctypes.byref(opts), ctypes.c_void_p(self.stream.cuda_stream),
+                                                           ctypes.byref(ctx))
+                if st != 0:
+                    raise MMOTError(st, self._lib.mmot_last_error(None).decode())
+                self._ctx = ctx
+                return
             idb = ctypes.create_string_buffer(bytes(uid), 128)
             st = self._lib.mmot_create_sharded(self.l, self.N_global, float(eta), _Grid(*self.grid),
                                                F64 if dtype == "f64" else F32, idb, int(rank), int(world),
@@ -285,6 +328,11 @@ class Context:
     @property
     def launches(self) -> int:
         return int(self._lib.mmot_launch_count(self._ctx))
+
+    @property
+    def fallbacks(self) -> int:
+        """Calls redone on the two-walk family after the single-walk precision guard tripped."""
+        return int(self._lib.mmot_fallback_count(self._ctx))
 
     # -- ABI calls ------------------------------------------------------------------------
     def init_uniform(self, u) -> None:

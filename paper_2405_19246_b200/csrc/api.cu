@@ -9,6 +9,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <vector>
 
 #include "../../include/mmot.h"
@@ -28,8 +30,8 @@ struct DevScalars {
     int fail_iter;
     int iters_done;
     int converged;
+    int guard;          // single-walk precision guard tripped (k_sw_guard)
     int flags[2 * mmot::kMaxL];
-    int pad;
     double resid;
     double res_acc;
     double W;
@@ -53,7 +55,7 @@ struct NcclApi {
     const char *(*GetErrorString)(nccl_result);
 };
 NcclApi g_nccl;
-constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+constexpr int kNcclInt32 = 2, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2;
 
 bool nccl_load() {
     if (g_nccl.tried) return g_nccl.ok;
@@ -73,6 +75,30 @@ bool nccl_load() {
 }
 
 }  // namespace
+
+// In-process group of `world` sharded contexts on one device (virtual shards, mmot_vgroup_create):
+// each context is driven by its own host thread on its own stream; a collective is a host barrier
+// plus cross-stream event waits and device copies -- no kernel ever waits on another.
+struct mmot_vgroup {
+    int world = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    int64_t gen = 0;
+    std::vector<const void *> src;
+    std::vector<cudaEvent_t> ready, done;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const int64_t g = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
 
 struct mmot_ctx {
     int l = 0;
@@ -99,6 +125,9 @@ struct mmot_ctx {
     int64_t nchp = 0;                       // sw: chains rounded up to 32 (transposed row length)
     double *mu_t[mmot::kMaxL] = {nullptr};  // sw: marginals in the chain-transposed layout
     double *out_t = nullptr;                // sw: marginal output in the chain-transposed layout
+    void *sw_end = nullptr;                 // sw: walked end state per chain ([nchunks][M] Dual-sized; guard)
+    mmot_ctx *fb = nullptr;                 // sw: two-walk context the guard falls back to (lazy)
+    int64_t fallbacks = 0;                  // sw: calls redone on the two-walk family
     // restricted next-update scan (single-walk contexts): second carry buffer + affine elements
     bool rx = false;
     void *rx_mem = nullptr;
@@ -110,6 +139,8 @@ struct mmot_ctx {
     int rank = 0, world = 1;
     int64_t N_global = 0, lo = 0;
     nccl_comm comm = nullptr;
+    mmot_vgroup *vg = nullptr;              // virtual shards: in-process group instead of NCCL
+    double *vg_tmp = nullptr;               // virtual shards: reduction result staging
     double *shard_mem = nullptr;            // agg_send [2*SZ], agg_all [world*2*SZ], rank_car [2*M] (Dual-sized)
     int exch_error = 0;
     // batched contexts (mmot_create_batched)
@@ -189,6 +220,7 @@ const char *mmot_strerror(mmot_status s) {
         case MMOT_ENCCL: return "NCCL error";
         case MMOT_ENOMEM: return "device allocation failed";
         case MMOT_EUNSUPPORTED: return "unsupported in this build";
+        case MMOT_EPRECISION: return "single-walk precision guard tripped";
     }
     return "unknown status";
 }
@@ -197,7 +229,9 @@ const char *mmot_last_error(const mmot_ctx *ctx) { return ctx ? ctx->err : g_err
 
 int mmot_version(void) { return (MMOT_VERSION_MAJOR << 16) | MMOT_VERSION_MINOR; }
 
-int64_t mmot_launch_count(const mmot_ctx *ctx) { return ctx ? ctx->launches : 0; }
+int64_t mmot_launch_count(const mmot_ctx *ctx) { return ctx ? ctx->launches + (ctx->fb ? ctx->fb->launches : 0) : 0; }
+
+int64_t mmot_fallback_count(const mmot_ctx *ctx) { return ctx ? ctx->fallbacks : 0; }
 
 mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t *nchains, int *kernel) {
     if (!ctx) { set_err(nullptr, "NULL context"); return MMOT_EINVAL; }
@@ -214,14 +248,17 @@ void mmot_destroy(mmot_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     else cudaDeviceSynchronize();
+    mmot_destroy(ctx->fb);
     cudaFree(ctx->ws);
     cudaFree(ctx->out_t);
+    cudaFree(ctx->sw_end);
     cudaFree(ctx->bat_mem);
     cudaFree(ctx->pts_mem);
     cudaFree(ctx->f32_mem);
     cudaFree(ctx->f32_stage);
     cudaFree(ctx->rx_mem);
     cudaFree(ctx->shard_mem);
+    cudaFree(ctx->vg_tmp);
     if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
     cudaFree(ctx->bat_int);
     cudaFree(ctx->bat_ptrs);
@@ -243,17 +280,28 @@ void mmot_destroy(mmot_ctx *ctx) {
 }
 
 static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype dt, const mmot_opts *opts,
-                                 void *cuda_stream, mmot_ctx **out, bool allow_persistent);
+                                 void *cuda_stream, mmot_ctx **out, bool allow_persistent, bool exact_chains = false);
 
 mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype dt, const mmot_opts *opts,
                         void *cuda_stream, mmot_ctx **out) {
     return create_single(l, N, eta, grid, dt, opts, cuda_stream, out, true);
 }
 
+// Single-walk chain length dividing N exactly (shards with a successor: padded points would add
+// spurious edge weights to the carries leaving the shard): the multiple of the slab length in
+// [lo, hi] closest to `want` that divides N, or 0 if there is none.
+static int64_t exact_chain_len(int64_t N, int64_t want, int64_t lo, int64_t hi, int64_t slab) {
+    int64_t best = 0;
+    for (int64_t P = std::max<int64_t>(slab, lo / slab * slab); P <= hi; P += slab)
+        if (N % P == 0 && (best == 0 || llabs(P - want) < llabs(best - want))) best = P;
+    return best;
+}
+
 // allow_persistent = false (shards of a sharded context): the persistent batched kernel has no
-// cross-rank exchange, so a shard always gets a scan-based kernel family.
+// cross-rank exchange, so a shard always gets a scan-based kernel family.  exact_chains = true
+// (shards with a successor): single-walk chains must tile the shard exactly (exact_chain_len).
 static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype dt, const mmot_opts *opts,
-                                 void *cuda_stream, mmot_ctx **out, bool allow_persistent) {
+                                 void *cuda_stream, mmot_ctx **out, bool allow_persistent, bool exact_chains) {
     if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
     *out = nullptr;
     if (l < 2 || l > 8) { set_err(nullptr, "l=%d outside [2,8]", l); return MMOT_EINVAL; }
@@ -319,6 +367,15 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
     if (c->opts.chunk > 0) {
         P = sw ? ((int64_t)c->opts.chunk + mmot::kSwSlab - 1) / mmot::kSwSlab * mmot::kSwSlab
                : std::min<int64_t>(c->opts.chunk, pmax);
+        if (sw && exact_chains && N % P != 0) {
+            P = exact_chain_len(N, P, slab, std::max<int64_t>(4 * P, 1024), slab);
+            if (P == 0) {
+                set_err(nullptr, "single-walk shard: no chain length (multiple of %d) divides the shard size %lld",
+                        slab, (long long)N);
+                delete c;
+                return MMOT_EUNSUPPORTED;
+            }
+        }
     } else {
         // one chain per lane, 2 waves of (SMs x resident warps x 32 lanes)
         int nsm = 148;
@@ -331,6 +388,17 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
         const int64_t Pcap = capd > 1e15 ? (int64_t)1e15 : (int64_t)capd;
         if (Psw > Pcap) Psw = (Pcap / slab) * slab;
         if (c->opts.kernel == MMOT_KERNEL_AUTO && NB <= 4 && Psw >= 64 && N >= 64LL * 148 * 8 * 32) sw = true;
+        if ((sw || c->opts.kernel == MMOT_KERNEL_SINGLE_WALK) && exact_chains && N % Psw != 0) {
+            const int64_t Pe = exact_chain_len(N, Psw, 64, std::min<int64_t>(Pcap, 2 * Psw + 64), slab);
+            if (Pe > 0) Psw = Pe;
+            else if (c->opts.kernel == MMOT_KERNEL_AUTO) sw = false;
+            else {
+                set_err(nullptr, "single-walk shard: no chain length (multiple of %d) divides the shard size %lld",
+                        slab, (long long)N);
+                delete c;
+                return MMOT_EUNSUPPORTED;
+            }
+        }
         if (sw) {
             P = std::max<int64_t>(slab, Psw);
         } else {
@@ -397,7 +465,8 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
         // chain-transposed internal vectors; zero-filled once so the tail of the last chain
         // (points >= N) holds phi = mu = 0 for the whole life of the context
         const size_t tb = (size_t)c->nchp * (size_t)c->P * sizeof(double);
-        bool ok = cudaMalloc(&c->out_t, tb) == cudaSuccess && cudaMemsetAsync(c->out_t, 0, tb, c->stream) == cudaSuccess;
+        bool ok = cudaMalloc(&c->out_t, tb) == cudaSuccess && cudaMemsetAsync(c->out_t, 0, tb, c->stream) == cudaSuccess &&
+                  cudaMalloc(&c->sw_end, (size_t)c->nchunks * M * sizeof(mmot::Dual)) == cudaSuccess;
         for (int qq = 0; qq < l && ok; ++qq)
             ok = cudaMalloc(&c->lin[qq], tb) == cudaSuccess && cudaMalloc(&c->mu_t[qq], tb) == cudaSuccess &&
                  cudaMemsetAsync(c->lin[qq], 0, tb, c->stream) == cudaSuccess &&
@@ -732,24 +801,89 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
 }
 
 // ---------------------------------------------------------------------------------------
-// Sharded contexts: all-gather of the whole-shard operators ([2][SZ] elements of elem_bytes)
-// on the context stream (called from inside the scan, between up-sweep and down-sweep).
+// Collectives of sharded contexts, on the context stream: NCCL across processes, or the
+// in-process virtual group (several shards on one device).  Every rank issues the same sequence.
+static int coll_fail(mmot_ctx *c, const char *what, int r) {
+    if (!c->exch_error) {
+        c->exch_error = r ? r : -1;
+        set_err(c, "%s: %s", what, c->vg ? "virtual group" : g_nccl.GetErrorString(r));
+    }
+    return c->exch_error;
+}
+
+// recv[r * n + i] = send_r[i] (n doubles per rank)
+static int coll_allgather(mmot_ctx *c, const double *send, double *recv, size_t n, cudaStream_t s) {
+    if (c->vg) {
+        mmot_vgroup *g = c->vg;
+        const int r = c->rank;
+        g->src[r] = send;
+        if (cudaEventRecord(g->ready[r], s) != cudaSuccess) return coll_fail(c, "cudaEventRecord", 0);
+        g->barrier();
+        for (int j = 0; j < g->world; ++j) {
+            cudaStreamWaitEvent(s, g->ready[j], 0);
+            cudaMemcpyAsync(recv + (size_t)j * n, g->src[j], n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+        }
+        cudaEventRecord(g->done[r], s);
+        g->barrier();  // every rank has read every send buffer before any rank overwrites its own
+        for (int j = 0; j < g->world; ++j)
+            if (j != r) cudaStreamWaitEvent(s, g->done[j], 0);
+        if (cudaGetLastError() != cudaSuccess) return coll_fail(c, "virtual all-gather", 0);
+        return 0;
+    }
+    const nccl_result rr = g_nccl.AllGather(send, recv, n, kNcclFloat64, c->comm, s);
+    return rr ? coll_fail(c, "ncclAllGather", rr) : 0;
+}
+
+// dev[0..n) <- sum (op 0, doubles) or max (op 1, ints) over the ranks, in place
+static int coll_allreduce(mmot_ctx *c, void *dev, int n, int op, cudaStream_t s) {
+    if (c->vg) {
+        mmot_vgroup *g = c->vg;
+        const int r = c->rank;
+        g->src[r] = dev;
+        if (cudaEventRecord(g->ready[r], s) != cudaSuccess) return coll_fail(c, "cudaEventRecord", 0);
+        g->barrier();
+        mmot::VPtrs vp{};
+        for (int j = 0; j < g->world; ++j) {
+            vp.p[j] = g->src[j];
+            cudaStreamWaitEvent(s, g->ready[j], 0);
+        }
+        int64_t dummy = 0;
+        mmot::launch_vreduce(vp, g->world, n, op, c->vg_tmp, s, &dummy);
+        c->launches += dummy;
+        cudaEventRecord(g->done[r], s);
+        g->barrier();
+        for (int j = 0; j < g->world; ++j)
+            if (j != r) cudaStreamWaitEvent(s, g->done[j], 0);
+        cudaMemcpyAsync(dev, c->vg_tmp, (size_t)n * (op == 0 ? sizeof(double) : sizeof(int)), cudaMemcpyDeviceToDevice, s);
+        if (cudaGetLastError() != cudaSuccess) return coll_fail(c, "virtual all-reduce", 0);
+        return 0;
+    }
+    const nccl_result rr = g_nccl.AllReduce(dev, dev, (size_t)n, op == 0 ? kNcclFloat64 : kNcclInt32,
+                                            op == 0 ? kNcclSum : kNcclMax, c->comm, s);
+    return rr ? coll_fail(c, "ncclAllReduce", rr) : 0;
+}
+
+// All-gather of the whole-shard operators ([2][SZ] elements) on the context stream (called from
+// inside the scan, between up-sweep and down-sweep).
 static void shard_exchange(void *vctx, size_t n, cudaStream_t s) {
     mmot_ctx *c = static_cast<mmot_ctx *>(vctx);
     const size_t SZ = (size_t)c->l * (1 << (c->l - 1));
-    const nccl_result r = g_nccl.AllGather(c->shard_mem, c->shard_mem + 2 * SZ * 2, n, kNcclFloat64, c->comm, s);
-    if (r != 0 && !c->exch_error) {
-        c->exch_error = r;
-        set_err(c, "ncclAllGather: %s", g_nccl.GetErrorString(r));
-    }
+    coll_allgather(c, c->shard_mem, c->shard_mem + 2 * SZ * 2, n, s);
 }
 
+static bool multi_rank(const mmot_ctx *c) { return c->sharded && c->world > 1; }
+
 // Sum a device double over the ranks (residual, cost) in place.
-static mmot_status shard_allreduce(mmot_ctx *c, double *dev) {
-    if (!c->sharded || c->world == 1) return MMOT_OK;
-    const nccl_result r = g_nccl.AllReduce(dev, dev, 1, kNcclFloat64, kNcclSum, c->comm, c->stream);
-    if (r != 0) { set_err(c, "ncclAllReduce: %s", g_nccl.GetErrorString(r)); return MMOT_ENCCL; }
-    return MMOT_OK;
+static mmot_status shard_allreduce(mmot_ctx *c, double *dev, int n = 1) {
+    if (!multi_rank(c)) return MMOT_OK;
+    return coll_allreduce(c, dev, n, 0, c->stream) ? MMOT_ENCCL : MMOT_OK;
+}
+
+// Max of the device ints stop, status, fail_iter (, iters_done, converged) over the ranks, so every
+// rank stops, and reports, together.
+static mmot_status shard_agree(mmot_ctx *c, int *first, int n) {
+    if (!multi_rank(c)) return MMOT_OK;
+    return coll_allreduce(c, first, n, 1, c->stream) ? MMOT_ENCCL : MMOT_OK;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -803,6 +937,10 @@ static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double
     p.status = &c->dsc->status;
     p.fail_iter = &c->dsc->fail_iter;
     p.iter = iter;
+    if (c->sw) {
+        p.sw_end = c->sw_end;
+        p.guard = &c->dsc->guard;
+    }
     return p;
 }
 
@@ -835,19 +973,43 @@ static mmot_status sync_report(mmot_ctx *c) {
     return MMOT_OK;
 }
 
+// Single-walk precision guard tripped (non-smooth scalings): the call is redone on a
+// two-walk context of the same problem (created on first use; fp64 internal vectors).  Sharded
+// contexts cannot switch families alone and report MMOT_EPRECISION on every rank instead.
+static mmot_status ensure_fallback(mmot_ctx *c) {
+    if (c->fb) return MMOT_OK;
+    mmot_opts o = c->opts;
+    o.kernel = MMOT_KERNEL_TWO_WALK;
+    o.chunk = 0;
+    mmot_status st = create_single(c->l, c->N, c->eta, c->grid, MMOT_F64, &o, c->stream, &c->fb, false);
+    if (st) set_err(c, "two-walk fallback context: %s", mmot_last_error(nullptr));
+    else c->fb->prof = c->prof;
+    return st;
+}
+
+static mmot_status guard_tripped(mmot_ctx *c) {
+    set_err(c, "single-walk precision guard: a walked suffix state lost accuracy (non-smooth scalings); "
+               "use MMOT_KERNEL_TWO_WALK");
+    return MMOT_EPRECISION;
+}
+
 static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters, double tol, void *const *u,
                                  mmot_report *rep) {
     const int l = c->l;
     mmot_status st = reset_scalars(c);
     if (st) return st;
-    // data checks (P:75 marginals are probability vectors; SPEC S:77 error vocabulary)
+    c->exch_error = 0;
+    // data checks (P:75 marginals are probability vectors; SPEC S:77 error vocabulary); a sharded
+    // context tests the mass of the whole marginal and all ranks adopt the worst status
     for (int q = 0; q < l; ++q) {
         CK(c, mmot::launch_check(mu[q], c->N, 0, &c->dsc->flags[q], &c->dsc->mass[q], c->stream, &c->launches));
         CK(c, mmot::launch_check(static_cast<const double *>(u[q]), c->N, c->opts.repr == MMOT_LOG ? 1 : 0,
                                  &c->dsc->flags[l + q], nullptr, c->stream, &c->launches));
     }
+    if ((st = shard_allreduce(c, c->dsc->mass, l))) return st;
     CK(c, mmot::launch_check_finish(c->dsc->flags, c->dsc->mass, 2 * l, l, &c->dsc->status, &c->dsc->stop,
                                     &c->dsc->fail_iter, c->stream, &c->launches));
+    if ((st = shard_agree(c, &c->dsc->stop, 3))) return st;
     // working scalings
     double *lin[mmot::kMaxL];
     for (int q = 0; q < l; ++q) {
@@ -916,13 +1078,30 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
         } else {
             CK(c, mmot::launch_sweep_done(t, &c->dsc->iters_done, &c->dsc->stop, c->stream, &c->launches));
         }
-        if (tol > 0 && !poll_pending && (t % 8 == 0)) {
+        if (tol > 0 && multi_rank(c) && t % 8 == 0) {
+            // sharded: the early exit must be collective -- agree on the stop flag, then read it
+            // synchronously, so every rank leaves the loop after the same sweep and issues the
+            // same collectives afterwards
+            if ((st = shard_agree(c, &c->dsc->stop, 3))) return st;
+            CK(c, cudaMemcpyAsync(c->hstop, &c->dsc->stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+            CK(c, cudaStreamSynchronize(c->stream));
+            if (*c->hstop) break;
+        } else if (tol > 0 && !multi_rank(c) && !poll_pending && (t % 8 == 0)) {
             CK(c, cudaMemcpyAsync(c->hstop, &c->dsc->stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
             CK(c, cudaEventRecord(c->poll_ev, c->stream));
             poll_pending = true;
         }
     }
     if (c->sw) {
+        // precision guard: decided before u is written, so a fallback restarts from the same input
+        if ((st = shard_agree(c, &c->dsc->stop, 6))) return st;
+        if ((st = sync_report(c))) return st;
+        if (c->hsc->guard && !c->hsc->status) {
+            if (c->sharded) return guard_tripped(c);
+            ++c->fallbacks;
+            if ((st = ensure_fallback(c))) return st;
+            return sinkhorn_impl(c->fb, mu, iters, tol, u, rep);
+        }
         for (int q = 0; q < l; ++q)
             CK(c, mmot::launch_from_t(c->lin[q], static_cast<double *>(u[q]), c->N, c->P, c->nchunks, c->nchp,
                                       c->opts.repr == MMOT_LOG ? 2 : 0, c->stream, &c->launches));
@@ -930,6 +1109,7 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
         for (int q = 0; q < l; ++q)
             CK(c, mmot::launch_log(c->lin[q], static_cast<double *>(u[q]), c->N, c->stream, &c->launches));
     }
+    if ((st = shard_agree(c, &c->dsc->stop, 6))) return st;
     st = sync_report(c);
     if (st) return st;
     if (c->exch_error) return MMOT_ENCCL;
@@ -996,11 +1176,24 @@ static mmot_status marginal_f64(mmot_ctx *c, int k, const void *const *u, void *
     }
     mmot_status st = reset_scalars(c);
     if (st) return st;
+    c->exch_error = 0;
     const double *lin[mmot::kMaxL];
     st = to_linear(c, u, lin);
     if (st) return st;
     Plan p = make_plan(c, k, lin, nullptr, c->sw ? c->out_t : static_cast<double *>(out), 0);
     CK(c, mmot::launch_product(p, mmot::MODE_MARG, c->stream, &c->launches, prof_events(c, mmot::MODE_MARG)));
+    if (c->exch_error) return MMOT_ENCCL;
+    if (c->sw) {
+        // precision guard (synchronises once)
+        if ((st = shard_agree(c, &c->dsc->stop, 6))) return st;
+        if ((st = sync_report(c))) return st;
+        if (c->hsc->guard) {
+            if (c->sharded) return guard_tripped(c);
+            ++c->fallbacks;
+            if ((st = ensure_fallback(c))) return st;
+            return marginal_f64(c->fb, k, u, out);
+        }
+    }
     if (c->sw)
         CK(c, mmot::launch_from_t(c->out_t, static_cast<double *>(out), c->N, c->P, c->nchunks, c->nchp, 0, c->stream,
                                   &c->launches));
@@ -1080,6 +1273,7 @@ mmot_status mmot_cost(mmot_ctx *c, const void *const *u, double *W) {
     }
     mmot_status st = reset_scalars(c);
     if (st) return st;
+    c->exch_error = 0;
     const double *lin[mmot::kMaxL];
     st = to_linear(c, u, lin);
     if (st) return st;
@@ -1091,8 +1285,16 @@ mmot_status mmot_cost(mmot_ctx *c, const void *const *u, double *W) {
                            &c->launches));
     st = shard_allreduce(c, &c->dsc->W);
     if (st) return st;
+    if ((st = shard_agree(c, &c->dsc->stop, 6))) return st;
     st = sync_report(c);
     if (st) return st;
+    if (c->exch_error) return MMOT_ENCCL;
+    if (c->sw && c->hsc->guard && !c->hsc->status) {
+        if (c->sharded) return guard_tripped(c);
+        ++c->fallbacks;
+        if ((st = ensure_fallback(c))) return st;
+        return mmot_cost(c->fb, u, W);
+    }
     *W = c->hsc->W;
     return (mmot_status)c->hsc->status;
 }
@@ -1130,7 +1332,9 @@ mmot_status mmot_profile_read(mmot_ctx *c, double *ms, double *ms_mode, int64_t 
 mmot_status mmot_init_uniform(mmot_ctx *c, void *const *u) {
     if (!c || !u) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
     cudaSetDevice(c->device);
-    const double v = c->opts.repr == MMOT_LOG ? -log((double)c->N) : 1.0 / (double)c->N;
+    // a shard starts from the global problem's 1/N
+    const double Ng = (double)(c->sharded ? c->N_global : c->N);
+    const double v = c->opts.repr == MMOT_LOG ? -log(Ng) : 1.0 / Ng;
     for (int q = 0; q < c->l; ++q) {
         if (!u[q]) { set_err(c, "u[%d] is NULL", q); return MMOT_EINVAL; }
         CK(c, mmot::launch_fill(static_cast<double *>(u[q]), v, c->N * c->batch, c->stream, &c->launches));
@@ -1175,12 +1379,13 @@ mmot_status mmot_compose_rank_affine(int l, const double *elems_all, int world, 
     return MMOT_OK;
 }
 
-mmot_status mmot_create_sharded(int l, int64_t N_global, double eta, mmot_grid grid, mmot_dtype dt,
-                                const void *nccl_unique_id, int rank, int world, const mmot_opts *opts,
-                                void *cuda_stream, mmot_ctx **out) {
+static mmot_status create_sharded(int l, int64_t N_global, double eta, mmot_grid grid, mmot_dtype dt,
+                                  const void *nccl_unique_id, mmot_vgroup *vg, int rank, int world,
+                                  const mmot_opts *opts, void *cuda_stream, mmot_ctx **out) {
     if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
     *out = nullptr;
-    if (!nccl_unique_id || world < 1 || rank < 0 || rank >= world) { set_err(nullptr, "bad rank/world/id"); return MMOT_EINVAL; }
+    if ((!nccl_unique_id && !vg) || world < 1 || rank < 0 || rank >= world) { set_err(nullptr, "bad rank/world/id"); return MMOT_EINVAL; }
+    if (vg && world != vg->world) { set_err(nullptr, "world=%d differs from the group's %d", world, vg->world); return MMOT_EINVAL; }
     int64_t lo, hi;
     mmot_shard_range(N_global, rank, world, &lo, &hi);
     if (N_global < world) { set_err(nullptr, "N_global=%lld < world=%d", (long long)N_global, world); return MMOT_ESHAPE; }
@@ -1189,7 +1394,7 @@ mmot_status mmot_create_sharded(int l, int64_t N_global, double eta, mmot_grid g
     mmot_grid g2{grid.x_min + lo * h, grid.x_min + (hi - 1) * h};
     if (hi - lo == 1) g2.x_max = g2.x_min + h;  // a 1-point shard keeps the global h below
     mmot_ctx *c = nullptr;
-    mmot_status st = create_single(l, hi - lo, eta, g2, dt, opts, cuda_stream, &c, false);
+    mmot_status st = create_single(l, hi - lo, eta, g2, dt, opts, cuda_stream, &c, false, rank + 1 < world);
     if (st) return st;
     c->h = h;
     for (int a = 0; a <= mmot::kMaxL; ++a) {
@@ -1204,27 +1409,32 @@ mmot_status mmot_create_sharded(int l, int64_t N_global, double eta, mmot_grid g
     c->grid = grid;
     const size_t SZ = (size_t)l * (1 << (l - 1));
     const size_t nd = (2 * SZ + (size_t)world * 2 * SZ + 2 * (1 << (l - 1))) * 2;  // Dual-sized
-    if (cudaMalloc(&c->shard_mem, nd * sizeof(double)) != cudaSuccess) {
+    if (cudaMalloc(&c->shard_mem, nd * sizeof(double)) != cudaSuccess ||
+        (vg && cudaMalloc(&c->vg_tmp, 16 * sizeof(double)) != cudaSuccess)) {
         set_err(c, "shard workspace allocation failed");
         snprintf(g_err, sizeof g_err, "%s", c->err);
         mmot_destroy(c);
         return MMOT_ENOMEM;
     }
-    if (!nccl_load()) {
-        set_err(c, "libnccl.so.2 not found");
-        snprintf(g_err, sizeof g_err, "%s", c->err);
-        mmot_destroy(c);
-        return MMOT_ENCCL;
-    }
-    ncclUniqueIdBytes id;
-    memcpy(id.internal, nccl_unique_id, sizeof id.internal);
-    const nccl_result r = g_nccl.CommInitRank(&c->comm, world, id, rank);
-    if (r != 0) {
-        set_err(c, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
-        snprintf(g_err, sizeof g_err, "%s", c->err);
-        c->comm = nullptr;
-        mmot_destroy(c);
-        return MMOT_ENCCL;
+    if (vg) {
+        c->vg = vg;
+    } else {
+        if (!nccl_load()) {
+            set_err(c, "libnccl.so.2 not found");
+            snprintf(g_err, sizeof g_err, "%s", c->err);
+            mmot_destroy(c);
+            return MMOT_ENCCL;
+        }
+        ncclUniqueIdBytes id;
+        memcpy(id.internal, nccl_unique_id, sizeof id.internal);
+        const nccl_result r = g_nccl.CommInitRank(&c->comm, world, id, rank);
+        if (r != 0) {
+            set_err(c, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+            snprintf(g_err, sizeof g_err, "%s", c->err);
+            c->comm = nullptr;
+            mmot_destroy(c);
+            return MMOT_ENCCL;
+        }
     }
     // Every rank must run the same collective sequence with the same payloads: the kernel family
     // and the scan mode, chosen from the local shard size, have to agree across ranks.
@@ -1233,7 +1443,7 @@ mmot_status mmot_create_sharded(int l, int64_t N_global, double eta, mmot_grid g
         std::vector<double> all((size_t)world);
         double *d = c->shard_mem;
         bool ok = cudaMemcpyAsync(d, &sig, sizeof sig, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
-                  g_nccl.AllGather(d, d + 1, 1, kNcclFloat64, c->comm, c->stream) == 0 &&
+                  coll_allgather(c, d, d + 1, 1, c->stream) == 0 &&
                   cudaMemcpyAsync(all.data(), d + 1, (size_t)world * sizeof(double), cudaMemcpyDeviceToHost,
                                   c->stream) == cudaSuccess &&
                   cudaStreamSynchronize(c->stream) == cudaSuccess;
@@ -1247,6 +1457,55 @@ mmot_status mmot_create_sharded(int l, int64_t N_global, double eta, mmot_grid g
     }
     *out = c;
     return MMOT_OK;
+}
+
+mmot_status mmot_create_sharded(int l, int64_t N_global, double eta, mmot_grid grid, mmot_dtype dt,
+                                const void *nccl_unique_id, int rank, int world, const mmot_opts *opts,
+                                void *cuda_stream, mmot_ctx **out) {
+    if (!nccl_unique_id) {
+        if (out) *out = nullptr;
+        set_err(nullptr, "nccl_unique_id is NULL");
+        return MMOT_EINVAL;
+    }
+    return create_sharded(l, N_global, eta, grid, dt, nccl_unique_id, nullptr, rank, world, opts, cuda_stream, out);
+}
+
+mmot_status mmot_vgroup_create(int world, mmot_vgroup **out) {
+    if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
+    *out = nullptr;
+    if (world < 1 || world > mmot::kMaxWorld) { set_err(nullptr, "world=%d outside [1,%d]", world, mmot::kMaxWorld); return MMOT_EINVAL; }
+    mmot_vgroup *g = new mmot_vgroup();
+    g->world = world;
+    g->src.assign((size_t)world, nullptr);
+    g->ready.assign((size_t)world, nullptr);
+    g->done.assign((size_t)world, nullptr);
+    for (int r = 0; r < world; ++r)
+        if (cudaEventCreateWithFlags(&g->ready[r], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&g->done[r], cudaEventDisableTiming) != cudaSuccess) {
+            set_err(nullptr, "cudaEventCreate failed");
+            mmot_vgroup_destroy(g);
+            return MMOT_ECUDA;
+        }
+    *out = g;
+    return MMOT_OK;
+}
+
+void mmot_vgroup_destroy(mmot_vgroup *g) {
+    if (!g) return;
+    for (cudaEvent_t e : g->ready) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : g->done) if (e) cudaEventDestroy(e);
+    delete g;
+}
+
+mmot_status mmot_create_sharded_virtual(int l, int64_t N_global, double eta, mmot_grid grid, mmot_dtype dt,
+                                        mmot_vgroup *group, int rank, const mmot_opts *opts, void *cuda_stream,
+                                        mmot_ctx **out) {
+    if (!group) {
+        if (out) *out = nullptr;
+        set_err(nullptr, "group is NULL");
+        return MMOT_EINVAL;
+    }
+    return create_sharded(l, N_global, eta, grid, dt, nullptr, group, rank, group->world, opts, cuda_stream, out);
 }
 
 }  // extern "C"

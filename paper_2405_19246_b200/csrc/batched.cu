@@ -843,23 +843,19 @@ static cudaError_t bat_run(const BatchArgs &a, int what, cudaStream_t s, int64_t
     const BPlan bp = to_bplan(a);
     const unsigned grid = (unsigned)((a.slots + kBWarps - 1) / kBWarps);
     const size_t sm = bat_smem<NB>();
-    static bool attr[3] = {false, false, false};
     switch (what) {
         case 0:
-            if (!attr[0]) {
-                cudaFuncSetAttribute(k_bat_sinkhorn<NB, PTS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                cudaFuncSetAttribute(k_bat_sinkhorn<NB, PTS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                attr[0] = true;
-            }
+            smem_attr((const void *)k_bat_sinkhorn<NB, PTS, false>, sm);
+            smem_attr((const void *)k_bat_sinkhorn<NB, PTS, true>, sm);
             if (a.tol > 0) k_bat_sinkhorn<NB, PTS, true><<<grid, kBWarps * 32, sm, s>>>(bp);
             else k_bat_sinkhorn<NB, PTS, false><<<grid, kBWarps * 32, sm, s>>>(bp);
             break;
         case 1:
-            if (!attr[1]) { cudaFuncSetAttribute(k_bat_product<NB, double, MODE_MARG, PTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[1] = true; }
+            smem_attr((const void *)k_bat_product<NB, double, MODE_MARG, PTS>, sm);
             k_bat_product<NB, double, MODE_MARG, PTS><<<grid, kBWarps * 32, sm, s>>>(bp);
             break;
         default:
-            if (!attr[2]) { cudaFuncSetAttribute(k_bat_product<NB, Dual, MODE_COST, PTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[2] = true; }
+            smem_attr((const void *)k_bat_product<NB, Dual, MODE_COST, PTS>, sm);
             k_bat_product<NB, Dual, MODE_COST, PTS><<<grid, kBWarps * 32, sm, s>>>(bp);
             break;
     }

@@ -18,6 +18,7 @@ constexpr int kGroup = 32;  // operators per group of the hierarchical scan when
 // NB >= 4 composes a group sequentially in one thread (an op_compose of 2^NB-state operators is
 // heavy): smaller groups shorten that serial chain at the price of more levels.
 __host__ __device__ constexpr int group_of(int NB) { return NB <= 3 ? 32 : 8; }
+constexpr double kSwGuardTol = 1e-11;  // single-walk guard: max relative error of a walked end state
 constexpr double kSwBound = 1.0;   // max P * max_a a(l-a) * h/eta for the single-walk kernels      // operators composed per thread in the hierarchical scan
 constexpr int kMaxLevels = 8;
 
@@ -64,6 +65,11 @@ struct Plan {
     int *status;                     // device status (mmot_status) of the run
     int *fail_iter;                  // device: sweep index of the first failure
     int iter;                        // current sweep index (for fail_iter)
+    // single-walk precision guard: every chain stores its walked end state (sw_end, [nchunks][M] in
+    // T units) and k_sw_guard compares it with the exact inclusive suffix carry of the next chain;
+    // a componentwise relative difference above kSwGuardTol sets *guard
+    void *sw_end = nullptr;
+    int *guard = nullptr;
     const double *lam = nullptr;     // non-uniform grid: per-edge decays [nchunks P + 1] (null: uniform)
     const double *hx = nullptr;      // non-uniform grid: edge lengths (cost duals)
 };
@@ -128,6 +134,19 @@ cudaError_t launch_batched(const BatchArgs &a, int what, cudaStream_t s, int64_t
 // u: DEVICE array of l device pointers; import: u -> (phit, E), else (phit, E) -> u
 cudaError_t launch_bat_convert(const BatchArgs &a, void *const *u_dev_ptrs, int import, int is_log, cudaStream_t s,
                                int64_t *launches);
+
+// Allow `bytes` of dynamic shared memory for kernel `func` on the CURRENT device.  The attribute is
+// per device, so it is set once per (kernel, device, size) (thread-safe cache).
+void smem_attr(const void *func, size_t bytes);
+
+// In-process collectives of virtual shard groups (several sharded contexts on one device, each
+// driven by its own host thread and stream): out[i] = op_r src[r][i], op 0 = sum (double),
+// op 1 = max (int).
+constexpr int kMaxWorld = 16;
+struct VPtrs {
+    const void *p[kMaxWorld];
+};
+cudaError_t launch_vreduce(const VPtrs &src, int world, int n, int op, void *out, cudaStream_t s, int64_t *launches);
 
 // Elementwise helpers.
 // fp32 <-> fp64 (to_f64: float in -> double out, else double in -> float out)

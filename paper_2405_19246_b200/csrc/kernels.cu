@@ -19,6 +19,10 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <mutex>
+#include <set>
+#include <tuple>
+
 #include "internal.h"
 #include "walk.cuh"
 
@@ -1222,6 +1226,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
                         reinterpret_cast<double &>(F[U | NEW]) = lane == 0 ? cin[U] : up;  // exclusive prefix
                     } else {
                         reinterpret_cast<double &>(B[U | NEW]) = out[U];                   // inclusive suffix
+                        // complete this chain's carry in car_bi (read by the precision guard)
+                        if (live && p.guard) static_cast<double *>(p.car_bi)[c * M + (U | NEW)] = out[U];
                     }
                 }
             }
@@ -1331,6 +1337,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
     }
     if (bad && live) raise_status(p, 6 /*EOVERFLOW*/);
     if ((MODE == MODE_RES || MODE == MODE_COST) && live) p.partial[c] = acc;
+    if (live && p.sw_end) {
+        T *e = static_cast<T *>(p.sw_end) + c * M;
+#pragma unroll
+        for (int R = 0; R < M; ++R) e[R] = B[R];
+    }
     if constexpr (NEXT) {
         if (live)
             opx_store<NB, T>(Gx, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
@@ -1640,12 +1651,7 @@ template <int NB, typename T, int MODE, bool NEXT, bool FULL, bool PTS = false>
 static void launch_apply_range(const Plan &p, int64_t cbeg, int64_t cend, cudaStream_t s, int64_t *launches) {
     if (cend <= cbeg) return;
     const size_t sm = apply_smem<NB, MODE>();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_chunk_apply<NB, T, MODE, NEXT, FULL, PTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sm);
-        attr = true;
-    }
+    smem_attr((const void *)k_chunk_apply<NB, T, MODE, NEXT, FULL, PTS>, sm);
     const int tpb = kWarpsPerCta * 32;
     const int64_t nb = (cend - cbeg + tpb - 1) / tpb;
     k_chunk_apply<NB, T, MODE, NEXT, FULL, PTS><<<(unsigned)nb, tpb, sm, s>>>(p, cbeg, cend);
@@ -1658,14 +1664,50 @@ template <int NB, int MODE, bool NEXT>
 static void launch_apply_tm(const Plan &p, int64_t cbeg, int64_t cend, cudaStream_t s, int64_t *launches) {
     if (cend <= cbeg) return;
     const size_t sm = apply_smem<NB, MODE>();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_chunk_apply_tm<NB, MODE, NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        attr = true;
-    }
+    smem_attr((const void *)k_chunk_apply_tm<NB, MODE, NEXT>, sm);
     const int tpb = kWarpsPerCta * 32;
     const int64_t nb = (cend - cbeg + tpb - 1) / tpb;
     k_chunk_apply_tm<NB, MODE, NEXT><<<(unsigned)nb, tpb, sm, s>>>(p, cbeg, cend);
+    ++*launches;
+}
+
+// Single-walk precision guard.  The inverse step B_{m+1} = D^-1 place_m^-1(B_m) subtracts; its
+// rounding errors grow like the suffix states' relative condition, which the forward (positive)
+// recurrence cannot shrink, so the componentwise relative error of any interior suffix state is
+// bounded by that of the walked END state (up to rounding), which is compared here with the exact
+// inclusive suffix carry of the next chain (the scan's car_bi).  Components whose exact value is 0
+// (a marginal zero on the whole remaining suffix) carry only harmless rounding residue and are
+// skipped.  last: exact end state of the last chain (nullptr: e_empty); skip_last: do not check it.
+template <typename T>
+__global__ void k_sw_guard(const T *__restrict__ end, const T *__restrict__ cbi, const T *last, int skip_last, int M,
+                           int64_t n, const int *stop, int *guard) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n || *stop) return;
+    constexpr int K = sizeof(T) / sizeof(double);
+    const double *x = reinterpret_cast<const double *>(end + c * M);
+    const double *y = c + 1 < n ? reinterpret_cast<const double *>(cbi + (c + 1) * M)
+                                : reinterpret_cast<const double *>(last);
+    if (c + 1 >= n && skip_last) return;
+    bool bad = false;
+    for (int i = 0; i < M * K; ++i) {
+        const double ex = y ? y[i] : (i == 0 ? 1.0 : 0.0);
+        if (ex != 0.0) bad |= !(fabs(x[i] - ex) <= kSwGuardTol * fabs(ex));
+    }
+    if (bad) atomicOr(guard, 1);
+}
+
+template <int NB, typename T>
+static void launch_sw_guard(const Plan &p, cudaStream_t s, int64_t *launches) {
+    constexpr int M = 1 << NB;
+    const T *last = nullptr;
+    int skip_last = 0;
+    if (p.exch && p.rank + 1 < p.world) {
+        if (p.rx_scan) skip_last = 1;  // the rank carry holds only the new parts (affine scan)
+        else last = static_cast<const T *>(p.rank_car) + M;
+    }
+    k_sw_guard<T><<<(unsigned)((p.nchunks + 255) / 256), 256, 0, s>>>(
+        static_cast<const T *>(p.sw_end), static_cast<const T *>(p.car_bi), last, skip_last, M, p.nchunks, p.stop,
+        p.guard);
     ++*launches;
 }
 
@@ -1677,11 +1719,7 @@ static constexpr size_t sw_smem() {
 template <int NB, typename T, int MODE, bool NEXT, bool NXR = false>
 static void launch_sw(const Plan &p, cudaStream_t s, int64_t *launches) {
     constexpr size_t sm = sw_smem<NB, MODE>();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_sw_apply<NB, T, MODE, NEXT, NXR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        attr = true;
-    }
+    smem_attr((const void *)k_sw_apply<NB, T, MODE, NEXT, NXR>, sm);
     const int tpb = kWarpsPerCta * 32;
     const int64_t nb = (p.nchp + tpb - 1) / tpb;
     k_sw_apply<NB, T, MODE, NEXT, NXR><<<(unsigned)nb, tpb, sm, s>>>(p);
@@ -1722,13 +1760,15 @@ static void launch_apply(const Plan &p, int64_t /*nb*/, int /*tpb*/, cudaStream_
     }
     if (p.sw) {
         if constexpr (NB <= 4) {
+            bool done = false;
             if constexpr (NEXT && MODE == MODE_UPD && sizeof(T) == sizeof(double) && NB >= 2) {
                 if (p.nxr) {
                     launch_sw<NB, T, MODE, false, true>(p, s, launches);
-                    return;
+                    done = true;
                 }
             }
-            launch_sw<NB, T, MODE, NEXT>(p, s, launches);
+            if (!done) launch_sw<NB, T, MODE, NEXT>(p, s, launches);
+            if (p.guard && p.sw_end) launch_sw_guard<NB, T>(p, s, launches);
         }
         return;
     }
@@ -1768,11 +1808,7 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
     if (with_ops && p.sw) {
         if constexpr (NB <= 4) {
             constexpr size_t sm = (size_t)kWarpsPerCta * kSwStages * NB * kSwS * 32 * sizeof(double);
-            static bool attr_sw = false;
-            if (!attr_sw) {
-                cudaFuncSetAttribute(k_sw_ops<NB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                attr_sw = true;
-            }
+            smem_attr((const void *)k_sw_ops<NB, T>, sm);
             k_sw_ops<NB, T><<<(unsigned)((p.nchp + tpb - 1) / tpb), tpb, sm, s>>>(p);
             ++*launches;
         }
@@ -1784,12 +1820,8 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
         }
     } else if (with_ops) {
         const size_t sm = ops_smem<NB, T>();
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_chunk_ops<NB, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            cudaFuncSetAttribute(k_chunk_ops<NB, T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr = true;
-        }
+        smem_attr((const void *)k_chunk_ops<NB, T>, sm);
+        smem_attr((const void *)k_chunk_ops<NB, T, true>, sm);
         if (p.lam) k_chunk_ops<NB, T, true><<<(unsigned)nb, tpb, sm, s>>>(p);
         else k_chunk_ops<NB, T><<<(unsigned)nb, tpb, sm, s>>>(p);
         ++*launches;
@@ -1933,6 +1965,36 @@ cudaError_t launch_product(const Plan &p, int mode, cudaStream_t s, int64_t *lau
 // ---------------------------------------------------------------------------------------
 // Small kernels.
 // ---------------------------------------------------------------------------------------
+void smem_attr(const void *func, size_t bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void *, int, size_t>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (done.insert(std::make_tuple(func, dev, bytes)).second)
+        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// In-process group reduction (virtual shards): out[i] = op over r of src[r][i].
+__global__ void k_vreduce(VPtrs src, int world, int n, int op, void *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (op == 0) {
+        double acc = 0.0;
+        for (int r = 0; r < world; ++r) acc += static_cast<const double *>(src.p[r])[i];
+        static_cast<double *>(out)[i] = acc;
+    } else {
+        int acc = static_cast<const int *>(src.p[0])[i];
+        for (int r = 1; r < world; ++r) acc = max(acc, static_cast<const int *>(src.p[r])[i]);
+        static_cast<int *>(out)[i] = acc;
+    }
+}
+
+cudaError_t launch_vreduce(const VPtrs &src, int world, int n, int op, void *out, cudaStream_t s, int64_t *launches) {
+    k_vreduce<<<(n + 127) / 128, 128, 0, s>>>(src, world, n, op, out);
+    ++*launches;
+    return cudaGetLastError();
+}
 __global__ void __launch_bounds__(1024) k_sum(const double *partial, int64_t n, double *out, double scale,
                                               int accumulate, const int *stop) {
     __shared__ double sh[1024];

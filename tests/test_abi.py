@@ -84,3 +84,18 @@ def test_points_argument_errors(lib):
     assert lib.mmot_create_points(3, 3, 0.1, None, 0, None, None, ctypes.byref(ctx)) == 1
     ok = (ctypes.c_double * 3)(0.0, 0.2, 1.0)
     assert lib.mmot_create_points(3, 3, -1.0, ok, 0, None, None, ctypes.byref(ctx)) == 1   # eta <= 0
+
+
+def test_virtual_group_argument_errors(lib):
+    """mmot_vgroup_create / mmot_create_sharded_virtual validate on the host (no device work)."""
+    g = ctypes.c_void_p()
+    assert lib.mmot_vgroup_create(0, ctypes.byref(g)) == 1
+    assert lib.mmot_vgroup_create(17, ctypes.byref(g)) == 1
+    assert g.value is None
+    lib.mmot_vgroup_destroy(None)
+    ctx = ctypes.c_void_p()
+    assert lib.mmot_create_sharded_virtual(4, 100, 0.1, mm._Grid(0.0, 1.0), 0, None, 0, None, None,
+                                           ctypes.byref(ctx)) == 1
+    assert ctx.value is None
+    assert lib.mmot_fallback_count(None) == 0
+    assert lib.mmot_strerror(11) == b"single-walk precision guard tripped"

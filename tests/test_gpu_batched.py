@@ -193,3 +193,65 @@ def test_batched_data_errors_per_instance(bad, code):
         ctx.sinkhorn(_planes([mus[:, q, :] for q in range(l)]), 3, 0.0, u)
     ctx.close()
     assert ei.value.name == code
+
+
+@pytest.mark.slow
+def test_batched_c5_full_run_stratified_instances():
+    """C5 as the bench runs it: the full batch (8192 x (l=5, N=4096), per-instance eta ~ logU[1e-3,
+    1e-1]) for the full T = 300 sweeps, then 8 stratified instances -- the median-eta instance of
+    each of 8 equal log-eta strata -- against the log-domain oracle (region chains, P:1062-1125,
+    in a pure log domain: Remark 1's purpose), run in parallel on the host cores:
+    marginals to 1e-10 L1-relative, W to 1e-10, log phi to 1e-9 relative.  This covers the lazy
+    chain-exponent renormalisation at |log phi| ~ 1.8e3 (eta = 1e-3) over a whole run."""
+    import concurrent.futures as cf
+    cfg = mmot_inputs.CONFIGS["C5"]
+    l, N, B, T = cfg.l, cfg.N, cfg.batch, cfg.iters
+    etas = mmot_inputs.c5_etas(B)
+    mus_all = mmot_inputs.c5_batch_marginals(0, B, N, l)          # [l][B][N]
+    mu_d = [torch.from_numpy(mus_all[q]).to(DEV) for q in range(l)]
+    ctx = mm.Context(l, N, [float(e) for e in etas], batch=B)
+    u = [torch.empty((B, N), dtype=torch.float64, device=DEV) for _ in range(l)]
+    ctx.init_uniform(u)
+    rep = ctx.sinkhorn(mu_d, T, 0.0, u)
+    assert rep["status"] == 0 and rep["iters_done"] == T
+    le = np.log10(etas)
+    edges = np.linspace(-3.0, -1.0, 9)
+    picks = []
+    for s in range(8):
+        idx = np.nonzero((le >= edges[s]) & (le <= edges[s + 1]))[0]
+        idx = idx[np.argsort(le[idx])]
+        picks.append(int(idx[len(idx) // 2]))
+    g = np.stack([x[picks].cpu().numpy() for x in u])               # [l][8][N]
+    marg = [ctx.marginal(k, u)[picks].cpu().numpy() for k in range(l)]
+    Wb = ctx.cost(u)
+    ctx.close()
+    h = mmot_inputs.grid_h(N)
+
+    def ref(b):
+        eta = float(etas[b])
+        g_ref, _, _ = osk.sinkhorn(mus_all[:, b, :], h, eta, T, domain="log")
+        lw = np.array([-(a * (l - a)) * h / eta for a in range(l + 1)])
+        m_ref = [np.exp(g_ref[k] + regions.marginal_product_log(list(g_ref), k, lw)) for k in range(l)]
+        return g_ref, m_ref
+
+    with cf.ThreadPoolExecutor(max_workers=len(picks)) as ex:   # ctypes releases the GIL
+        refs = list(ex.map(ref, picks))
+    n_cost = 0
+    for j, b in enumerate(picks):
+        g_ref, m_ref = refs[j]
+        fin = np.isfinite(g_ref)
+        assert np.max(np.abs(g[:, j, :][fin] - g_ref[fin]) / np.maximum(1.0, np.abs(g_ref[fin]))) <= 1e-9, b
+        for k in range(l):
+            assert np.abs(marg[k][j] - m_ref[k]).sum() / np.abs(m_ref[k]).sum() <= RTOL, (b, k)
+        # W of the plan with the oracle's scalings, gauge-shifted towards fp64 range (A16:
+        # sum_q c_q = 0 leaves the plan unchanged); the plain-fp64 cost oracle applies where every
+        # shifted scaling is representable (the larger-eta strata)
+        c = g_ref.max(axis=1)
+        c[-1] -= c.sum()
+        with np.errstate(over="ignore"):
+            phis = np.exp(g_ref - c[:, None])
+        if np.all(np.isfinite(phis)) and phis.max() < 1e250:
+            W_ref = osk.cost(phis, h, float(etas[b]))
+            assert abs(Wb[b] - W_ref) <= RTOL * abs(W_ref), (b, Wb[b], W_ref)
+            n_cost += 1
+    assert n_cost >= 3, n_cost

@@ -57,10 +57,12 @@ def test_single_walk_marginal_parity(l, N, chunk):
     assert ctx.info["kernel"] == "single_walk"
     u = _dev(phis)
     got = [ctx.marginal(k, u).cpu().numpy() for k in range(l)]
+    fb = ctx.fallbacks
     ctx.close()
     want = _oracle_marginals(phis, h, eta)
     for k in range(l):
         assert _rel(got[k], want[k]) <= RTOL, (l, N, chunk, k)
+    assert fb == 0, fb   # U[0.1, 1] scalings: the single-walk states stay accurate
 
 
 @pytest.mark.parametrize("l", [3, 4])
@@ -98,6 +100,101 @@ def test_single_walk_sinkhorn_lockstep(l, N, chunk, T):
     for k in range(l):
         assert np.abs(marg[k] - m_ref[k]).sum() / np.abs(m_ref[k]).sum() <= RTOL, k
     assert np.max(np.abs(g - g_ref)) <= 1e-9
+
+
+def _zero_runs(x, rng, runs, length):
+    x = x.copy()
+    for _ in range(runs):
+        a = int(rng.integers(0, len(x) - length))
+        x[a:a + length] = 0.0
+    return x
+
+
+@pytest.mark.parametrize("l", [3, 4, 5])
+def test_single_walk_zero_runs_sinkhorn_lockstep(l):
+    """Marginals with zero runs (several runs longer than a chain, and a zero tail): the scalings of
+    those marginals are exactly 0 there, so the inverse step subtracts placed terms
+    that vanish on the rest of the chain.  Lockstep with the oracle at 1e-10 and no fallback (the
+    walked states stay accurate: the stability bound also bounds the growth across a run)."""
+    N, chunk, T = 20000, 64, 4
+    h = mmot_inputs.grid_h(N)
+    eta = _eta_for(l, N, chunk)
+    rng = np.random.default_rng(4242 + l)
+    mus = np.stack(mmot_inputs.random_marginals(610 + l, l, N))
+    for q in range(l):
+        mus[q] = _zero_runs(mus[q], rng, 4, 3 * chunk + 5)
+    mus[0, N - 700:] = 0.0
+    mus /= mus.sum(axis=1, keepdims=True)
+    ctx = mm.Context(l, N, eta, repr="linear", chunk=chunk, kernel="single_walk")
+    u = [torch.full((N,), 1.0 / N, dtype=torch.float64, device=DEV) for _ in range(l)]
+    rep = ctx.sinkhorn(_dev(mus), T, 0.0, u)
+    assert rep["status"] == 0 and rep["iters_done"] == T
+    marg = np.stack([ctx.marginal(k, u).cpu().numpy() for k in range(l)])
+    phi = np.stack([x.cpu().numpy() for x in u])
+    fb = ctx.fallbacks
+    ctx.close()
+    phi_ref, _, _ = osk.sinkhorn(mus, h, eta, T, domain="plain")
+    m_ref = osk.marginals(phi_ref, h, eta)
+    for k in range(l):
+        assert np.abs(marg[k] - m_ref[k]).sum() / np.abs(m_ref[k]).sum() <= RTOL, k
+        assert np.array_equal(phi[k] == 0.0, phi_ref[k] == 0.0), k
+        nz = phi_ref[k] > 0
+        assert np.max(np.abs(phi[k][nz] - phi_ref[k][nz]) / phi_ref[k][nz]) <= 1e-9, k
+    assert fb == 0, fb
+
+
+@pytest.mark.parametrize("l", [3, 4])
+def test_single_walk_huge_dynamic_range_guard(l):
+    """Scalings spanning 1e+-50 between neighbouring points (i.i.d. log-uniform): the inverse step's
+    subtraction cancels catastrophically, the precision guard (end state vs the next chain's exact
+    carry) trips and the call is redone on the two-walk family -- the results still match the oracle
+    at 1e-10 (products elementwise, W, and a Sinkhorn solve)."""
+    N, chunk = 5000, 40
+    h = mmot_inputs.grid_h(N)
+    eta = _eta_for(l, N, chunk)
+    rng = np.random.default_rng(77 + l)
+    phis = 10.0 ** rng.uniform(-50, 50, (l, N))
+    ctx = mm.Context(l, N, eta, repr="linear", chunk=chunk, kernel="single_walk")
+    u = _dev(phis)
+    got = [ctx.marginal(k, u).cpu().numpy() for k in range(l)]
+    assert ctx.fallbacks >= 1
+    W = ctx.cost(u)
+    want = _oracle_marginals(phis, h, eta)
+    for k in range(l):
+        assert _rel(got[k], want[k]) <= RTOL, k
+    w = regions.edge_weights(l, h, eta)
+    _, jh = regions.marginal_product(list(phis), l - 1, w, want_hat=True)
+    W_ref = h * float(np.dot(phis[l - 1], jh))
+    assert abs(W - W_ref) <= RTOL * abs(W_ref)
+    # Sinkhorn with marginals spanning 1e-50..1 (so do the scalings)
+    mus = 10.0 ** rng.uniform(-50, 0, (l, N))
+    mus /= mus.sum(axis=1, keepdims=True)
+    v = [torch.full((N,), 1.0 / N, dtype=torch.float64, device=DEV) for _ in range(l)]
+    n0 = ctx.fallbacks
+    rep = ctx.sinkhorn(_dev(mus), 3, 0.0, v)
+    assert rep["status"] == 0 and ctx.fallbacks == n0 + 1
+    phi = np.stack([x.cpu().numpy() for x in v])
+    ctx.close()
+    phi_ref, _, _ = osk.sinkhorn(mus, h, eta, 3, domain="plain")
+    assert np.max(np.abs(phi - phi_ref) / phi_ref) <= 1e-9
+
+
+@pytest.mark.parametrize("l", [3, 4])
+def test_single_walk_smooth_large_range(l):
+    """log phi a smooth wave of amplitude 115 (phi spanning 1e+-50 across the grid, smoothly):
+    single-walk parity at 1e-10 (with or without the guard's fallback)."""
+    N, chunk = 20000, 64
+    h = mmot_inputs.grid_h(N)
+    eta = _eta_for(l, N, chunk)
+    x = np.arange(N) / (N - 1)
+    phis = np.stack([np.exp(115.0 * np.sin(2 * np.pi * (3 + q) * x + q)) for q in range(l)])
+    ctx = mm.Context(l, N, eta, repr="linear", chunk=chunk, kernel="single_walk")
+    u = _dev(phis)
+    got = [ctx.marginal(k, u).cpu().numpy() for k in range(l)]
+    ctx.close()
+    want = _oracle_marginals(phis, h, eta)
+    for k in range(l):
+        assert _rel(got[k], want[k]) <= RTOL, k
 
 
 def test_auto_selects_single_walk_for_c4_shape():
@@ -147,3 +244,54 @@ def test_c4_full_size_sweeps_match_two_walk_and_fix_last_marginal():
     for k in range(l):
         d = float((g["auto"][k] - g["two_walk"][k]).abs().max())
         assert d <= 1e-9, (k, d)
+
+
+@pytest.mark.slow
+def test_c4_full_size_sweeps_match_oracle():
+    """C4 at its full size (l=4, N=1e8, eta=1e-4) through mmot_sinkhorn in exactly the bench's
+    launch configuration (auto: single-walk, restricted next-update scan, 4 scan levels), 2 sweeps
+    from the paper's init, then all l marginals and W through the library -- each
+    compared with the fp64 CPU oracle (oracle/regions.c region chains, 2 plain Gauss-Seidel sweeps,
+    P:1029-1035) on every element: 1e-10 L1-relative per marginal, 1e-10 relative for W, and
+    log phi to 1e-9.  The oracle takes ~3-4 min on the host (8 sequential products, then the l
+    marginals and the cost product on parallel threads)."""
+    import concurrent.futures as cf
+    cfg = mmot_inputs.CONFIGS["C4"]
+    l, N, eta, T = cfg.l, cfg.N, cfg.eta, 2
+    h = mmot_inputs.grid_h(N)
+    mus = mmot_inputs.make_marginals("C4", 0)
+    mu_d = _dev(mus)
+    ctx = mm.Context(l, N, eta, repr="log")
+    info = ctx.info
+    assert info["kernel"] == "single_walk"
+    u = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in range(l)]
+    ctx.init_uniform(u)
+    rep = ctx.sinkhorn(mu_d, T, 0.0, u)
+    assert rep["status"] == 0 and rep["iters_done"] == T
+    del mu_d
+    m_gpu = [ctx.marginal(k, u).cpu().numpy() for k in range(l)]
+    W_gpu = ctx.cost(u)
+    g_gpu = [x.cpu().numpy() for x in u]
+    assert ctx.fallbacks == 0   # the precision guard held: these are single-walk results
+    ctx.close()
+    del u
+    torch.cuda.empty_cache()
+    # oracle: plain fp64 Gauss-Seidel sweeps (C4 stays representable, SURVEY App. A)
+    w = regions.edge_weights(l, h, eta)
+    phis = [np.full(N, 1.0 / N) for _ in range(l)]
+    for _ in range(T):
+        for k in range(l):
+            phis[k] = mus[k] / regions.marginal_product(phis, k, w)
+    for k in range(l):
+        assert np.max(np.abs(g_gpu[k] - np.log(phis[k]))) <= 1e-9, k
+    del g_gpu
+    with cf.ThreadPoolExecutor(max_workers=l + 1) as ex:   # ctypes releases the GIL
+        fut = [ex.submit(regions.marginal_product, phis, k, w) for k in range(l)]
+        fut_c = ex.submit(regions.marginal_product, phis, l - 1, w, True)
+        for k in range(l):
+            m_ref = phis[k] * fut[k].result()
+            assert np.abs(m_gpu[k] - m_ref).sum() / np.abs(m_ref).sum() <= RTOL, k
+            del m_ref
+        _, jh = fut_c.result()
+    W_ref = h * float(np.dot(phis[l - 1], jh))
+    assert abs(W_gpu - W_ref) <= RTOL * abs(W_ref), (W_gpu, W_ref)

@@ -127,3 +127,49 @@ def test_tol_stop_rule():
     assert res <= 1e-9
     _, t2, res2 = sinkhorn.sinkhorn(mus, h, eta, t - 1, tol=1e-9)
     assert res2 > 1e-9
+
+
+@pytest.mark.parametrize("eps", [0.5, 0.1, 0.03])
+def test_residual_pinned_to_algorithm4_line7(eps):
+    """The residual (oracle/sinkhorn.residual) equals, sweep by sweep, the literal Algorithm 4
+    line 7: Res = ||phi (.) FTVP-1(psi, varphi) - u||_1 + ||psi (.) FTVP-1(phi, varphi) - v||_1,
+    with Algorithm 2's FTVP-1 computing the products -- an independent evaluation of the
+    same l = 3 quantity (A6: the sum over k < l of the L1 marginal violations)."""
+    from oracle import paper3
+    N = 14
+    h = 1.0 / (N - 1)
+    u, v, w = _mus(700 + int(100 * eps), 3, N)
+    mus = np.stack([u, v, w])
+    for T in (1, 2, 3, 7):
+        _, _, _, t, res_paper, _ = paper3.fast_sinkhorn_3(u, v, w, h, eps, T, 0.0)
+        assert t == T
+        phis, t2, res = sinkhorn.sinkhorn(mus, h, eps, T, tol=1e-300)
+        assert t2 == T
+        assert res == pytest.approx(res_paper, rel=1e-12, abs=1e-17), (T, res, res_paper)
+        assert sinkhorn.residual(phis, mus, h, eps) == pytest.approx(res_paper, rel=1e-12, abs=1e-17)
+
+
+@pytest.mark.parametrize("l", [3, 4])
+def test_residual_pinned_to_plan_marginals(l):
+    """The residual equals the L1 violation of the marginals of the explicit plan tensor
+    T = K (.) (phi_1 x ... x phi_l), summed over k < l (Algorithm 1 line 7, P:168,
+    generalised), with the plan built by an outer product and summed over all axes but k -- not by a
+    tensor-vector product.  The l-th term vanishes after the sweep's last update."""
+    N = 5
+    h, eta = 1.0 / (N - 1), 0.15
+    mus = _mus(800 + l, l, N)
+    K = dense.kernel_tensor(l, N, h, eta)
+    for T in (1, 2, 5):
+        phis, _, res = sinkhorn.sinkhorn(mus, h, eta, T, tol=1e-300)
+        outer = phis[0]
+        for q in range(1, l):
+            outer = np.multiply.outer(outer, phis[q])
+        plan = K * outer
+        viol = [np.abs(plan.sum(axis=tuple(a for a in range(l) if a != k)) - mus[k]).sum() for k in range(l)]
+        assert res == pytest.approx(sum(viol[:-1]), rel=1e-11, abs=1e-17), T
+        assert viol[-1] < 1e-15
+        # the dense driver's stop rule sees the same residual: same stop sweep for a tolerance
+        tol = 0.5 * res
+        _, t_fast, _ = sinkhorn.sinkhorn(mus, h, eta, 200, tol=tol)
+        _, t_dense, _ = dense.sinkhorn(mus, h, eta, 200, tol=tol)
+        assert t_fast == t_dense
