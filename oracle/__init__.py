@@ -21,6 +21,10 @@ Everything is plain fp64 and follows the paper (``P:n`` = line n of PAPER.md):
                  in the normalised form of Algorithm 2 (relative powers of
                  lambda only).  Plain, log-domain and cost (E-weighted,
                  P:1103-1125) variants; C implementation ``regions.c``.
+* ``subset``  -- O4: the subset-lattice DP over the 2^(l-1) placement states,
+                 written as plain subset sums; plain, log-domain and tangent variants; C
+                 implementation ``subset.c``.  Pinned against O1 and O3; the fast oracle for
+                 full-size parity and the timed CPU baseline.
 * ``sinkhorn`` -- O5: Gauss-Seidel Sinkhorn driver over any of the above,
                  residual (Algorithm 1 line 7 generalised), cost W.
 * ``comonotone`` -- closed-form unregularised optimum W_0 of the 1-D pairwise
@@ -30,4 +34,4 @@ Everything is plain fp64 and follows the paper (``P:n`` = line n of PAPER.md):
 
 Every function and the tests that pin it are listed in DESIGN.md §2b; none is "parity unpinned".
 """
-from . import dense, paper3, regions, sinkhorn, comonotone  # noqa: F401
+from . import dense, paper3, regions, subset, sinkhorn, comonotone  # noqa: F401

@@ -21,16 +21,20 @@ from typing import Callable, Optional, Sequence
 
 import numpy as np
 
-from . import regions
+from . import regions, subset
+
+# product engine: "regions" (O3, the paper's §4.2 recursion) or "subset" (O4, subset-lattice DP,
+# pinned against O1 and O3 by tests/test_oracle_subset.py; several times faster at l >= 5)
+_ENGINES = {"regions": regions, "subset": subset}
 
 
 def _weights(l, h, eta):
     return regions.edge_weights(l, h, eta)
 
 
-def product(phis, k, h, eta):
-    """J_k by region chains (plain fp64)."""
-    return regions.marginal_product(list(phis), k, _weights(len(phis), h, eta))
+def product(phis, k, h, eta, engine: str = "regions"):
+    """J_k by region chains (plain fp64), or by the subset DP (engine="subset")."""
+    return _ENGINES[engine].marginal_product(list(phis), k, _weights(len(phis), h, eta))
 
 
 def marginals(phis, h, eta):
@@ -38,10 +42,10 @@ def marginals(phis, h, eta):
     return np.stack([phis[k] * product(phis, k, h, eta) for k in range(len(phis))])
 
 
-def log_product(gs, k, h, eta):
+def log_product(gs, k, h, eta, engine: str = "regions"):
     l = len(gs)
     lw = np.array([-(a * (l - a)) * h / eta for a in range(l + 1)])
-    return regions.marginal_product_log(list(gs), k, lw)
+    return _ENGINES[engine].marginal_product_log(list(gs), k, lw)
 
 
 def cost(phis, h, eta, k: Optional[int] = None):
@@ -52,15 +56,16 @@ def cost(phis, h, eta, k: Optional[int] = None):
     return float(h * np.dot(phis[k], jh))
 
 
-def residual(phis, mus, h, eta):
+def residual(phis, mus, h, eta, engine: str = "regions"):
     l = len(phis)
-    return float(sum(np.abs(phis[k] * product(phis, k, h, eta) - mus[k]).sum() for k in range(l - 1)))
+    return float(sum(np.abs(phis[k] * product(phis, k, h, eta, engine) - mus[k]).sum() for k in range(l - 1)))
 
 
 def sinkhorn(mus: np.ndarray, h: float, eta: float, iters: int, tol: float = 0.0,
              phis0: Optional[np.ndarray] = None, domain: str = "plain",
-             record: Optional[Callable] = None, check_every: int = 1):
-    """Run Sinkhorn; returns (scalings, t, Res).  Scalings are phi (plain) or g = log phi (log)."""
+             record: Optional[Callable] = None, check_every: int = 1, engine: str = "regions"):
+    """Run Sinkhorn; returns (scalings, t, Res).  Scalings are phi (plain) or g = log phi (log).
+    engine: "regions" (O3) or "subset" (O4) products."""
     l, N = mus.shape
     if domain == "plain":
         x = [np.full(N, 1.0 / N) for _ in range(l)] if phis0 is None else [p.astype(np.float64).copy() for p in phis0]
@@ -74,14 +79,14 @@ def sinkhorn(mus: np.ndarray, h: float, eta: float, iters: int, tol: float = 0.0
         t += 1
         for k in range(l):
             if domain == "plain":
-                x[k] = mus[k] / product(x, k, h, eta)
+                x[k] = mus[k] / product(x, k, h, eta, engine)
             else:
-                x[k] = logmu[k] - log_product(x, k, h, eta)
+                x[k] = logmu[k] - log_product(x, k, h, eta, engine)
         if tol > 0 and (t % check_every == 0 or t == iters):
             if domain == "plain":
-                res = residual(x, mus, h, eta)
+                res = residual(x, mus, h, eta, engine)
             else:
-                res = float(sum(np.abs(np.exp(x[k] + log_product(x, k, h, eta)) - mus[k]).sum()
+                res = float(sum(np.abs(np.exp(x[k] + log_product(x, k, h, eta, engine)) - mus[k]).sum()
                                 for k in range(l - 1)))
         if record is not None:
             record(t, [v.copy() for v in x])

@@ -200,7 +200,7 @@ def test_batched_c5_full_run_stratified_instances():
     """C5 as the bench runs it: the full batch (8192 x (l=5, N=4096), per-instance eta ~ logU[1e-3,
     1e-1]) for the full T = 300 sweeps, then 8 stratified instances -- the median-eta instance of
     each of 8 equal log-eta strata -- against the log-domain oracle (region chains, P:1062-1125,
-    in a pure log domain: Remark 1's purpose), run in parallel on the host cores:
+    in a pure log domain: Remark 1's purpose; O4 products), in parallel on the host cores:
     marginals to 1e-10 L1-relative, W to 1e-10, log phi to 1e-9 relative.  This covers the lazy
     chain-exponent renormalisation at |log phi| ~ 1.8e3 (eta = 1e-3) over a whole run."""
     import concurrent.futures as cf
@@ -228,10 +228,12 @@ def test_batched_c5_full_run_stratified_instances():
     h = mmot_inputs.grid_h(N)
 
     def ref(b):
+        # O4 products (subset DP, pinned against O1/O3 in tests/test_oracle_subset.py): 4x faster
+        from oracle import subset
         eta = float(etas[b])
-        g_ref, _, _ = osk.sinkhorn(mus_all[:, b, :], h, eta, T, domain="log")
+        g_ref, _, _ = osk.sinkhorn(mus_all[:, b, :], h, eta, T, domain="log", engine="subset")
         lw = np.array([-(a * (l - a)) * h / eta for a in range(l + 1)])
-        m_ref = [np.exp(g_ref[k] + regions.marginal_product_log(list(g_ref), k, lw)) for k in range(l)]
+        m_ref = [np.exp(g_ref[k] + subset.marginal_product_log(list(g_ref), k, lw)) for k in range(l)]
         return g_ref, m_ref
 
     with cf.ThreadPoolExecutor(max_workers=len(picks)) as ex:   # ctypes releases the GIL
