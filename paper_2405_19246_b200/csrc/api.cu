@@ -31,6 +31,8 @@ struct DevScalars {
     int iters_done;
     int converged;
     int guard;          // single-walk precision guard tripped (k_sw_guard)
+    int sweep;          // completed sweeps of the current solve (device counter)
+    int g_done, g_n;    // device-resident loop: periods done / to do
     int flags[2 * mmot::kMaxL];
     double resid;
     double res_acc;
@@ -160,8 +162,15 @@ struct mmot_ctx {
     double *bat_rhost = nullptr;            // pinned [batch]: last residual
     double *stage_mu[mmot::kMaxL] = {nullptr};
     double *stage_u[mmot::kMaxL] = {nullptr};
-    int *hstop = nullptr;       // pinned, async stop polling
+    int *hstop = nullptr;       // pinned, async stop polling (hstop[1]: loop period count for the graph)
     cudaEvent_t poll_ev = nullptr;
+    // device-resident Sinkhorn loop: cached graph (a WHILE node whose body is `period` sweeps)
+    cudaGraphExec_t g_exec = nullptr;
+    cudaGraph_t g_graph = nullptr;
+    const void *g_key[2 * mmot::kMaxL + 4] = {nullptr};
+    int64_t g_launches = 0;     // kernels per graph period (launch accounting)
+    int64_t graph_solves = 0;
+    bool graph_broken = false;  // capture failed once: host loop from then on
     int64_t launches = 0;
     char err[256] = "";
     // profiling (mmot_profile_enable)
@@ -274,6 +283,8 @@ void mmot_destroy(mmot_ctx *ctx) {
     if (ctx->hsc) cudaFreeHost(ctx->hsc);
     if (ctx->hstop) cudaFreeHost(ctx->hstop);
     if (ctx->poll_ev) cudaEventDestroy(ctx->poll_ev);
+    if (ctx->g_exec) cudaGraphExecDestroy(ctx->g_exec);
+    if (ctx->g_graph) cudaGraphDestroy(ctx->g_graph);
     for (cudaEvent_t e : ctx->pool) cudaEventDestroy(e);
     cudaSetDevice(cur);
     delete ctx;
@@ -466,7 +477,7 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
         // (points >= N) holds phi = mu = 0 for the whole life of the context
         const size_t tb = (size_t)c->nchp * (size_t)c->P * sizeof(double);
         bool ok = cudaMalloc(&c->out_t, tb) == cudaSuccess && cudaMemsetAsync(c->out_t, 0, tb, c->stream) == cudaSuccess &&
-                  cudaMalloc(&c->sw_end, (size_t)c->nchunks * M * sizeof(mmot::Dual)) == cudaSuccess;
+                  cudaMalloc(&c->sw_end, 2 * (size_t)c->nchunks * M * sizeof(mmot::Dual)) == cudaSuccess;
         for (int qq = 0; qq < l && ok; ++qq)
             ok = cudaMalloc(&c->lin[qq], tb) == cudaSuccess && cudaMalloc(&c->mu_t[qq], tb) == cudaSuccess &&
                  cudaMemsetAsync(c->lin[qq], 0, tb, c->stream) == cudaSuccess &&
@@ -518,7 +529,7 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
         }
     }
     if (cudaMallocHost(&c->hsc, sizeof(DevScalars)) != cudaSuccess ||
-        cudaMallocHost(&c->hstop, sizeof(int)) != cudaSuccess ||
+        cudaMallocHost(&c->hstop, 2 * sizeof(int)) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->poll_ev, cudaEventDisableTiming) != cudaSuccess) {
         set_err(c, "host allocation failed");
         snprintf(g_err, sizeof g_err, "%s", c->err);
@@ -937,6 +948,7 @@ static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double
     p.status = &c->dsc->status;
     p.fail_iter = &c->dsc->fail_iter;
     p.iter = iter;
+    if (iter > 0) p.sweep = &c->dsc->sweep;  // inside a solve
     if (c->sw) {
         p.sw_end = c->sw_end;
         p.guard = &c->dsc->guard;
@@ -993,6 +1005,127 @@ static mmot_status guard_tripped(mmot_ctx *c) {
     return MMOT_EPRECISION;
 }
 
+// Host-side state of the update sequence: which chain operators / restricted-scan elements the
+// previous product left behind (they decide the launch configuration of the next update).
+struct SweepState {
+    int ops_for = -1;      // bound set whose chain operators are in ops level 0
+    bool rx_ready = false; // the previous update wrote this update's affine elements
+    int cur = 0;           // restricted scan: which carry set is current
+    bool operator==(const SweepState &o) const { return ops_for == o.ops_for && rx_ready == o.rx_ready && cur == o.cur; }
+};
+
+// Enqueue sweep t (l fused updates, then the residual check or the sweep counter).
+static mmot_status enqueue_sweep(mmot_ctx *c, int t, bool check, double tol, const double *const *lin,
+                                 const double *const *mu, SweepState &ss) {
+    const int l = c->l;
+    const bool rx = c->rx && (!c->sharded || c->nlev >= 2);
+    void *cf[2] = {c->car_f[0], c->carB_f}, *cb[2] = {c->car_bi, c->carB_bi};
+    for (int k = 0; k < l; ++k) {
+        // fused update: scan (+ operators only if not produced by the previous update),
+        // apply phi_k <- mu_k / J_k and build the operators of update k+1 in the same walk
+        Plan p = make_plan(c, k, lin, mu[k], const_cast<double *>(lin[k]), t);
+        if (rx) {
+            p.car_f[0] = cf[ss.cur];
+            p.car_bi = cb[ss.cur];
+            p.ncar_f = cf[1 - ss.cur];
+            p.ncar_bi = cb[1 - ss.cur];
+            p.nxr = 1;
+            p.rx_scan = ss.rx_ready ? 1 : 0;
+        }
+        CK(c, mmot::launch_product(p, mmot::MODE_UPD, c->stream, &c->launches, prof_events(c, mmot::MODE_UPD),
+                                   rx ? !ss.rx_ready : ss.ops_for != k, true));
+        // l = 6 / non-uniform grids: next-update operators are not fused
+        ss.ops_for = (l <= 5 && !c->pts_lam) ? (k + 1) % l : -1;
+        if (rx) {
+            ss.rx_ready = true;
+            ss.cur = 1 - ss.cur;
+        }
+    }
+    CK(c, mmot::launch_sweep_done(&c->dsc->sweep, &c->dsc->iters_done, &c->dsc->stop, c->stream, &c->launches));
+    if (check) {
+        for (int k = 0; k + 1 < l; ++k) {
+            Plan p = make_plan(c, k, lin, mu[k], nullptr, t);
+            CK(c, mmot::launch_product(p, mmot::MODE_RES, c->stream, &c->launches, prof_events(c, mmot::MODE_RES)));
+            ss.ops_for = -1;      // the residual products overwrote the chain operators
+            ss.rx_ready = false;  // ... and the level-0 carries: the next update starts from a full scan
+            ss.cur = 0;
+            CK(c, mmot::launch_sum(c->partial, c->nchunks, &c->dsc->res_acc, 1.0, k > 0, &c->dsc->stop, c->stream,
+                                   &c->launches));
+        }
+        mmot_status st = shard_allreduce(c, &c->dsc->res_acc);
+        if (st) return st;
+        CK(c, mmot::launch_resid_finish(&c->dsc->res_acc, tol, &c->dsc->sweep, &c->dsc->resid, &c->dsc->iters_done,
+                                        &c->dsc->converged, &c->dsc->stop, c->stream, &c->launches));
+    }
+    return MMOT_OK;
+}
+
+// Device-resident loop: a CUDA graph whose WHILE node runs `n` periods of `period` sweeps (each
+// ending with the residual check when tol > 0) until the periods are done or the device stop flag is
+// set -- one graph launch, no host round trip per sweep.  The graph bakes in the context's vectors,
+// so it is rebuilt when the caller's pointers (or the schedule) change.
+static mmot_status run_graph_loop(mmot_ctx *c, int period, int n, bool check, double tol, const double *const *lin,
+                                  const double *const *mu, const SweepState &ss0) {
+    const void *key[2 * mmot::kMaxL + 4] = {nullptr};
+    for (int q = 0; q < c->l; ++q) {
+        key[q] = lin[q];
+        key[mmot::kMaxL + q] = mu[q];
+    }
+    key[2 * mmot::kMaxL] = reinterpret_cast<const void *>((intptr_t)period);
+    key[2 * mmot::kMaxL + 1] = reinterpret_cast<const void *>((intptr_t)(check ? 1 : 0));
+    key[2 * mmot::kMaxL + 2] = reinterpret_cast<const void *>((intptr_t)(ss0.ops_for + 8 * ss0.rx_ready + 64 * ss0.cur));
+    double tkey = check ? tol : 0.0;
+    memcpy(&key[2 * mmot::kMaxL + 3], &tkey, sizeof(tkey) <= sizeof(void *) ? sizeof(tkey) : sizeof(void *));
+    if (!c->g_exec || memcmp(key, c->g_key, sizeof key) != 0) {
+        if (c->g_exec) { cudaGraphExecDestroy(c->g_exec); c->g_exec = nullptr; }
+        if (c->g_graph) { cudaGraphDestroy(c->g_graph); c->g_graph = nullptr; }
+        cudaGraph_t g = nullptr;
+        CK(c, cudaGraphCreate(&g, 0));
+        c->g_graph = g;
+        cudaGraphConditionalHandle h;
+        CK(c, cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams np = {};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = h;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(c, cudaGraphAddNode(&node, g, nullptr, 0, &np));
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        const int64_t l0 = c->launches;
+        CK(c, cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        SweepState ss = ss0;
+        mmot_status st = MMOT_OK;
+        for (int i = 0; i < period && !st; ++i) st = enqueue_sweep(c, 1, check && i + 1 == period, tol, lin, mu, ss);
+        if (!st) {
+            cudaError_t e = mmot::launch_loop_cond(h, &c->dsc->g_done, &c->dsc->g_n, &c->dsc->stop, c->stream,
+                                                   &c->launches);
+            if (e != cudaSuccess) { set_err(c, "loop condition: %s", cudaGetErrorString(e)); st = MMOT_ECUDA; }
+        }
+        cudaGraph_t cap = nullptr;
+        cudaError_t e = cudaStreamEndCapture(c->stream, &cap);
+        if (st || e != cudaSuccess) {
+            // capture refused something: forget the graph, clear the error, let the host loop run
+            cudaGetLastError();
+            c->launches = l0;
+            c->graph_broken = true;
+            return MMOT_EUNSUPPORTED;
+        }
+        if (!(ss == ss0)) { set_err(c, "internal: graph period does not return to its start state"); return MMOT_ECUDA; }
+        c->g_launches = c->launches - l0;
+        c->launches = l0;
+        CK(c, cudaGraphInstantiate(&c->g_exec, g, 0));
+        memcpy(c->g_key, key, sizeof key);
+    }
+    c->hstop[1] = n;
+    CK(c, cudaMemsetAsync(&c->dsc->g_done, 0, sizeof(int), c->stream));
+    CK(c, cudaMemcpyAsync(&c->dsc->g_n, &c->hstop[1], sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaGraphLaunch(c->g_exec, c->stream));
+    c->launches += c->g_launches * n;  // upper bound: periods after a stop exit at the condition
+    ++c->graph_solves;
+    return MMOT_OK;
+}
+
 static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters, double tol, void *const *u,
                                  mmot_report *rep) {
     const int l = c->l;
@@ -1000,84 +1133,63 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
     if (st) return st;
     c->exch_error = 0;
     // data checks (P:75 marginals are probability vectors; SPEC S:77 error vocabulary); a sharded
-    // context tests the mass of the whole marginal and all ranks adopt the worst status
-    for (int q = 0; q < l; ++q) {
-        CK(c, mmot::launch_check(mu[q], c->N, 0, &c->dsc->flags[q], &c->dsc->mass[q], c->stream, &c->launches));
-        CK(c, mmot::launch_check(static_cast<const double *>(u[q]), c->N, c->opts.repr == MMOT_LOG ? 1 : 0,
-                                 &c->dsc->flags[l + q], nullptr, c->stream, &c->launches));
-    }
-    if ((st = shard_allreduce(c, c->dsc->mass, l))) return st;
-    CK(c, mmot::launch_check_finish(c->dsc->flags, c->dsc->mass, 2 * l, l, &c->dsc->status, &c->dsc->stop,
-                                    &c->dsc->fail_iter, c->stream, &c->launches));
-    if ((st = shard_agree(c, &c->dsc->stop, 3))) return st;
-    // working scalings
+    // context tests the mass of the whole marginal and all ranks adopt the worst status.  The
+    // single-walk family fuses them into its layout conversion (one pass over each input).
     double *lin[mmot::kMaxL];
     for (int q = 0; q < l; ++q) {
+        const int is_log = c->opts.repr == MMOT_LOG ? 1 : 0;
         if (c->sw) {
             CK(c, mmot::launch_to_t(static_cast<const double *>(u[q]), c->lin[q], c->N, c->P, c->nchunks, c->nchp,
-                                    c->opts.repr == MMOT_LOG ? 1 : 0, c->stream, &c->launches));
-            CK(c, mmot::launch_to_t(mu[q], c->mu_t[q], c->N, c->P, c->nchunks, c->nchp, 0, c->stream, &c->launches));
+                                    is_log, c->stream, &c->launches, &c->dsc->flags[l + q], nullptr, is_log));
+            CK(c, mmot::launch_to_t(mu[q], c->mu_t[q], c->N, c->P, c->nchunks, c->nchp, 0, c->stream, &c->launches,
+                                    &c->dsc->flags[q], &c->dsc->mass[q], 0));
             lin[q] = c->lin[q];
-        } else if (c->opts.repr == MMOT_LOG) {
+            continue;
+        }
+        CK(c, mmot::launch_check(mu[q], c->N, 0, &c->dsc->flags[q], &c->dsc->mass[q], c->stream, &c->launches));
+        CK(c, mmot::launch_check(static_cast<const double *>(u[q]), c->N, is_log, &c->dsc->flags[l + q], nullptr,
+                                 c->stream, &c->launches));
+        if (is_log) {
             CK(c, mmot::launch_exp(static_cast<const double *>(u[q]), c->lin[q], c->N, c->stream, &c->launches));
             lin[q] = c->lin[q];
         } else {
             lin[q] = static_cast<double *>(u[q]);
         }
     }
+    if ((st = shard_allreduce(c, c->dsc->mass, l))) return st;
+    CK(c, mmot::launch_check_finish(c->dsc->flags, c->dsc->mass, 2 * l, l, &c->dsc->status, &c->dsc->stop,
+                                    &c->dsc->fail_iter, c->stream, &c->launches));
+    if ((st = shard_agree(c, &c->dsc->stop, 3))) return st;
     const int check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
-    bool poll_pending = false;
-    int ops_for = -1;  // bound set whose chain operators are currently in ops level 0
-    // restricted next-update scan: carries alternate between the context's level-0 arrays (0) and
-    // the second set (1); rx_ready = the previous update wrote this update's affine elements
     const bool rx = c->rx && (!c->sharded || c->nlev >= 2);
-    int cur = 0;
-    bool rx_ready = false;
-    void *cf[2] = {c->car_f[0], c->carB_f}, *cb[2] = {c->car_bi, c->carB_bi};
-    for (int t = 1; t <= iters; ++t) {
+    SweepState ss;
+    // Device-resident loop (CUDA graph, WHILE node) for single-process contexts when not profiling:
+    // tol > 0 -- periods of check_every sweeps ending with the residual check, from the solve's
+    // start state; tol <= 0 -- after `warm` host-issued sweeps the update sequence is periodic with
+    // `period` sweeps (the restricted scan alternates two carry sets, so odd l needs two sweeps).
+    const bool graph = !c->sharded && !c->prof && !c->graph_broken && iters >= 4 && getenv("MMOT_NO_GRAPH") == nullptr;
+    int t = 1;
+    if (graph) {
+        const int period = tol > 0 ? check_every : ((rx && (l & 1)) ? 2 : 1);
+        const int warm = tol > 0 ? 0 : period;
+        for (; t <= warm; ++t)
+            if ((st = enqueue_sweep(c, t, false, tol, lin, mu, ss))) return st;
+        const int n = (iters - warm) / period;
+        if (n >= 1) {
+            st = run_graph_loop(c, period, n, tol > 0, tol, lin, mu, ss);
+            if (st == MMOT_OK) t += n * period;
+            else if (st != MMOT_EUNSUPPORTED) return st;  // EUNSUPPORTED: not capturable, host loop
+        }
+    }
+    bool poll_pending = false;
+    for (; t <= iters; ++t) {
         // asynchronous early exit: the device stop flag is polled without blocking
         if (poll_pending && cudaEventQuery(c->poll_ev) == cudaSuccess) {
             poll_pending = false;
             if (*c->hstop) break;
         }
-        for (int k = 0; k < l; ++k) {
-            // fused update: scan (+ operators only if not produced by the previous update),
-            // apply phi_k <- mu_k / J_k and build the operators of update k+1 in the same walk
-            Plan p = make_plan(c, k, lin, mu[k], lin[k], t);
-            if (rx) {
-                p.car_f[0] = cf[cur];
-                p.car_bi = cb[cur];
-                p.ncar_f = cf[1 - cur];
-                p.ncar_bi = cb[1 - cur];
-                p.nxr = 1;
-                p.rx_scan = rx_ready ? 1 : 0;
-            }
-            CK(c, mmot::launch_product(p, mmot::MODE_UPD, c->stream, &c->launches, prof_events(c, mmot::MODE_UPD),
-                                       rx ? !rx_ready : ops_for != k, true));
-            // l = 6 / non-uniform grids: next-update operators are not fused
-            ops_for = (l <= 5 && !c->pts_lam) ? (k + 1) % l : -1;
-            if (rx) {
-                rx_ready = true;
-                cur = 1 - cur;
-            }
-        }
-        if (tol > 0 && (t % check_every == 0 || t == iters)) {
-            for (int k = 0; k + 1 < l; ++k) {
-                Plan p = make_plan(c, k, lin, mu[k], nullptr, t);
-                CK(c, mmot::launch_product(p, mmot::MODE_RES, c->stream, &c->launches, prof_events(c, mmot::MODE_RES)));
-                ops_for = -1;  // the residual products overwrote the chain operators
-                rx_ready = false;  // ... and the level-0 carries: the next update starts from a full scan
-                cur = 0;
-                CK(c, mmot::launch_sum(c->partial, c->nchunks, &c->dsc->res_acc, 1.0, k > 0, &c->dsc->stop, c->stream,
-                                       &c->launches));
-            }
-            st = shard_allreduce(c, &c->dsc->res_acc);
-            if (st) return st;
-            CK(c, mmot::launch_resid_finish(&c->dsc->res_acc, tol, t, &c->dsc->resid, &c->dsc->iters_done,
-                                            &c->dsc->converged, &c->dsc->stop, c->stream, &c->launches));
-        } else {
-            CK(c, mmot::launch_sweep_done(t, &c->dsc->iters_done, &c->dsc->stop, c->stream, &c->launches));
-        }
+        const bool check = tol > 0 && (t % check_every == 0 || t == iters);
+        if ((st = enqueue_sweep(c, t, check, tol, lin, mu, ss))) return st;
         if (tol > 0 && multi_rank(c) && t % 8 == 0) {
             // sharded: the early exit must be collective -- agree on the stop flag, then read it
             // synchronously, so every rank leaves the loop after the same sweep and issues the
@@ -1096,7 +1208,8 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
         // precision guard: decided before u is written, so a fallback restarts from the same input
         if ((st = shard_agree(c, &c->dsc->stop, 6))) return st;
         if ((st = sync_report(c))) return st;
-        if (c->hsc->guard && !c->hsc->status) {
+        // (an EOVERFLOW of the single walk may itself be the lost precision: redo it too)
+        if (c->hsc->guard && (!c->hsc->status || c->hsc->status == MMOT_EOVERFLOW)) {
             if (c->sharded) return guard_tripped(c);
             ++c->fallbacks;
             if ((st = ensure_fallback(c))) return st;
@@ -1289,7 +1402,7 @@ mmot_status mmot_cost(mmot_ctx *c, const void *const *u, double *W) {
     st = sync_report(c);
     if (st) return st;
     if (c->exch_error) return MMOT_ENCCL;
-    if (c->sw && c->hsc->guard && !c->hsc->status) {
+    if (c->sw && c->hsc->guard && (!c->hsc->status || c->hsc->status == MMOT_EOVERFLOW)) {
         if (c->sharded) return guard_tripped(c);
         ++c->fallbacks;
         if ((st = ensure_fallback(c))) return st;

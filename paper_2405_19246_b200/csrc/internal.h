@@ -64,7 +64,8 @@ struct Plan {
     int *stop;                       // device flag: nonzero -> every kernel returns at once
     int *status;                     // device status (mmot_status) of the run
     int *fail_iter;                  // device: sweep index of the first failure
-    int iter;                        // current sweep index (for fail_iter)
+    int iter;                        // current sweep index (for fail_iter) outside a solve
+    const int *sweep = nullptr;      // inside a solve: device count of completed sweeps (fail_iter)
     // single-walk precision guard: every chain stores its walked end state (sw_end, [nchunks][M] in
     // T units) and k_sw_guard compares it with the exact inclusive suffix carry of the next chain;
     // a componentwise relative difference above kSwGuardTol sets *guard
@@ -92,8 +93,11 @@ cudaError_t launch_sum(const double *partial, int64_t n, double *out, double sca
                        const int *stop, cudaStream_t s, int64_t *launches);
 
 // Natural <-> chain-blocked layout (x = c*P + t <-> (c/32)*32P + t*32 + c%32); op 0 copy, 1 exp, 2 log.
+// flags != nullptr fuses launch_check into the pass (flags bit0 non-finite, bit1 negative; mass += sum
+// when mass != nullptr).
 cudaError_t launch_to_t(const double *src, double *dst, int64_t N, int64_t P, int64_t nchains, int64_t nchp, int op,
-                        cudaStream_t s, int64_t *launches);
+                        cudaStream_t s, int64_t *launches, int *flags = nullptr, double *mass = nullptr,
+                        int allow_neg_inf = 0);
 cudaError_t launch_from_t(const double *src, double *dst, int64_t N, int64_t P, int64_t nchains, int64_t nchp, int op,
                           cudaStream_t s, int64_t *launches);
 constexpr int kSwSlab = 8;  // chain length of single-walk contexts is a multiple of this
@@ -160,10 +164,13 @@ cudaError_t launch_check(const double *v, int64_t n, int allow_neg_inf, int *fla
 // After checks: turn flags/mass into a status and stop flag.
 cudaError_t launch_check_finish(const int *flags, const double *mass, int nvec, int nmarg, int *status,
                                 int *stop, int *fail_iter, cudaStream_t s, int64_t *launches);
-// End of a residual evaluation: res = *acc; if res <= tol stop (converged).
-cudaError_t launch_resid_finish(double *acc, double tol, int iter, double *res_out, int *iters_done,
+// End of a residual evaluation: res = *acc; iters_done = *sweep; if res <= tol stop (converged).
+cudaError_t launch_resid_finish(double *acc, double tol, const int *sweep, double *res_out, int *iters_done,
                                 int *converged, int *stop, cudaStream_t s, int64_t *launches);
-// End of a sweep without residual: iters_done = iter unless stopped.
-cudaError_t launch_sweep_done(int iter, int *iters_done, const int *stop, cudaStream_t s, int64_t *launches);
+// End of a sweep: unless stopped, ++*sweep and iters_done = *sweep.
+cudaError_t launch_sweep_done(int *sweep, int *iters_done, const int *stop, cudaStream_t s, int64_t *launches);
+// Device-resident loop: ++*done; conditional h = (*done < *n && !*stop) (graph WHILE node body end).
+cudaError_t launch_loop_cond(cudaGraphConditionalHandle h, int *done, const int *n, const int *stop, cudaStream_t s,
+                             int64_t *launches);
 
 }  // namespace mmot

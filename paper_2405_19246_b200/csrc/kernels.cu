@@ -655,7 +655,8 @@ __global__ void __launch_bounds__(128) k_ops_down_w(const double *ops_f, const d
 // Phase 3: apply.
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ void raise_status(const Plan &p, int st) {
-    if (atomicCAS(p.status, 0, st) == 0) *p.fail_iter = p.iter;
+    // fail_iter: the sweep in progress (completed sweeps + 1 inside a solve; p.iter otherwise)
+    if (atomicCAS(p.status, 0, st) == 0) *p.fail_iter = p.sweep ? *p.sweep + 1 : p.iter;
     *(volatile int *)p.stop = 1;
 }
 
@@ -1335,12 +1336,19 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
     if constexpr (NEXT) {
         if (have_prev) next_ops_step<NB, T>(Gx, wt, fprev, oprev, ns == 1 && kSwS == 1);
     }
-    if (bad && live) raise_status(p, 6 /*EOVERFLOW*/);
+    if (bad && live) {
+        raise_status(p, 6 /*EOVERFLOW*/);
+        if (p.guard) atomicOr(p.guard, 1);  // may be the single walk's lost precision: redo on two-walk
+    }
     if ((MODE == MODE_RES || MODE == MODE_COST) && live) p.partial[c] = acc;
     if (live && p.sw_end) {
-        T *e = static_cast<T *>(p.sw_end) + c * M;
+        // walked suffix state after the chain's last point and the prefix state at that point
+        T *e = static_cast<T *>(p.sw_end) + c * 2 * M;
 #pragma unroll
-        for (int R = 0; R < M; ++R) e[R] = B[R];
+        for (int R = 0; R < M; ++R) {
+            e[R] = B[R];
+            e[M + R] = F[R];
+        }
     }
     if constexpr (NEXT) {
         if (live)
@@ -1581,21 +1589,44 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_sw_ops(Plan p) {
 // Natural <-> chain-blocked layout: natural x = c*P + t  <->  (c/32)*32P + t*32 + c%32.
 // op: 0 copy, 1 exp (natural log-scalings -> linear), 2 log (linear -> log-scalings).
 // One CTA per 32 chains x 32 offsets tile (blockIdx.y = chain group).
+// flags != nullptr: the input check of launch_check fused into the pass (bit0 NaN/Inf, bit1
+// negative; -inf allowed when allow_neg_inf) and, if mass != nullptr, the sum of the inputs.
 __global__ void k_to_t(const double *__restrict__ src, double *__restrict__ dst, int64_t N, int64_t P, int64_t nchains,
-                       int op) {
+                       int op, int *flags, double *mass, int allow_neg_inf) {
     __shared__ double tile[32][33];
+    __shared__ double msum[8];
     const int64_t t0 = (int64_t)blockIdx.x * 32, g = blockIdx.y, c0 = g * 32;
+    int fl = 0;
+    double a = 0.0;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {  // r: chain within tile, threadIdx.x: offset t
         const int64_t c = c0 + r, t = t0 + threadIdx.x;
         const int64_t x = c * P + t;
         double v = 0.0;
         if (c < nchains && t < P && x < N) {
             v = src[x];
+            if (flags) {
+                if (isnan(v) || (isinf(v) && !(allow_neg_inf && v < 0))) fl |= 1;
+                else if (v < 0 && !allow_neg_inf) fl |= 2;
+                else if (!allow_neg_inf) a += v;
+            }
             if (op == 1) v = exp(v);
         }
         tile[r][threadIdx.x] = v;
     }
+    if (flags) {
+        if (fl) atomicOr(flags, fl);
+        if (mass) {
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) a += __shfl_xor_sync(0xffffffffu, a, d);
+            if (threadIdx.x == 0) msum[threadIdx.y] = a;
+        }
+    }
     __syncthreads();
+    if (flags && mass && threadIdx.y == 0 && threadIdx.x == 0) {
+        double b = 0.0;
+        for (int i = 0; i < (int)blockDim.y; ++i) b += msum[i];
+        atomicAdd(mass, b);
+    }
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {  // r: offset within tile, threadIdx.x: chain
         const int64_t t = t0 + r;
         if (t < P) dst[g * 32 * P + t * 32 + threadIdx.x] = tile[threadIdx.x][r];
@@ -1623,9 +1654,9 @@ __global__ void k_from_t(const double *__restrict__ src, double *__restrict__ ds
 }
 
 cudaError_t launch_to_t(const double *src, double *dst, int64_t N, int64_t P, int64_t nchains, int64_t nchp, int op,
-                        cudaStream_t s, int64_t *launches) {
+                        cudaStream_t s, int64_t *launches, int *flags, double *mass, int allow_neg_inf) {
     dim3 grid((unsigned)((P + 31) / 32), (unsigned)(nchp / 32));
-    k_to_t<<<grid, dim3(32, 8), 0, s>>>(src, dst, N, P, nchains, op);
+    k_to_t<<<grid, dim3(32, 8), 0, s>>>(src, dst, N, P, nchains, op, flags, mass, allow_neg_inf);
     ++*launches;
     return cudaGetLastError();
 }
@@ -1671,28 +1702,50 @@ static void launch_apply_tm(const Plan &p, int64_t cbeg, int64_t cend, cudaStrea
     ++*launches;
 }
 
-// Single-walk precision guard.  The inverse step B_{m+1} = D^-1 place_m^-1(B_m) subtracts; its
-// rounding errors grow like the suffix states' relative condition, which the forward (positive)
-// recurrence cannot shrink, so the componentwise relative error of any interior suffix state is
-// bounded by that of the walked END state (up to rounding), which is compared here with the exact
-// inclusive suffix carry of the next chain (the scan's car_bi).  Components whose exact value is 0
-// (a marginal zero on the whole remaining suffix) carry only harmless rounding residue and are
-// skipped.  last: exact end state of the last chain (nullptr: e_empty); skip_last: do not check it.
-template <typename T>
-__global__ void k_sw_guard(const T *__restrict__ end, const T *__restrict__ cbi, const T *last, int skip_last, int M,
-                           int64_t n, const int *stop, int *guard) {
+// Single-walk precision guard.  The inverse step B_{m+1} = D^-1 place_m^-1(B_m) subtracts; the
+// rounding errors of the walked suffix states grow like their relative condition, which the forward
+// (positive) recurrence never shrinks, so the error at a chain's END bounds the errors inside it.
+// The end is checked where it matters, through the combine at the chain's last point m:
+//   err = sum_S F_m[S] w_{|S|+1} |B_walked[S^c] - B_exact[S^c]|  <=  kSwGuardTol * J_exact[m],
+// B_exact = the exact inclusive suffix carry of the next chain (the scan's car_bi); components that
+// cannot reach J (tiny suffix states multiplied by small prefix states) cannot trip it.  For dual
+// numbers (the cost) the tangent parts are checked the same way against the tangent of J.
+// last: exact end state of the last chain (nullptr: e_empty); skip_last: do not check it.
+template <int NB, typename T>
+__global__ void k_sw_guard(const T *__restrict__ end, const T *__restrict__ cbi, const T *last, int skip_last,
+                           Weights W, int64_t n, const int *stop, int *guard) {
+    constexpr int M = 1 << NB;
+    constexpr int K = sizeof(T) / sizeof(double);
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= n || *stop) return;
-    constexpr int K = sizeof(T) / sizeof(double);
-    const double *x = reinterpret_cast<const double *>(end + c * M);
-    const double *y = c + 1 < n ? reinterpret_cast<const double *>(cbi + (c + 1) * M)
-                                : reinterpret_cast<const double *>(last);
     if (c + 1 >= n && skip_last) return;
-    bool bad = false;
-    for (int i = 0; i < M * K; ++i) {
-        const double ex = y ? y[i] : (i == 0 ? 1.0 : 0.0);
-        if (ex != 0.0) bad |= !(fabs(x[i] - ex) <= kSwGuardTol * fabs(ex));
+    const double *bw = reinterpret_cast<const double *>(end + c * 2 * M);
+    const double *fw = reinterpret_cast<const double *>(end + c * 2 * M + M);
+    const double *be = c + 1 < n ? reinterpret_cast<const double *>(cbi + (c + 1) * M)
+                                 : reinterpret_cast<const double *>(last);
+    // value: J = sum F w B; tangent (duals): hatJ = sum (F' w + F w') B + F w B'
+    double err[K], ref[K];
+#pragma unroll
+    for (int d = 0; d < K; ++d) err[d] = ref[d] = 0.0;
+#pragma unroll
+    for (int S = 0; S < M; ++S) {
+        const int Sc = (M - 1) & ~S;
+        const int a1 = __popc(S) + 1;
+        const double a = W.w[a1] * fw[S * K];  // F w (value parts)
+        const double bv = be ? be[Sc * K] : (Sc == 0 ? 1.0 : 0.0);
+        const double dv = fabs(bw[Sc * K] - bv);
+        err[0] += a * dv;
+        ref[0] += a * bv;
+        if constexpr (K == 2) {
+            const double ad = W.w[a1] * fw[S * K + 1] + W.e[a1] * a;  // (F w)'
+            const double bd = be ? be[Sc * K + 1] : 0.0;
+            err[1] += a * fabs(bw[Sc * K + 1] - bd) + fabs(ad) * dv;
+            ref[1] += ad * bv + a * bd;
+        }
     }
+    bool bad = false;
+#pragma unroll
+    for (int d = 0; d < K; ++d) bad |= !(err[d] <= kSwGuardTol * fabs(ref[d]));
     if (bad) atomicOr(guard, 1);
 }
 
@@ -1705,8 +1758,8 @@ static void launch_sw_guard(const Plan &p, cudaStream_t s, int64_t *launches) {
         if (p.rx_scan) skip_last = 1;  // the rank carry holds only the new parts (affine scan)
         else last = static_cast<const T *>(p.rank_car) + M;
     }
-    k_sw_guard<T><<<(unsigned)((p.nchunks + 255) / 256), 256, 0, s>>>(
-        static_cast<const T *>(p.sw_end), static_cast<const T *>(p.car_bi), last, skip_last, M, p.nchunks, p.stop,
+    k_sw_guard<NB, T><<<(unsigned)((p.nchunks + 255) / 256), 256, 0, s>>>(
+        static_cast<const T *>(p.sw_end), static_cast<const T *>(p.car_bi), last, skip_last, p.W, p.nchunks, p.stop,
         p.guard);
     ++*launches;
 }
@@ -2120,33 +2173,50 @@ cudaError_t launch_check_finish(const int *flags, const double *mass, int nvec, 
     return cudaGetLastError();
 }
 
-__global__ void k_resid_finish(double *acc, double tol, int iter, double *res_out, int *iters_done, int *converged,
-                               int *stop) {
+__global__ void k_resid_finish(double *acc, double tol, const int *sweep, double *res_out, int *iters_done,
+                               int *converged, int *stop) {
     if (*stop) return;
     const double r = *acc;
     *res_out = r;
-    *iters_done = iter;
+    *iters_done = *sweep;
     if (r <= tol) {
         *converged = 1;
         *stop = 1;
     }
 }
 
-cudaError_t launch_resid_finish(double *acc, double tol, int iter, double *res_out, int *iters_done, int *converged,
-                                int *stop, cudaStream_t s, int64_t *launches) {
-    k_resid_finish<<<1, 1, 0, s>>>(acc, tol, iter, res_out, iters_done, converged, stop);
+cudaError_t launch_resid_finish(double *acc, double tol, const int *sweep, double *res_out, int *iters_done,
+                                int *converged, int *stop, cudaStream_t s, int64_t *launches) {
+    k_resid_finish<<<1, 1, 0, s>>>(acc, tol, sweep, res_out, iters_done, converged, stop);
     ++*launches;
     return cudaGetLastError();
 }
 
-__global__ void k_sweep_done(int iter, int *iters_done, const int *stop) {
-    if (!*stop) *iters_done = iter;
+// End of a sweep: unless the solve has stopped, count it (sweep = completed sweeps, read by the
+// residual check and by raise_status) and report it.
+__global__ void k_sweep_done(int *sweep, int *iters_done, const int *stop) {
+    if (*stop) return;
+    const int t = *sweep + 1;
+    *sweep = t;
+    *iters_done = t;
 }
-
-cudaError_t launch_sweep_done(int iter, int *iters_done, const int *stop, cudaStream_t s, int64_t *launches) {
-    k_sweep_done<<<1, 1, 0, s>>>(iter, iters_done, stop);
+cudaError_t launch_sweep_done(int *sweep, int *iters_done, const int *stop, cudaStream_t s, int64_t *launches) {
+    k_sweep_done<<<1, 1, 0, s>>>(sweep, iters_done, stop);
     ++*launches;
     return cudaGetLastError();
 }
 
+// Device-resident Sinkhorn loop (CUDA graph with a conditional WHILE node, api.cu): the last node of
+// the loop body counts the periods and keeps looping while periods remain and nothing stopped.
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, int *done, const int *n, const int *stop) {
+    const int d = *done + 1;
+    *done = d;
+    cudaGraphSetConditional(h, (d < *n && !*(volatile const int *)stop) ? 1u : 0u);
+}
+cudaError_t launch_loop_cond(cudaGraphConditionalHandle h, int *done, const int *n, const int *stop, cudaStream_t s,
+                             int64_t *launches) {
+    k_loop_cond<<<1, 1, 0, s>>>(h, done, n, stop);
+    ++*launches;
+    return cudaGetLastError();
+}
 }  // namespace mmot

@@ -133,12 +133,12 @@ def test_vshard_sinkhorn_lockstep(G, kernel, chunk, tol):
 def test_vshard_collective_early_exit(G):
     """tol > 0: the ranks agree on the stop flag and leave the sweep loop after the same sweep as
     the oracle's stop rule (A7)."""
-    l, N, eta, tol = 3, 20_000, 0.05, 1e-7
+    l, N, eta, tol = 3, 20_000, 0.1, 1e-6
     h = mmot_inputs.grid_h(N)
     mus = mmot_inputs.c4_marginals(8, N, l, width=200)
     sl = _slices(N, G)
-    _, t_ref, res_ref = osk.sinkhorn(mus, h, eta, 500, tol=tol, domain="plain")
-    assert t_ref < 500
+    _, t_ref, res_ref = osk.sinkhorn(mus, h, eta, 500, tol=tol, domain="plain", engine="subset")
+    assert t_ref < 500 and t_ref % 8 != 0   # the stop falls between two polls of the flag
 
     def rank(r, group):
         lo, hi = sl[r]
