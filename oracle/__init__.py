@@ -29,9 +29,11 @@ Everything is plain fp64 and follows the paper (``P:n`` = line n of PAPER.md):
                  residual (Algorithm 1 line 7 generalised), cost W.
 * ``comonotone`` -- closed-form unregularised optimum W_0 of the 1-D pairwise
                  L1 MMOT (sanity pin: W_eta >= W_0).
+* ``grid2d``  -- O6: 2-D grids (§4.1), l = 3: the product written out, Algorithm 6
+                 (FTVP_2d) with Algorithm 2 inside, the 2-D cost (reading A21), Sinkhorn.
 * ``points``  -- non-uniform 1-D grids (footnote P:182): one decay per grid edge;
                  brute force and the subset recursion with per-edge weights, Sinkhorn driver.
 
 Every function and the tests that pin it are listed in DESIGN.md §2b; none is "parity unpinned".
 """
-from . import dense, paper3, regions, subset, sinkhorn, comonotone  # noqa: F401
+from . import dense, paper3, regions, subset, sinkhorn, comonotone, grid2d  # noqa: F401
