@@ -403,9 +403,8 @@ def run_mmot(args, cfg):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     clocks.begin()
-    ctx.profile(True)
-    ctx.profile_read()
     launches0 = ctx.launches
+    graphs0 = ctx.graph_solves
     barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
@@ -416,9 +415,16 @@ def run_mmot(args, cfg):
     barrier()
     clk = clocks.stop()
     ms_local = ev0.elapsed_time(ev1) / args.steps
+    launches = (ctx.launches - launches0) // args.steps
+    graph_solves = ctx.graph_solves - graphs0
+    # per-update kernel time: one more step with CUDA events around every product on the context
+    # stream (profiling switches the solve to the host-issued launch sequence: the same kernels)
+    ctx.profile(True)
+    ctx.profile_read()
+    step()
+    torch.cuda.synchronize()
     prof = ctx.profile_read()
     ctx.profile(False)
-    launches = (ctx.launches - launches0) // args.steps
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -446,9 +452,12 @@ def run_mmot(args, cfg):
             traffic = json.load(open(tf)).get(cfg.name)
         except Exception:
             traffic = None
+    step_frac = alg_bytes * iters_done * l / (ms / 1e3) / 1e9 / peak
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "fused update (ops + scan + apply of one J_k)",
                 "alg_bytes_per_launch": alg_bytes, "ms_per_launch": upd_ms, "peak_source": peak_src,
+                "ms_per_launch_source": "CUDA events around each update of one profiled step after the timed region",
+                "step_level_frac": step_frac,
                 "phase_ms_per_update": {k: v / max(sum(prof["mode_n"].values()), 1) for k, v in prof["phase_ms"].items()}}
 
     # end-to-end through the C ABI with HOST buffers (pinned), copies inside the timed region
@@ -502,6 +511,8 @@ def run_mmot(args, cfg):
             "e2e": e2e,
             "clocks": clk,
             "gpu_launches": int(launches),
+            "device_loop": ("CUDA graph, conditional WHILE node (one graph launch per solve)" if graph_solves
+                            else "persistent kernel" if ctx.info["kernel"] == "persistent" else "host-issued launches"),
             "iters_per_s": iters_done / (ms / 1e3),
             "iters_done": iters_done,
             "W": state["W"],

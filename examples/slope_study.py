@@ -6,7 +6,7 @@ of the difference of the two transport plans and the empirical complexity slopes
 regression of log time on log N (paper: O(N^1.01) fast, O(N^3.01) dense, on MATLAB / i5-1135G7).
 
 The paper's grid N = 10..160 is latency-bound on a GPU (a whole 100-sweep solve is one persistent
-launch), so the GPU slope is also fitted on large N (1e5..1e8), where the product is HBM-bound.
+launch), so the GPU slope is also fitted on large N (3e7..3e8), where the product is HBM-bound.
 
     python examples/slope_study.py [--out profiles/r02_slope_study.json]
 """
@@ -27,7 +27,7 @@ import mmot_inputs  # noqa: E402
 
 EPS, T, L = 0.1, 100, 3
 PAPER_N = [10, 20, 40, 80, 160]
-LARGE_N = [100_000, 1_000_000, 10_000_000, 100_000_000]
+LARGE_N = [1_000_000, 30_000_000, 100_000_000, 300_000_000]
 
 
 def u01_marginals(N: int, seed: int) -> np.ndarray:

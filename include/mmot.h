@@ -84,8 +84,15 @@ typedef enum {
     MMOT_KERNEL_AUTO = 0,
     MMOT_KERNEL_TWO_WALK = 1,
     MMOT_KERNEL_SINGLE_WALK = 2,
-    MMOT_KERNEL_PERSISTENT = 3  /* one warp per instance, all sweeps in one launch (the batched kernel,
+    MMOT_KERNEL_PERSISTENT = 3, /* one warp per instance, all sweeps in one launch (the batched kernel,
                                    batch = 1); AUTO picks it for l <= 5, N <= 4096, MMOT_F64, chunk = 0 */
+    MMOT_KERNEL_STABLE = 4      /* stabilised family (a8): the recurrence in the LOG domain (states carried
+                                   as logarithms; the paper's log-domain stabilisation, Remark 1 P:138-151,
+                                   Algorithm 5), one warp per instance walking the whole grid:
+                                   any eta / dynamic range, O(N) latency per product.  Uniform grids,
+                                   single (mmot_create) and batched (mmot_create_batched) contexts.  The
+                                   other families fall back to it automatically, see
+                                   mmot_stable_fallback_count. */
 } mmot_kernel;
 
 typedef struct {
@@ -147,6 +154,21 @@ MMOT_API mmot_status mmot_create_points(int l, int64_t N, double eta, const doub
 MMOT_API mmot_status mmot_create_batched_points(int l, int64_t N, int64_t batch, const double *eta_host,
                                                 const double *x_host, mmot_dtype dt, const mmot_opts *opts,
                                                 void *cuda_stream, mmot_ctx **out);
+
+/* 2-D grids (§4.1).  An N1 x N2 uniform mesh of
+ * [x_min, x_max] x [y_min, y_max] (endpoints included; vertical spacing h1 = (x_max-x_min)/(N1-1),
+ * horizontal h2 = (y_max-y_min)/(N2-1)), the L1 cost c = sum_{p<q} (|i1_p - i1_q| h1 + |i2_p - i2_q| h2)
+ * and K = lambda1^{E1} lambda2^{E2}.  l = 3 (the paper's 2-D case; other l:
+ * EUNSUPPORTED).  Every vector argument of the compute calls is the flattened mesh, COLUMN-MAJOR:
+ * x[i1 + N1 i2], N1 N2 elements.  The product is Algorithm 6's structure: an
+ * outer recurrence over the N2 columns whose states are column vectors, with six batched 1-D
+ * FTVP-1 products per column (grid2d.cu); mmot_cost returns W = <phi_3, (C.K) x phi_1 x phi_2>
+ * (the 2-D cost product the paper omits, by dual numbers, A21).
+ * Plain fp64 (EOVERFLOW on loss of range); mmot_sinkhorn / mmot_marginal / mmot_cost /
+ * mmot_init_uniform (phi = 1/(N1 N2)) as for mmot_create. */
+typedef struct { double x_min, x_max, y_min, y_max; } mmot_grid2d;
+MMOT_API mmot_status mmot_create_2d(int l, int64_t N1, int64_t N2, double eta, mmot_grid2d grid, mmot_dtype dt,
+                                    const mmot_opts *opts, void *cuda_stream, mmot_ctx **out);
 
 /* Create rank `rank`'s part of ONE instance sharded over `world` GPUs by contiguous grid
  * chunks (BASELINE C4 on 1/2/4/8 GPUs).  The rank owns global points
@@ -252,7 +274,8 @@ MMOT_API const char *mmot_last_error(const mmot_ctx *ctx);
 MMOT_API int mmot_version(void);
 
 /* Launch plan of a context: grid points per chain P, number of chains, kernel family actually
- * used (MMOT_KERNEL_TWO_WALK or MMOT_KERNEL_SINGLE_WALK).  Any output pointer may be NULL. */
+ * used (MMOT_KERNEL_* value; 5 = 2-D grid, with chain_len = N1 and nchains = N2).  Any output
+ * pointer may be NULL. */
 MMOT_API mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t *nchains, int *kernel);
 
 /* Kernel-launch counter: number of CUDA kernels this context has launched so far. */
@@ -267,6 +290,25 @@ MMOT_API int64_t mmot_launch_count(const mmot_ctx *ctx);
  * therefore synchronises the stream once), and sharded contexts return MMOT_EPRECISION on every
  * rank.  Returns how many calls of this context were redone. */
 MMOT_API int64_t mmot_fallback_count(const mmot_ctx *ctx);
+
+/* Range fallback (a8).  When a product of the plain fp64 families leaves the fp64 range
+ * (MMOT_EOVERFLOW: e.g. disjoint supports at small eta, where J_k spans e^-8000 .. e^+4000),
+ * mmot_sinkhorn / mmot_marginal / mmot_cost of single-instance contexts redo the call from its
+ * inputs on the stabilised family (MMOT_KERNEL_STABLE), and batched contexts redo exactly the failed
+ * instances; uniform grids, not sharded (sharded contexts still return MMOT_EOVERFLOW on every rank).
+ * Marginal / cost calls of a batched context that needed it run on the stabilised family from then
+ * on.  MMOT_NO_STABLE=1 disables it.  Returns how many calls were redone. */
+MMOT_API int64_t mmot_stable_fallback_count(const mmot_ctx *ctx);
+
+/* Device-resident driver.  Single-process contexts run the sweep loop of mmot_sinkhorn as
+ * ONE launch of a cached CUDA graph whose conditional WHILE node repeats a captured period of
+ * sweeps (tol > 0: check_every sweeps ending with the residual check and the device stop rule;
+ * tol <= 0: the periodic steady state after the first sweep(s)) until the sweeps are done or the
+ * device stop flag is set -- no host round trip per sweep.  The persistent family runs a whole solve
+ * in one kernel; sharded contexts and profiled contexts (mmot_profile_enable) keep host-issued
+ * launches (MMOT_NO_GRAPH=1 forces them).  The graph is rebuilt when the vectors passed change.
+ * Returns how many solves of this context used the graph. */
+MMOT_API int64_t mmot_graph_solves(const mmot_ctx *ctx);
 
 /* Benchmark instrumentation.  While enabled, every tensor-vector product records CUDA events
  * on the context stream around its phases.  mmot_profile_read synchronises the stream and

@@ -123,6 +123,10 @@ def load_library():
     lib.mmot_launch_count.restype = ctypes.c_int64
     lib.mmot_fallback_count.argtypes = [vp]
     lib.mmot_fallback_count.restype = ctypes.c_int64
+    lib.mmot_stable_fallback_count.argtypes = [vp]
+    lib.mmot_stable_fallback_count.restype = ctypes.c_int64
+    lib.mmot_graph_solves.argtypes = [vp]
+    lib.mmot_graph_solves.restype = ctypes.c_int64
     lib.mmot_profile_enable.argtypes = [vp, ctypes.c_int]
     lib.mmot_profile_enable.restype = ctypes.c_int
     dp = ctypes.POINTER(ctypes.c_double)
@@ -248,7 +252,7 @@ class Context:
         self.dtype = dtype  # f32: float marginals / marginal outputs (fp32 I/O), fp64 scans; u[] stays float64
         self.h = (self.grid[1] - self.grid[0]) / (self.N - 1) if self.N > 1 else 1.0
         self.stream = stream if stream is not None else torch.cuda.current_stream()
-        kern = {"auto": 0, "two_walk": 1, "single_walk": 2, "persistent": 3}[kernel]
+        kern = {"auto": 0, "two_walk": 1, "single_walk": 2, "persistent": 3, "stable": 4}[kernel]
         opts = _Opts(int(check_every), 0, LOG if repr == "log" else LINEAR, int(chunk), kern)
         ctx = ctypes.c_void_p()
         self.shard = shard
@@ -323,11 +327,21 @@ class Context:
         P, n, k = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
         self._check(self._lib.mmot_info(self._ctx, ctypes.byref(P), ctypes.byref(n), ctypes.byref(k)))
         return dict(chain_len=P.value, nchains=n.value,
-                    kernel={1: "two_walk", 2: "single_walk", 3: "persistent"}[k.value])
+                    kernel={1: "two_walk", 2: "single_walk", 3: "persistent", 4: "stable"}[k.value])
 
     @property
     def launches(self) -> int:
         return int(self._lib.mmot_launch_count(self._ctx))
+
+    @property
+    def stable_fallbacks(self) -> int:
+        """Calls redone on the stabilised (log-domain) family after a product left the fp64 range."""
+        return int(self._lib.mmot_stable_fallback_count(self._ctx))
+
+    @property
+    def graph_solves(self) -> int:
+        """Solves whose sweep loop ran as one device-resident CUDA graph launch."""
+        return int(self._lib.mmot_graph_solves(self._ctx))
 
     @property
     def fallbacks(self) -> int:

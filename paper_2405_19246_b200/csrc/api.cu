@@ -145,6 +145,23 @@ struct mmot_ctx {
     double *vg_tmp = nullptr;               // virtual shards: reduction result staging
     double *shard_mem = nullptr;            // agg_send [2*SZ], agg_all [world*2*SZ], rank_car [2*M] (Dual-sized)
     int exch_error = 0;
+    // stabilised family (MMOT_KERNEL_STABLE, stable.cu): log-domain, one warp per instance
+    bool stable = false;
+    mmot::SPlan sp{};
+    double *st_mem = nullptr;               // eta, g planes, scratch, wout, resid
+    int *st_int = nullptr;                  // status, fail_iter, iters_done, converged, sel  ([5][batch])
+    int *st_shost = nullptr;                // pinned [4][batch]
+    double *st_rhost = nullptr, *st_whost = nullptr;  // pinned [batch]
+    std::vector<double> eta_host;           // per-instance eta (fallback creation)
+    mmot_ctx *st_fb = nullptr;              // stabilised context the plain families fall back to (lazy)
+    int64_t st_fallbacks = 0;               // calls redone on the stabilised family
+    double *u_save = nullptr;               // two-walk LINEAR solves: initial u (for the fallback)
+    // 2-D grids (mmot_create_2d, grid2d.cu): l = 3 on an N1 x N2 mesh, vectors column-major
+    bool g2 = false;
+    int64_t g2N = 0, g2M = 0;               // rows (inner), columns (outer)
+    double g2h1 = 0, g2h2 = 0;              // spacings
+    double *g2_mem = nullptr;               // Fa, Fb, Ga, Gb [4][N1 N2] + transposed scalings [3][N1 N2]
+    void *g2_T = nullptr;                   // Y, st, Gab (Dual-sized)
     // batched contexts (mmot_create_batched)
     bool batched = false;
     int64_t batch = 1;
@@ -171,6 +188,7 @@ struct mmot_ctx {
     int64_t g_launches = 0;     // kernels per graph period (launch accounting)
     int64_t graph_solves = 0;
     bool graph_broken = false;  // capture failed once: host loop from then on
+    cudaStream_t cap_stream = nullptr;  // private stream the loop graph is captured on
     int64_t launches = 0;
     char err[256] = "";
     // profiling (mmot_profile_enable)
@@ -242,11 +260,18 @@ int64_t mmot_launch_count(const mmot_ctx *ctx) { return ctx ? ctx->launches + (c
 
 int64_t mmot_fallback_count(const mmot_ctx *ctx) { return ctx ? ctx->fallbacks : 0; }
 
+int64_t mmot_stable_fallback_count(const mmot_ctx *ctx) {
+    return ctx ? ctx->st_fallbacks + (ctx->fb ? ctx->fb->st_fallbacks : 0) : 0;
+}
+
+int64_t mmot_graph_solves(const mmot_ctx *ctx) { return ctx ? ctx->graph_solves + (ctx->fb ? ctx->fb->graph_solves : 0) : 0; }
+
 mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t *nchains, int *kernel) {
     if (!ctx) { set_err(nullptr, "NULL context"); return MMOT_EINVAL; }
-    if (chain_len) *chain_len = ctx->batched ? ctx->ba.P : ctx->P;
-    if (nchains) *nchains = ctx->batched ? 32 * ctx->batch : ctx->nchunks;
-    if (kernel) *kernel = ctx->batched ? MMOT_KERNEL_PERSISTENT : (ctx->sw ? MMOT_KERNEL_SINGLE_WALK : MMOT_KERNEL_TWO_WALK);
+    if (chain_len) *chain_len = ctx->g2 ? ctx->g2N : ctx->stable ? ctx->N : ctx->batched ? ctx->ba.P : ctx->P;
+    if (nchains) *nchains = ctx->g2 ? ctx->g2M : ctx->stable ? ctx->batch : ctx->batched ? 32 * ctx->batch : ctx->nchunks;
+    if (kernel) *kernel = ctx->g2 ? 5 : ctx->stable ? MMOT_KERNEL_STABLE
+                          : ctx->batched ? MMOT_KERNEL_PERSISTENT : (ctx->sw ? MMOT_KERNEL_SINGLE_WALK : MMOT_KERNEL_TWO_WALK);
     return MMOT_OK;
 }
 
@@ -258,6 +283,15 @@ void mmot_destroy(mmot_ctx *ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     else cudaDeviceSynchronize();
     mmot_destroy(ctx->fb);
+    mmot_destroy(ctx->st_fb);
+    cudaFree(ctx->st_mem);
+    cudaFree(ctx->g2_mem);
+    cudaFree(ctx->g2_T);
+    cudaFree(ctx->st_int);
+    cudaFree(ctx->u_save);
+    if (ctx->st_shost) cudaFreeHost(ctx->st_shost);
+    if (ctx->st_rhost) cudaFreeHost(ctx->st_rhost);
+    if (ctx->st_whost) cudaFreeHost(ctx->st_whost);
     cudaFree(ctx->ws);
     cudaFree(ctx->out_t);
     cudaFree(ctx->sw_end);
@@ -285,6 +319,7 @@ void mmot_destroy(mmot_ctx *ctx) {
     if (ctx->poll_ev) cudaEventDestroy(ctx->poll_ev);
     if (ctx->g_exec) cudaGraphExecDestroy(ctx->g_exec);
     if (ctx->g_graph) cudaGraphDestroy(ctx->g_graph);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     for (cudaEvent_t e : ctx->pool) cudaEventDestroy(e);
     cudaSetDevice(cur);
     delete ctx;
@@ -292,6 +327,8 @@ void mmot_destroy(mmot_ctx *ctx) {
 
 static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype dt, const mmot_opts *opts,
                                  void *cuda_stream, mmot_ctx **out, bool allow_persistent, bool exact_chains = false);
+static mmot_status create_stable(int l, int64_t N, int64_t batch, const double *eta_host, mmot_grid grid, mmot_dtype dt,
+                                 const mmot_opts *opts, void *cuda_stream, mmot_ctx **out);
 
 mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, mmot_dtype dt, const mmot_opts *opts,
                         void *cuda_stream, mmot_ctx **out) {
@@ -324,7 +361,7 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
     }
     if (dt != MMOT_F64 && dt != MMOT_F32) { set_err(nullptr, "bad dtype"); return MMOT_EINVAL; }
     if (opts && (opts->check_every < 0 || opts->chunk < 0 || (opts->repr != MMOT_LOG && opts->repr != MMOT_LINEAR) ||
-                 opts->kernel < MMOT_KERNEL_AUTO || opts->kernel > MMOT_KERNEL_PERSISTENT)) {
+                 opts->kernel < MMOT_KERNEL_AUTO || opts->kernel > MMOT_KERNEL_STABLE)) {
         set_err(nullptr, "bad opts");
         return MMOT_EINVAL;
     }
@@ -333,6 +370,10 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
     // no per-update kernel latency)
     const int kern = opts ? opts->kernel : MMOT_KERNEL_AUTO;
     const int chunk = opts ? opts->chunk : 0;
+    if (kern == MMOT_KERNEL_STABLE) {
+        if (!allow_persistent) { set_err(nullptr, "sharded contexts cannot use the stabilised family"); return MMOT_EUNSUPPORTED; }
+        return create_stable(l, N, 1, &eta, grid, dt, opts, cuda_stream, out);
+    }
     if (kern == MMOT_KERNEL_PERSISTENT && !allow_persistent) {
         set_err(nullptr, "sharded contexts cannot use the persistent kernel");
         return MMOT_EUNSUPPORTED;
@@ -545,6 +586,75 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
     return MMOT_OK;
 }
 
+// Stabilised family (stable.cu): `batch` instances (1 for mmot_create), log-domain scalings g.
+static mmot_status create_stable(int l, int64_t N, int64_t batch, const double *eta_host, mmot_grid grid, mmot_dtype dt,
+                                 const mmot_opts *opts, void *cuda_stream, mmot_ctx **out) {
+    mmot_ctx *c = new mmot_ctx();
+    c->l = l;
+    c->N = N;
+    c->eta = eta_host[0];
+    c->grid = grid;
+    c->dt = dt;
+    if (opts) c->opts = *opts;
+    c->opts.kernel = MMOT_KERNEL_STABLE;
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    cudaGetDevice(&c->device);
+    c->h = N > 1 ? (grid.x_max - grid.x_min) / (double)(N - 1) : 1.0;
+    c->stable = true;
+    c->batch = batch;
+    c->eta_host.assign(eta_host, eta_host + batch);
+    const int M = 1 << (l - 1);
+    mmot::SPlan &sp = c->sp;
+    sp.l = l;
+    sp.N = N;
+    sp.batch = batch;
+    sp.h = c->h;
+    sp.hc = c->h;
+    sp.slots = std::min<int64_t>(batch, 148 * 8);
+    sp.scratch_per_warp = 2 * N * M;
+    const size_t nd = (size_t)batch + (size_t)l * batch * N + (size_t)sp.slots * sp.scratch_per_warp + 2 * (size_t)batch;
+    bool ok = cudaMalloc(&c->st_mem, nd * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&c->st_int, 5 * (size_t)batch * sizeof(int)) == cudaSuccess &&
+              cudaMallocHost(&c->st_shost, 4 * (size_t)batch * sizeof(int)) == cudaSuccess &&
+              cudaMallocHost(&c->st_rhost, (size_t)batch * sizeof(double)) == cudaSuccess &&
+              cudaMallocHost(&c->st_whost, (size_t)batch * sizeof(double)) == cudaSuccess &&
+              cudaMallocHost(&c->hsc, sizeof(DevScalars)) == cudaSuccess &&
+              cudaMallocHost(&c->hstop, 2 * sizeof(int)) == cudaSuccess &&
+              cudaMalloc(&c->ws, sizeof(DevScalars)) == cudaSuccess;
+    if (!ok) {
+        set_err(c, "stabilised workspace allocation failed (%zu B)", nd * sizeof(double));
+        snprintf(g_err, sizeof g_err, "%s", c->err);
+        mmot_destroy(c);
+        return MMOT_ENOMEM;
+    }
+    c->dsc = static_cast<DevScalars *>(c->ws);
+    double *p = c->st_mem;
+    sp.eta = p;
+    p += batch;
+    for (int q = 0; q < l; ++q) {
+        sp.g[q] = p;
+        p += (size_t)batch * N;
+    }
+    sp.scratch = p;
+    p += (size_t)sp.slots * sp.scratch_per_warp;
+    sp.wout = p;
+    sp.resid = p + batch;
+    sp.status = c->st_int;
+    sp.fail_iter = c->st_int + batch;
+    sp.iters_done = c->st_int + 2 * batch;
+    sp.converged = c->st_int + 3 * batch;
+    if (cudaMemcpyAsync(const_cast<double *>(sp.eta), eta_host, (size_t)batch * sizeof(double), cudaMemcpyHostToDevice,
+                        c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->dsc, 0, sizeof(DevScalars), c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess) {
+        set_err(c, "stabilised workspace init failed");
+        mmot_destroy(c);
+        return MMOT_ECUDA;
+    }
+    *out = c;
+    return MMOT_OK;
+}
+
 mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *eta_host, mmot_grid grid,
                                 mmot_dtype dt, const mmot_opts *opts, void *cuda_stream, mmot_ctx **out) {
     if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
@@ -562,6 +672,7 @@ mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *e
         set_err(nullptr, "bad opts");
         return MMOT_EINVAL;
     }
+    if (opts && opts->kernel == MMOT_KERNEL_STABLE) return create_stable(l, N, batch, eta_host, grid, dt, opts, cuda_stream, out);
     if (l > 5) { set_err(nullptr, "batched contexts support l <= 5 in this build"); return MMOT_EUNSUPPORTED; }
     mmot_ctx *c = new mmot_ctx();
     c->l = l;
@@ -575,6 +686,7 @@ mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *e
     c->h = N > 1 ? (grid.x_max - grid.x_min) / (double)(N - 1) : 1.0;
     c->batched = true;
     c->batch = batch;
+    c->eta_host.assign(eta_host, eta_host + batch);
     mmot::BatchArgs &a = c->ba;
     a.l = l;
     a.N = N;
@@ -685,6 +797,66 @@ mmot_status mmot_create_batched_points(int l, int64_t N, int64_t batch, const do
     return MMOT_OK;
 }
 
+mmot_status mmot_create_2d(int l, int64_t N1, int64_t N2, double eta, mmot_grid2d grid, mmot_dtype dt,
+                           const mmot_opts *opts, void *cuda_stream, mmot_ctx **out) {
+    if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
+    *out = nullptr;
+    if (l < 2 || l > 8) { set_err(nullptr, "l=%d outside [2,8]", l); return MMOT_EINVAL; }
+    if (N1 < 1 || N2 < 1) { set_err(nullptr, "N1, N2 must be >= 1"); return MMOT_EINVAL; }
+    if (!(eta > 0) || !isfinite(eta)) { set_err(nullptr, "eta must be finite and > 0"); return MMOT_EINVAL; }
+    if (!isfinite(grid.x_min) || !isfinite(grid.x_max) || !isfinite(grid.y_min) || !isfinite(grid.y_max) ||
+        (N1 > 1 && !(grid.x_max > grid.x_min)) || (N2 > 1 && !(grid.y_max > grid.y_min))) {
+        set_err(nullptr, "grid must satisfy x_max > x_min, y_max > y_min");
+        return MMOT_EINVAL;
+    }
+    if (dt != MMOT_F64 && dt != MMOT_F32) { set_err(nullptr, "bad dtype"); return MMOT_EINVAL; }
+    if (opts && (opts->check_every < 0 || (opts->repr != MMOT_LOG && opts->repr != MMOT_LINEAR))) {
+        set_err(nullptr, "bad opts");
+        return MMOT_EINVAL;
+    }
+    if (l != 3) { set_err(nullptr, "2-D grids: l = 3 in this build (the paper's 2-D case, P:712-979)"); return MMOT_EUNSUPPORTED; }
+    mmot_ctx *c = new mmot_ctx();
+    c->l = l;
+    c->N = N1 * N2;
+    c->eta = eta;
+    c->dt = dt;
+    if (opts) c->opts = *opts;
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    cudaGetDevice(&c->device);
+    c->g2 = true;
+    c->g2N = N1;
+    c->g2M = N2;
+    c->g2h1 = N1 > 1 ? (grid.x_max - grid.x_min) / (double)(N1 - 1) : 1.0;
+    c->g2h2 = N2 > 1 ? (grid.y_max - grid.y_min) / (double)(N2 - 1) : 1.0;
+    c->h = c->g2h1;
+    c->grid = mmot_grid{grid.x_min, grid.x_max};
+    const int64_t n = c->N;
+    const size_t tsz = ((size_t)6 * n + (size_t)18 * n + (size_t)(std::max(N1, N2) + 1) * std::max(N1, N2) + 64) *
+                       sizeof(mmot::Dual);
+    bool ok = cudaMalloc(&c->g2_mem, (size_t)7 * n * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&c->g2_T, tsz) == cudaSuccess &&
+              cudaMalloc(&c->ws, sizeof(DevScalars) + (size_t)(std::max(N1, N2) + 64) * sizeof(double)) == cudaSuccess &&
+              cudaMallocHost(&c->hsc, sizeof(DevScalars)) == cudaSuccess &&
+              cudaMallocHost(&c->hstop, 2 * sizeof(int)) == cudaSuccess &&
+              cudaEventCreateWithFlags(&c->poll_ev, cudaEventDisableTiming) == cudaSuccess;
+    for (int q = 0; q < l && ok; ++q) ok = cudaMalloc(&c->lin[q], (size_t)n * sizeof(double)) == cudaSuccess;
+    if (!ok) {
+        set_err(c, "2-D workspace allocation failed");
+        snprintf(g_err, sizeof g_err, "%s", c->err);
+        mmot_destroy(c);
+        return MMOT_ENOMEM;
+    }
+    c->dsc = static_cast<DevScalars *>(c->ws);
+    c->partial = reinterpret_cast<double *>(static_cast<char *>(c->ws) + ((sizeof(DevScalars) + 255) / 256) * 256);
+    if (cudaMemsetAsync(c->dsc, 0, sizeof(DevScalars), c->stream) != cudaSuccess) {
+        set_err(c, "memset failed");
+        mmot_destroy(c);
+        return MMOT_ECUDA;
+    }
+    *out = c;
+    return MMOT_OK;
+}
+
 mmot_status mmot_create_points(int l, int64_t N, double eta, const double *x_host, mmot_dtype dt, const mmot_opts *opts,
                                void *cuda_stream, mmot_ctx **out) {
     if (!out) { set_err(nullptr, "out is NULL"); return MMOT_EINVAL; }
@@ -734,6 +906,7 @@ mmot_status mmot_create_points(int l, int64_t N, double eta, const double *x_hos
 }  // extern "C"
 
 static mmot_status reset_scalars(mmot_ctx *c);
+static mmot_status sync_report(mmot_ctx *c);
 
 // Upload an array of l device pointers (for the batched import / export kernels).
 static mmot_status bat_upload_ptrs(mmot_ctx *c, const void *const *u, int slot) {
@@ -751,6 +924,135 @@ static mmot_status bat_import(mmot_ctx *c, const void *const *u) {
     if (st) return st;
     CK(c, mmot::launch_bat_convert(c->ba, c->bat_ptrs, 1, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
     return MMOT_OK;
+}
+
+// Per-instance report arrays [status | fail_iter | iters_done | converged] (ints) and residuals ->
+// the batch report (max sweeps, max residual, all converged, first failing instance).
+static mmot_status aggregate_report(mmot_ctx *c, int64_t B, const int *sh, const double *rh, double tol,
+                                    mmot_report *rep) {
+    int status = 0, fail = -1, done = 0, conv = 1;
+    double res = 0.0;
+    for (int64_t b = 0; b < B; ++b) {
+        if (sh[b] && !status) { status = sh[b]; fail = sh[B + b]; }
+        done = std::max(done, sh[2 * B + b]);
+        conv &= sh[3 * B + b];
+        res = std::max(res, rh[b]);  // NaN (never computed) propagates as "not a number"
+        if (isnan(rh[b])) res = NAN;
+    }
+    if (rep) {
+        rep->iters_done = done;                      // max over instances
+        rep->residual = tol > 0 ? res : NAN;         // max over instances
+        rep->converged = tol > 0 && conv;            // all instances
+        rep->status = status;
+        rep->fail_iter = status ? fail : -1;
+    }
+    if (status) set_err(c, "%s (an instance failed at sweep %d)", mmot_strerror((mmot_status)status), fail);
+    return (mmot_status)status;
+}
+
+// ---------------------------------------------------------------------------------------
+// Stabilised family (stable.cu).  u (caller layout, repr per opts) <-> g = log phi; sel: device
+// mask of the instances to touch (null: all).
+static mmot_status st_import(mmot_ctx *c, const void *const *u, const int *sel) {
+    for (int q = 0; q < c->l; ++q) {
+        if (!u[q]) { set_err(c, "u[%d] is NULL", q); return MMOT_EINVAL; }
+        CK(c, mmot::launch_st_convert(static_cast<const double *>(u[q]), c->sp.g[q], c->batch, c->N, sel,
+                                      c->opts.repr == MMOT_LOG ? 0 : 1, c->stream, &c->launches));
+    }
+    return MMOT_OK;
+}
+static mmot_status st_export(mmot_ctx *c, void *const *u, const int *sel) {
+    for (int q = 0; q < c->l; ++q)
+        CK(c, mmot::launch_st_convert(c->sp.g[q], static_cast<double *>(u[q]), c->batch, c->N, sel,
+                                      c->opts.repr == MMOT_LOG ? 0 : 2, c->stream, &c->launches));
+    return MMOT_OK;
+}
+
+// Sinkhorn on the stabilised family from u_in into u_out (may alias).  sel_host (optional): the
+// instances to run; the per-instance results are left in st_shost / st_rhost.  report_all = false:
+// the caller merges them (no aggregate, returns MMOT_OK unless the call itself failed).
+static mmot_status st_sinkhorn(mmot_ctx *c, const double *const *mu, int iters, double tol, const void *const *u_in,
+                               void *const *u_out, mmot_report *rep, const int *sel_host, bool report_all = true) {
+    const int l = c->l;
+    const int64_t B = c->batch, n = B * c->N;
+    mmot_status st = reset_scalars(c);
+    if (st) return st;
+    for (int q = 0; q < l; ++q) {
+        if (!u_in[q] || !u_out[q]) { set_err(c, "u[%d] is NULL", q); return MMOT_EINVAL; }
+        CK(c, mmot::launch_check(mu[q], n, 0, &c->dsc->flags[q], nullptr, c->stream, &c->launches));
+        CK(c, mmot::launch_bat_min_mass(mu[q], B, c->N, &c->dsc->mass[q], c->stream, &c->launches));
+        CK(c, mmot::launch_check(static_cast<const double *>(u_in[q]), n, c->opts.repr == MMOT_LOG ? 1 : 0,
+                                 &c->dsc->flags[l + q], nullptr, c->stream, &c->launches));
+    }
+    CK(c, mmot::launch_check_finish(c->dsc->flags, c->dsc->mass, 2 * l, l, &c->dsc->status, &c->dsc->stop,
+                                    &c->dsc->fail_iter, c->stream, &c->launches));
+    if ((st = sync_report(c))) return st;
+    if (c->hsc->status) {
+        if (rep) { rep->status = c->hsc->status; rep->fail_iter = 0; }
+        set_err(c, "%s", mmot_strerror((mmot_status)c->hsc->status));
+        return (mmot_status)c->hsc->status;
+    }
+    int *sel = nullptr;
+    if (sel_host) {
+        sel = c->st_int + 4 * B;
+        CK(c, cudaMemcpyAsync(sel, sel_host, (size_t)B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    }
+    CK(c, cudaMemsetAsync(c->st_int, 0, 4 * (size_t)B * sizeof(int), c->stream));
+    if ((st = st_import(c, u_in, sel))) return st;
+    mmot::SPlan sp = c->sp;
+    for (int q = 0; q < l; ++q) sp.mu[q] = mu[q];
+    sp.iters = iters;
+    sp.tol = tol;
+    sp.check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
+    sp.sel = sel;
+    CK(c, mmot::launch_stable(sp, 0, c->stream, &c->launches));
+    if ((st = st_export(c, u_out, sel))) return st;
+    CK(c, cudaMemcpyAsync(c->st_shost, c->st_int, 4 * (size_t)B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaMemcpyAsync(c->st_rhost, sp.resid, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    if (!report_all) return MMOT_OK;
+    return aggregate_report(c, B, c->st_shost, c->st_rhost, tol, rep);
+}
+
+static mmot_status st_marginal(mmot_ctx *c, int k, const void *const *u, void *out) {
+    mmot_status st = st_import(c, u, nullptr);
+    if (st) return st;
+    CK(c, cudaMemsetAsync(c->st_int, 0, 4 * (size_t)c->batch * sizeof(int), c->stream));
+    mmot::SPlan sp = c->sp;
+    sp.k = k;
+    sp.out = static_cast<double *>(out);
+    CK(c, mmot::launch_stable(sp, 1, c->stream, &c->launches));
+    return MMOT_OK;
+}
+
+static mmot_status st_cost(mmot_ctx *c, const void *const *u, double *W) {
+    mmot_status st = st_import(c, u, nullptr);
+    if (st) return st;
+    CK(c, cudaMemsetAsync(c->st_int, 0, 4 * (size_t)c->batch * sizeof(int), c->stream));
+    CK(c, mmot::launch_stable(c->sp, 2, c->stream, &c->launches));
+    CK(c, cudaMemcpyAsync(c->st_whost, c->sp.wout, (size_t)c->batch * sizeof(double), cudaMemcpyDeviceToHost,
+                          c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    memcpy(W, c->st_whost, (size_t)c->batch * sizeof(double));
+    return MMOT_OK;
+}
+
+// The plain families fall back to the stabilised one when a product leaves the fp64 range
+// (MMOT_EOVERFLOW): the call is redone from its inputs on a stabilised context of the same problem
+// (created on first use).  Uniform grids only (the stabilised family has no per-edge weights).
+static mmot_status ensure_stable(mmot_ctx *c) {
+    if (c->st_fb) return MMOT_OK;
+    if (c->eta_host.empty()) c->eta_host.assign(1, c->eta);
+    mmot_opts o = c->opts;
+    o.kernel = MMOT_KERNEL_STABLE;
+    mmot_status st = create_stable(c->l, c->N, (int64_t)c->eta_host.size(), c->eta_host.data(), c->grid, MMOT_F64, &o,
+                                   c->stream, &c->st_fb);
+    if (st) set_err(c, "stabilised fallback context: %s", mmot_last_error(nullptr));
+    return st;
+}
+
+static bool can_stabilise(const mmot_ctx *c) {
+    return !c->sharded && !c->pts_lam && !c->ba.lam && !c->stable && getenv("MMOT_NO_STABLE") == nullptr;
 }
 
 static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters, double tol, void *const *u,
@@ -782,33 +1084,54 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
     a.tol = tol;
     a.check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
     CK(c, mmot::launch_batched(a, 0, c->stream, &c->launches));
-    st = bat_upload_ptrs(c, const_cast<const void *const *>(u), 0);
-    if (st) return st;
-    CK(c, mmot::launch_bat_convert(c->ba, c->bat_ptrs, 0, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
     CK(c, cudaMemcpyAsync(c->bat_shost, c->ba.status, 4 * (size_t)c->batch * sizeof(int), cudaMemcpyDeviceToHost,
                           c->stream));
     CK(c, cudaMemcpyAsync(c->bat_rhost, c->ba.resid, (size_t)c->batch * sizeof(double), cudaMemcpyDeviceToHost,
                           c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
-    int status = 0, fail = -1, done = 0, conv = 1;
-    double res = 0.0;
     const int64_t B = c->batch;
-    for (int64_t b = 0; b < B; ++b) {
-        if (c->bat_shost[b] && !status) { status = c->bat_shost[b]; fail = c->bat_shost[B + b]; }
-        done = std::max(done, c->bat_shost[2 * B + b]);
-        conv &= c->bat_shost[3 * B + b];
-        res = std::max(res, c->bat_rhost[b]);  // NaN (never computed) propagates as "not a number"
-        if (isnan(c->bat_rhost[b])) res = NAN;
+    // instances whose products left the fp64 range: redo them on the stabilised family, from this
+    // call's u (still untouched: the export below comes after the stabilised import)
+    std::vector<int> sel((size_t)B, 0);
+    int64_t nfail = 0;
+    for (int64_t b = 0; b < B; ++b)
+        if (c->bat_shost[b] == MMOT_EOVERFLOW) { sel[(size_t)b] = 1; ++nfail; }
+    const bool redo = nfail > 0 && can_stabilise(c);
+    if (redo) {
+        if ((st = ensure_stable(c))) return st;
+        mmot_ctx *sc = c->st_fb;
+        ++c->st_fallbacks;
+        // import first (reads the caller's u), then this context's export, then the stabilised solve
+        int *dsel = sc->st_int + 4 * B;
+        CK(c, cudaMemcpyAsync(dsel, sel.data(), (size_t)B * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        if ((st = st_import(sc, const_cast<const void *const *>(u), dsel))) return st;
     }
-    if (rep) {
-        rep->iters_done = done;                      // max over instances
-        rep->residual = tol > 0 ? res : NAN;         // max over instances
-        rep->converged = tol > 0 && conv;            // all instances
-        rep->status = status;
-        rep->fail_iter = status ? fail : -1;
+    st = bat_upload_ptrs(c, const_cast<const void *const *>(u), 0);
+    if (st) return st;
+    CK(c, mmot::launch_bat_convert(c->ba, c->bat_ptrs, 0, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
+    if (redo) {
+        mmot_ctx *sc = c->st_fb;
+        CK(c, cudaMemsetAsync(sc->st_int, 0, 4 * (size_t)B * sizeof(int), c->stream));
+        mmot::SPlan sp = sc->sp;
+        for (int q = 0; q < c->l; ++q) sp.mu[q] = mu[q];
+        sp.iters = iters;
+        sp.tol = tol;
+        sp.check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
+        sp.sel = sc->st_int + 4 * B;
+        CK(c, mmot::launch_stable(sp, 0, c->stream, &sc->launches));
+        if ((st = st_export(sc, u, sp.sel))) return st;
+        CK(c, cudaMemcpyAsync(sc->st_shost, sc->st_int, 4 * (size_t)B * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaMemcpyAsync(sc->st_rhost, sp.resid, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        for (int64_t b = 0; b < B; ++b)
+            if (sel[(size_t)b]) {
+                for (int f = 0; f < 4; ++f) c->bat_shost[f * B + b] = sc->st_shost[f * B + b];
+                c->bat_rhost[b] = sc->st_rhost[b];
+            }
+    } else {
+        CK(c, cudaStreamSynchronize(c->stream));
     }
-    if (status) set_err(c, "%s (an instance failed at sweep %d)", mmot_strerror((mmot_status)status), fail);
-    return (mmot_status)status;
+    return aggregate_report(c, B, c->bat_shost, c->bat_rhost, tol, rep);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1093,17 +1416,23 @@ static mmot_status run_graph_loop(mmot_ctx *c, int period, int n, bool check, do
         CK(c, cudaGraphAddNode(&node, g, nullptr, 0, &np));
         cudaGraph_t body = np.conditional.phGraph_out[0];
         const int64_t l0 = c->launches;
-        CK(c, cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-        SweepState ss = ss0;
+        // capture on a private stream (the caller's may be the legacy default stream, which cannot
+        // be captured); the graph is launched on the context stream
+        if (!c->cap_stream) CK(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+        cudaStream_t user = c->stream;
+        c->stream = c->cap_stream;
         mmot_status st = MMOT_OK;
+        cudaError_t e = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) st = MMOT_ECUDA;
+        SweepState ss = ss0;
         for (int i = 0; i < period && !st; ++i) st = enqueue_sweep(c, 1, check && i + 1 == period, tol, lin, mu, ss);
         if (!st) {
-            cudaError_t e = mmot::launch_loop_cond(h, &c->dsc->g_done, &c->dsc->g_n, &c->dsc->stop, c->stream,
-                                                   &c->launches);
-            if (e != cudaSuccess) { set_err(c, "loop condition: %s", cudaGetErrorString(e)); st = MMOT_ECUDA; }
+            e = mmot::launch_loop_cond(h, &c->dsc->g_done, &c->dsc->g_n, &c->dsc->stop, c->stream, &c->launches);
+            if (e != cudaSuccess) st = MMOT_ECUDA;
         }
         cudaGraph_t cap = nullptr;
-        cudaError_t e = cudaStreamEndCapture(c->stream, &cap);
+        e = cudaStreamEndCapture(c->stream, &cap);
+        c->stream = user;
         if (st || e != cudaSuccess) {
             // capture refused something: forget the graph, clear the error, let the host loop run
             cudaGetLastError();
@@ -1160,6 +1489,13 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
     CK(c, mmot::launch_check_finish(c->dsc->flags, c->dsc->mass, 2 * l, l, &c->dsc->status, &c->dsc->stop,
                                     &c->dsc->fail_iter, c->stream, &c->launches));
     if ((st = shard_agree(c, &c->dsc->stop, 3))) return st;
+    if (!c->sw && c->opts.repr == MMOT_LINEAR && can_stabilise(c)) {
+        // the updates rewrite u in place: keep the input for a stabilised redo
+        if (!c->u_save) CK(c, cudaMalloc(&c->u_save, (size_t)l * c->N * sizeof(double)));
+        for (int q = 0; q < l; ++q)
+            CK(c, cudaMemcpyAsync(c->u_save + (size_t)q * c->N, u[q], (size_t)c->N * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, c->stream));
+    }
     const int check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
     const bool rx = c->rx && (!c->sharded || c->nlev >= 2);
     SweepState ss;
@@ -1204,17 +1540,26 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
             poll_pending = true;
         }
     }
+    // decided before u is written, so that a redo starts from this call's input: the single-walk
+    // precision guard (-> two-walk family) and products beyond the fp64 range (-> stabilised family)
+    if ((st = shard_agree(c, &c->dsc->stop, 6))) return st;
+    if ((st = sync_report(c))) return st;
+    if (c->exch_error) return MMOT_ENCCL;
+    // (an EOVERFLOW of the single walk may itself be the lost precision: redo it on two-walk first)
+    if (c->sw && c->hsc->guard && (!c->hsc->status || c->hsc->status == MMOT_EOVERFLOW)) {
+        if (c->sharded) return guard_tripped(c);
+        ++c->fallbacks;
+        if ((st = ensure_fallback(c))) return st;
+        return sinkhorn_impl(c->fb, mu, iters, tol, u, rep);
+    }
+    if (c->hsc->status == MMOT_EOVERFLOW && can_stabilise(c)) {
+        ++c->st_fallbacks;
+        if ((st = ensure_stable(c))) return st;
+        const void *uin[mmot::kMaxL];
+        for (int q = 0; q < l; ++q) uin[q] = c->u_save ? c->u_save + (size_t)q * c->N : u[q];
+        return st_sinkhorn(c->st_fb, mu, iters, tol, uin, u, rep, nullptr);
+    }
     if (c->sw) {
-        // precision guard: decided before u is written, so a fallback restarts from the same input
-        if ((st = shard_agree(c, &c->dsc->stop, 6))) return st;
-        if ((st = sync_report(c))) return st;
-        // (an EOVERFLOW of the single walk may itself be the lost precision: redo it too)
-        if (c->hsc->guard && (!c->hsc->status || c->hsc->status == MMOT_EOVERFLOW)) {
-            if (c->sharded) return guard_tripped(c);
-            ++c->fallbacks;
-            if ((st = ensure_fallback(c))) return st;
-            return sinkhorn_impl(c->fb, mu, iters, tol, u, rep);
-        }
         for (int q = 0; q < l; ++q)
             CK(c, mmot::launch_from_t(c->lin[q], static_cast<double *>(u[q]), c->N, c->P, c->nchunks, c->nchp,
                                       c->opts.repr == MMOT_LOG ? 2 : 0, c->stream, &c->launches));
@@ -1222,10 +1567,7 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
         for (int q = 0; q < l; ++q)
             CK(c, mmot::launch_log(c->lin[q], static_cast<double *>(u[q]), c->N, c->stream, &c->launches));
     }
-    if ((st = shard_agree(c, &c->dsc->stop, 6))) return st;
-    st = sync_report(c);
-    if (st) return st;
-    if (c->exch_error) return MMOT_ENCCL;
+    CK(c, cudaStreamSynchronize(c->stream));
     const DevScalars &h = *c->hsc;
     if (rep) {
         rep->iters_done = h.iters_done;
@@ -1238,10 +1580,153 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
     return (mmot_status)h.status;
 }
 
+// ---------------------------------------------------------------------------------------
+// 2-D grids (grid2d.cu; §4.1).  Free marginal k, bound marginals k+1, k+2 (mod 3).
+static mmot::G2Plan g2_plan(mmot_ctx *c, int k, const double *const *lin, const double *mu, double *out, int iter,
+                            bool transposed = false) {
+    mmot::G2Plan p{};
+    const int64_t N = transposed ? c->g2M : c->g2N, M = transposed ? c->g2N : c->g2M;
+    const double hi = transposed ? c->g2h2 : c->g2h1, ho = transposed ? c->g2h1 : c->g2h2;
+    p.N = N;
+    p.M = M;
+    for (int a = 0; a <= mmot::kMaxL; ++a) {
+        const int e = a <= 3 ? a * (3 - a) : 0;
+        p.Wi.e[a] = (double)e;
+        p.Wi.w[a] = a <= 3 ? exp(-(double)e * hi / c->eta) : 0.0;
+    }
+    p.wo1 = exp(-2.0 * ho / c->eta);  // lambda2^{1*2}
+    p.wo2 = p.wo1;                    // lambda2^{2*1}
+    p.a = lin[(k + 1) % 3];
+    p.b = lin[(k + 2) % 3];
+    p.phik = lin[k];
+    p.muk = mu;
+    p.outk = out;
+    const int64_t n = c->N;
+    p.Fa = c->g2_mem;
+    p.Fb = c->g2_mem + n;
+    p.Ga = c->g2_mem + 2 * n;
+    p.Gb = c->g2_mem + 3 * n;
+    mmot::Dual *T = static_cast<mmot::Dual *>(c->g2_T);
+    p.Y = T;
+    p.st = T + 6 * n;
+    p.Gab = T + 24 * n;
+    p.partial = c->partial;
+    p.status = &c->dsc->status;
+    p.stop = &c->dsc->stop;
+    p.fail_iter = &c->dsc->fail_iter;
+    p.iter = iter;
+    return p;
+}
+
+static mmot_status g2_linear(mmot_ctx *c, const void *const *u, const double **lin) {
+    for (int q = 0; q < c->l; ++q) {
+        if (!u[q]) { set_err(c, "u[%d] is NULL", q); return MMOT_EINVAL; }
+        if (c->opts.repr == MMOT_LOG) {
+            CK(c, mmot::launch_exp(static_cast<const double *>(u[q]), c->lin[q], c->N, c->stream, &c->launches));
+            lin[q] = c->lin[q];
+        } else {
+            lin[q] = static_cast<const double *>(u[q]);
+        }
+    }
+    return MMOT_OK;
+}
+
+static mmot_status g2_sinkhorn(mmot_ctx *c, const double *const *mu, int iters, double tol, void *const *u,
+                               mmot_report *rep) {
+    const int l = c->l;
+    mmot_status st = reset_scalars(c);
+    if (st) return st;
+    for (int q = 0; q < l; ++q) {
+        CK(c, mmot::launch_check(mu[q], c->N, 0, &c->dsc->flags[q], &c->dsc->mass[q], c->stream, &c->launches));
+        CK(c, mmot::launch_check(static_cast<const double *>(u[q]), c->N, c->opts.repr == MMOT_LOG ? 1 : 0,
+                                 &c->dsc->flags[l + q], nullptr, c->stream, &c->launches));
+    }
+    CK(c, mmot::launch_check_finish(c->dsc->flags, c->dsc->mass, 2 * l, l, &c->dsc->status, &c->dsc->stop,
+                                    &c->dsc->fail_iter, c->stream, &c->launches));
+    const double *lin[mmot::kMaxL];
+    if ((st = g2_linear(c, const_cast<const void *const *>(u), lin))) return st;
+    const int check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
+    bool poll_pending = false;
+    for (int t = 1; t <= iters; ++t) {
+        if (poll_pending && cudaEventQuery(c->poll_ev) == cudaSuccess) {
+            poll_pending = false;
+            if (*c->hstop) break;
+        }
+        for (int k = 0; k < l; ++k) {
+            mmot::G2Plan p = g2_plan(c, k, lin, mu[k], const_cast<double *>(lin[k]), t);
+            CK(c, mmot::launch_g2_product(p, mmot::MODE_UPD, c->stream, &c->launches));
+        }
+        CK(c, mmot::launch_sweep_done(&c->dsc->sweep, &c->dsc->iters_done, &c->dsc->stop, c->stream, &c->launches));
+        if (tol > 0 && (t % check_every == 0 || t == iters)) {
+            for (int k = 0; k + 1 < l; ++k) {
+                mmot::G2Plan p = g2_plan(c, k, lin, mu[k], nullptr, t);
+                CK(c, mmot::launch_g2_product(p, mmot::MODE_RES, c->stream, &c->launches));
+                CK(c, mmot::launch_sum(c->partial, c->g2N, &c->dsc->res_acc, 1.0, k > 0, &c->dsc->stop, c->stream,
+                                       &c->launches));
+            }
+            CK(c, mmot::launch_resid_finish(&c->dsc->res_acc, tol, &c->dsc->sweep, &c->dsc->resid, &c->dsc->iters_done,
+                                            &c->dsc->converged, &c->dsc->stop, c->stream, &c->launches));
+            if (!poll_pending && t % 8 == 0) {
+                CK(c, cudaMemcpyAsync(c->hstop, &c->dsc->stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+                CK(c, cudaEventRecord(c->poll_ev, c->stream));
+                poll_pending = true;
+            }
+        }
+    }
+    if (c->opts.repr == MMOT_LOG)
+        for (int q = 0; q < l; ++q)
+            CK(c, mmot::launch_log(lin[q], static_cast<double *>(u[q]), c->N, c->stream, &c->launches));
+    if ((st = sync_report(c))) return st;
+    const DevScalars &h = *c->hsc;
+    if (rep) {
+        rep->iters_done = h.iters_done;
+        rep->residual = tol > 0 && h.iters_done > 0 ? h.resid : NAN;
+        rep->converged = h.converged;
+        rep->status = h.status;
+        rep->fail_iter = h.status ? h.fail_iter : -1;
+    }
+    if (h.status) set_err(c, "%s (sweep %d)", mmot_strerror((mmot_status)h.status), h.fail_iter);
+    return (mmot_status)h.status;
+}
+
+static mmot_status g2_marginal(mmot_ctx *c, int k, const void *const *u, void *out) {
+    mmot_status st = reset_scalars(c);
+    if (st) return st;
+    const double *lin[mmot::kMaxL];
+    if ((st = g2_linear(c, u, lin))) return st;
+    mmot::G2Plan p = g2_plan(c, k, lin, nullptr, static_cast<double *>(out), 0);
+    CK(c, mmot::launch_g2_product(p, mmot::MODE_MARG, c->stream, &c->launches));
+    return MMOT_OK;
+}
+
+// W = h1 <phi_3, hatJ^(1)> + h2 <phi_3, hatJ^(2)>: the lambda1 tangent on the mesh, the lambda2
+// tangent on the transposed mesh (reading A21; the paper omits the 2-D cost product).
+static mmot_status g2_cost(mmot_ctx *c, const void *const *u, double *W) {
+    mmot_status st = reset_scalars(c);
+    if (st) return st;
+    const double *lin[mmot::kMaxL];
+    if ((st = g2_linear(c, u, lin))) return st;
+    mmot::G2Plan p = g2_plan(c, 2, lin, nullptr, nullptr, 0);
+    CK(c, mmot::launch_g2_product(p, mmot::MODE_COST, c->stream, &c->launches));
+    CK(c, mmot::launch_sum(c->partial, c->g2N, &c->dsc->W, c->g2h1, 0, &c->dsc->stop, c->stream, &c->launches));
+    const double *tr[mmot::kMaxL];
+    for (int q = 0; q < 3; ++q) {
+        double *dst = c->g2_mem + (4 + q) * c->N;
+        CK(c, mmot::launch_g2_transpose(lin[q], dst, c->g2N, c->g2M, c->stream, &c->launches));
+        tr[q] = dst;
+    }
+    mmot::G2Plan pt = g2_plan(c, 2, tr, nullptr, nullptr, 0, true);
+    CK(c, mmot::launch_g2_product(pt, mmot::MODE_COST, c->stream, &c->launches));
+    CK(c, mmot::launch_sum(c->partial, c->g2M, &c->dsc->W, c->g2h2, 1, &c->dsc->stop, c->stream, &c->launches));
+    if ((st = sync_report(c))) return st;
+    *W = c->hsc->W;
+    return (mmot_status)c->hsc->status;
+}
+
 // MMOT_F32 contexts take float marginals and write float marginal outputs; the scans run in fp64
 // on widened copies (on B200 an fp32 scan would need per-state exponents and issue
 // more instructions than the fp64 one).
-static int64_t io_elems(const mmot_ctx *c) { return c->N * (c->batched ? c->batch : 1); }
+static int64_t io_elems(const mmot_ctx *c) { return c->N * (c->batched || c->stable ? c->batch : 1); }
 static mmot_status f32_ensure(mmot_ctx *c) {
     if (c->f32_mem) return MMOT_OK;
     CK(c, cudaMalloc(&c->f32_mem, (size_t)(c->l + 1) * io_elems(c) * sizeof(double)));
@@ -1278,6 +1763,9 @@ mmot_status mmot_marginal(mmot_ctx *c, int k, const void *const *u, void *out) {
 }
 
 static mmot_status marginal_f64(mmot_ctx *c, int k, const void *const *u, void *out) {
+    if (c->g2) return g2_marginal(c, k, u, out);
+    if (c->stable) return st_marginal(c, k, u, out);
+    if (c->batched && c->st_fb) return st_marginal(c->st_fb, k, u, out);  // a solve of it needed the log domain
     if (c->batched) {
         mmot_status st = bat_import(c, u);
         if (st) return st;
@@ -1296,16 +1784,24 @@ static mmot_status marginal_f64(mmot_ctx *c, int k, const void *const *u, void *
     Plan p = make_plan(c, k, lin, nullptr, c->sw ? c->out_t : static_cast<double *>(out), 0);
     CK(c, mmot::launch_product(p, mmot::MODE_MARG, c->stream, &c->launches, prof_events(c, mmot::MODE_MARG)));
     if (c->exch_error) return MMOT_ENCCL;
-    if (c->sw) {
-        // precision guard (synchronises once)
-        if ((st = shard_agree(c, &c->dsc->stop, 6))) return st;
-        if ((st = sync_report(c))) return st;
-        if (c->hsc->guard) {
-            if (c->sharded) return guard_tripped(c);
-            ++c->fallbacks;
-            if ((st = ensure_fallback(c))) return st;
-            return marginal_f64(c->fb, k, u, out);
-        }
+    // precision guard (single walk) and range check (synchronises once): a product that left the
+    // fp64 range is redone on the stabilised family
+    if ((st = shard_agree(c, &c->dsc->stop, 6))) return st;
+    if ((st = sync_report(c))) return st;
+    if (c->sw && c->hsc->guard) {
+        if (c->sharded) return guard_tripped(c);
+        ++c->fallbacks;
+        if ((st = ensure_fallback(c))) return st;
+        return marginal_f64(c->fb, k, u, out);
+    }
+    if (c->hsc->status == MMOT_EOVERFLOW && can_stabilise(c)) {
+        ++c->st_fallbacks;
+        if ((st = ensure_stable(c))) return st;
+        return st_marginal(c->st_fb, k, u, out);
+    }
+    if (c->hsc->status) {
+        set_err(c, "%s", mmot_strerror((mmot_status)c->hsc->status));
+        return (mmot_status)c->hsc->status;
     }
     if (c->sw)
         CK(c, mmot::launch_from_t(c->out_t, static_cast<double *>(out), c->N, c->P, c->nchunks, c->nchp, 0, c->stream,
@@ -1328,6 +1824,8 @@ mmot_status mmot_sinkhorn(mmot_ctx *c, const void *const *marginals, int iters, 
         mmot_status st = f32_widen(c, marginals, mu);
         if (st) return st;
     }
+    if (c->g2) return g2_sinkhorn(c, mu, iters, tol, u, rep);
+    if (c->stable) return st_sinkhorn(c, mu, iters, tol, const_cast<const void *const *>(u), u, rep, nullptr);
     if (c->batched) return bat_sinkhorn(c, mu, iters, tol, u, rep);
     return sinkhorn_impl(c, mu, iters, tol, u, rep);
 }
@@ -1362,7 +1860,10 @@ mmot_status mmot_sinkhorn_host(mmot_ctx *c, const void *const *marginals_host, i
         mu[q] = c->stage_mu[q];
         ud[q] = c->stage_u[q];
     }
-    mmot_status st = c->batched ? bat_sinkhorn(c, mu, iters, tol, ud, rep) : sinkhorn_impl(c, mu, iters, tol, ud, rep);
+    mmot_status st = c->g2        ? g2_sinkhorn(c, mu, iters, tol, ud, rep)
+                     : c->stable  ? st_sinkhorn(c, mu, iters, tol, const_cast<const void *const *>(ud), ud, rep, nullptr)
+                     : c->batched ? bat_sinkhorn(c, mu, iters, tol, ud, rep)
+                                  : sinkhorn_impl(c, mu, iters, tol, ud, rep);
     for (int q = 0; q < c->l; ++q)
         CK(c, cudaMemcpyAsync(u_host[q], c->stage_u[q], bytes, cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
@@ -1372,6 +1873,9 @@ mmot_status mmot_sinkhorn_host(mmot_ctx *c, const void *const *marginals_host, i
 mmot_status mmot_cost(mmot_ctx *c, const void *const *u, double *W) {
     if (!c || !u || !W) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
     cudaSetDevice(c->device);
+    if (c->g2) return g2_cost(c, u, W);
+    if (c->stable) return st_cost(c, u, W);
+    if (c->batched && c->st_fb) return st_cost(c->st_fb, u, W);
     if (c->batched) {
         mmot_status st = bat_import(c, u);
         if (st) return st;
@@ -1407,6 +1911,11 @@ mmot_status mmot_cost(mmot_ctx *c, const void *const *u, double *W) {
         ++c->fallbacks;
         if ((st = ensure_fallback(c))) return st;
         return mmot_cost(c->fb, u, W);
+    }
+    if (c->hsc->status == MMOT_EOVERFLOW && can_stabilise(c)) {
+        ++c->st_fallbacks;
+        if ((st = ensure_stable(c))) return st;
+        return st_cost(c->st_fb, u, W);
     }
     *W = c->hsc->W;
     return (mmot_status)c->hsc->status;

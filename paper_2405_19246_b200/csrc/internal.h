@@ -152,6 +152,51 @@ struct VPtrs {
 };
 cudaError_t launch_vreduce(const VPtrs &src, int world, int n, int op, void *out, cudaStream_t s, int64_t *launches);
 
+// Stabilised family (stable.cu): log-domain subset recurrence, one warp per instance.
+struct SPlan {
+    int l;
+    int64_t N, batch;
+    double h;                    // grid spacing
+    const double *eta;           // device [batch]
+    double *g[kMaxL];            // device [batch][N] log scalings (in/out)
+    const double *mu[kMaxL];     // device [batch][N] marginals (linear)
+    double *scratch;             // device [slots][scratch_per_warp]
+    int64_t scratch_per_warp;    // 2 N 2^(l-1) doubles
+    int64_t slots;               // resident warps (scratch slots)
+    const int *sel;              // device [batch] 1 = process (null: all instances)
+    int iters, check_every, k;
+    double tol;
+    double *out, *wout;          // marginal [batch][N] / cost [batch]
+    double hc;                   // cost factor h
+    int *status, *fail_iter, *iters_done, *converged;  // device [batch]
+    double *resid;               // device [batch]
+};
+// what: 0 Sinkhorn (iters sweeps), 1 marginal k -> out, 2 cost -> wout
+cudaError_t launch_stable(const SPlan &sp, int what, cudaStream_t s, int64_t *launches);
+// in -> out for the selected instances: op 0 copy, 1 log, 2 exp
+cudaError_t launch_st_convert(const double *in, double *out, int64_t batch, int64_t N, const int *sel, int op,
+                              cudaStream_t s, int64_t *launches);
+
+// 2-D grids (grid2d.cu, §4.1): l = 3 on an N x M mesh, column-major vectors x[i1 + N i2].
+struct G2Plan {
+    int64_t N, M;                // rows (inner dimension, lambda1), columns (outer, lambda2)
+    Weights Wi;                  // inner weights w_a = lambda1^{a(3-a)} and e_a (cost tangent)
+    double wo1, wo2;             // outer weights lambda2^{1*2}, lambda2^{2*1}
+    const double *a, *b;         // the two bound scalings
+    const double *phik, *muk;    // free marginal's scaling / target (per mode)
+    double *outk;                // marginal output or the new phi_k
+    double *Fa, *Fb, *Ga, *Gb;   // [N M] column recursions
+    void *Y;                     // [6][M][N] inner products (T)
+    void *st;                    // [6 M][N][3] inner suffix states (T)
+    void *Gab;                   // [M + 1][N] output-space suffix states (T)
+    double *partial;             // [N] per-row partial sums (residual / cost)
+    int *status, *stop, *fail_iter;
+    int iter;
+};
+cudaError_t launch_g2_product(const G2Plan &p, int mode, cudaStream_t s, int64_t *launches);
+cudaError_t launch_g2_transpose(const double *in, double *out, int64_t N, int64_t M, cudaStream_t s,
+                                int64_t *launches);
+
 // Elementwise helpers.
 // fp32 <-> fp64 (to_f64: float in -> double out, else double in -> float out)
 cudaError_t launch_convert(const void *in, void *out, int64_t n, int to_f64, cudaStream_t s, int64_t *launches);

@@ -758,7 +758,9 @@ __device__ __forceinline__ double epilogue(const T &J, const double *cur, int la
     constexpr int S = slab_s(NB);
     const double jv = value_of(J);
     if (MODE == MODE_MARG) {
-        return cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * jv;
+        const double ph = cur[(AV::IPHI * 32 + lane) * (S + 1) + jx];
+        bad |= ph > 0.0 && !finite_positive(jv);  // J left the fp64 range (all terms are positive)
+        return ph * jv;
     } else if (MODE == MODE_UPD) {
         const double mu = cur[(AV::IMU * 32 + lane) * (S + 1) + jx];
         const double q = div_nr1(mu, jv);
@@ -766,11 +768,14 @@ __device__ __forceinline__ double epilogue(const T &J, const double *cur, int la
         bad |= nz && !finite_positive(q);  // J = 0 / inf / NaN or mu/J out of range
         return nz ? q : 0.0;
     } else if (MODE == MODE_RES) {
-        acc += fabs(cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * jv - cur[(AV::IMU * 32 + lane) * (S + 1) + jx]);
+        const double ph = cur[(AV::IPHI * 32 + lane) * (S + 1) + jx];
+        bad |= ph > 0.0 && !finite_positive(jv);
+        acc += fabs(ph * jv - cur[(AV::IMU * 32 + lane) * (S + 1) + jx]);
         return 0.0;
     } else {
-        if constexpr (sizeof(T) == sizeof(Dual))
-            acc += cur[(AV::IPHI * 32 + lane) * (S + 1) + jx] * reinterpret_cast<const Dual &>(J).d;
+        const double ph = cur[(AV::IPHI * 32 + lane) * (S + 1) + jx];
+        bad |= ph > 0.0 && !finite_positive(jv);
+        if constexpr (sizeof(T) == sizeof(Dual)) acc += ph * reinterpret_cast<const Dual &>(J).d;
         return 0.0;
     }
 }
@@ -1301,7 +1306,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
             const double jv = value_of(J);
             double o = 0.0;
             if (MODE == MODE_MARG) {
-                o = cur[(AV::IPHI * S + j) * 32 + lane] * jv;
+                const double ph = cur[(AV::IPHI * S + j) * 32 + lane];
+                bad |= ph > 0.0 && !finite_positive(jv);  // J left the fp64 range
+                o = ph * jv;
             } else if (MODE == MODE_UPD) {
                 const double mu = cur[(AV::IMU * S + j) * 32 + lane];
                 const double q = div_nr0(mu, jv);  // 2^-46 relative: inside the 1e-10 parity tolerance
@@ -1309,10 +1316,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
                 bad |= nz && !finite_positive(q);
                 o = nz ? q : 0.0;
             } else if (MODE == MODE_RES) {
-                acc += fabs(cur[(AV::IPHI * S + j) * 32 + lane] * jv - cur[(AV::IMU * S + j) * 32 + lane]);
+                const double ph = cur[(AV::IPHI * S + j) * 32 + lane];
+                bad |= ph > 0.0 && !finite_positive(jv);
+                acc += fabs(ph * jv - cur[(AV::IMU * S + j) * 32 + lane]);
             } else {
-                if constexpr (sizeof(T) == sizeof(Dual))
-                    acc += cur[(AV::IPHI * S + j) * 32 + lane] * reinterpret_cast<const Dual &>(J).d;
+                const double ph = cur[(AV::IPHI * S + j) * 32 + lane];
+                bad |= ph > 0.0 && !finite_positive(jv);
+                if constexpr (sizeof(T) == sizeof(Dual)) acc += ph * reinterpret_cast<const Dual &>(J).d;
             }
             if (AV::kOut) outp[j * 32] = o;
             if constexpr (NEXT) {

@@ -162,10 +162,12 @@ def test_data_errors(bad, code):
     assert ei.value.name == code
 
 
-def test_overflow_reported():
+def test_overflow_reported_without_stabilised_fallback(monkeypatch):
     """Plain fp64 scalings cannot represent disjoint supports at eta = 1e-4 (the kernel between the
-    supports underflows to 0, so phi = mu / 0): the run stops with EOVERFLOW and the sweep index
-    (the analogue of the paper's unstabilised failure)."""
+    supports underflows to 0, so phi = mu / 0): with the range fallback disabled (MMOT_NO_STABLE=1)
+    the run stops with EOVERFLOW and the sweep index (the analogue of the paper's unstabilised
+    failure); tests/test_gpu_stable.py covers the default, stabilised behaviour."""
+    monkeypatch.setenv("MMOT_NO_STABLE", "1")
     N = 400
     x = np.arange(N) / (N - 1)
     mus = np.stack([(x < 0.3).astype(float), (x > 0.7).astype(float), np.ones(N)])
@@ -208,11 +210,12 @@ def test_argument_errors():
 
 
 @pytest.mark.parametrize("N,eta", [(400, 1e-4), (12000, 1e-3)])
-def test_overflow_reported_by_persistent_kernel(N, eta):
+def test_overflow_reported_by_persistent_kernel(N, eta, monkeypatch):
     """Disjoint supports at small eta: J_k between the supports is below e^-708 relative to the
     chain scale (the cost of crossing the gap is 0.8 / eta), beyond what per-chain exponents of
-    the scalings can absorb -- the persistent kernel reports EOVERFLOW with the sweep, like the
-    plain fp64 families, instead of returning garbage (range of the stabilisation)."""
+    the scalings can absorb -- with the range fallback disabled the persistent kernel reports
+    EOVERFLOW with the sweep, like the plain fp64 families, instead of returning garbage."""
+    monkeypatch.setenv("MMOT_NO_STABLE", "1")
     x = np.arange(N) / (N - 1)
     mus = np.stack([(x < 0.3).astype(float), (x > 0.7).astype(float), np.ones(N)])
     mus /= mus.sum(axis=1, keepdims=True)

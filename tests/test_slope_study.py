@@ -18,8 +18,15 @@ import slope_study  # noqa: E402
 
 
 def test_slope_study_table1():
-    res = slope_study.run(paper_n=[10, 20, 40, 80, 160], large_n=[1_000_000, 10_000_000, 100_000_000])
+    """Large-N slope fitted on 3e7 .. 3e8 points: the bandwidth-bound regime (smaller N still carries
+    fixed per-update latencies)."""
+    res = slope_study.run(paper_n=[10, 20, 40, 80, 160], large_n=[1_000_000, 30_000_000, 100_000_000, 300_000_000])
+    out = os.environ.get("SLOPE_OUT")
+    if out:
+        import json
+        with open(out, "w") as f:
+            json.dump(res, f, indent=1)
     for r in res["rows"]:
         assert r["plan_diff_F"] <= 1e-14, r
     assert 2.5 <= res["dense_slope"] <= 3.5, res["dense_slope"]
-    assert 0.85 <= res["gpu_slope_large_n"] <= 1.15, res["large_n"]
+    assert 0.9 <= res["gpu_slope_large_n"] <= 1.1, res["large_n"]
