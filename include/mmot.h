@@ -300,6 +300,16 @@ MMOT_API int64_t mmot_fallback_count(const mmot_ctx *ctx);
  * on.  MMOT_NO_STABLE=1 disables it.  Returns how many calls were redone. */
 MMOT_API int64_t mmot_stable_fallback_count(const mmot_ctx *ctx);
 
+/* All-marginals residual.  The residual check of mmot_sinkhorn (sum over k < l-1 of
+ * ||phi_k J_k - mu_k||_1, Algorithm 1 line 7, generalised) needs every J_k on the same
+ * end-of-sweep vectors.  Two-walk contexts with l <= 5 (uniform grid, one process) evaluate them in
+ * ONE pass of the subset recurrence over all l scalings (2^l states: the states without marginal k
+ * are exactly update k's states, so each J_k is a combine over the subsets without k) instead of
+ * l-1 products, in a workspace of its own, so the update sequence keeps its fused operators.  Other
+ * families keep the l-1 residual products (the persistent kernel folds the k = 0 term into the next
+ * sweep).  MMOT_NO_ALLRES=1 disables it.  Returns how many checks used the single pass. */
+MMOT_API int64_t mmot_allres_checks(const mmot_ctx *ctx);
+
 /* Device-resident driver.  Single-process contexts run the sweep loop of mmot_sinkhorn as
  * ONE launch of a cached CUDA graph whose conditional WHILE node repeats a captured period of
  * sweeps (tol > 0: check_every sweeps ending with the residual check and the device stop rule;

@@ -14,8 +14,9 @@ phi <- u / (K x psi x varphi) etc. (eqs. 2D 1-3), W = <varphi, (C.K) 
   Algorithm 2 (FTVP-1, oracle/paper3.py) as the inner 1-D product along columns.
 * ``cost_2d``       -- W.  The paper omits the 2-D cost product (P:938: "similar idea ... omitted");
   reading (A21): C.K = (C1.K1) (x) K2 + K1 (x) (C2.K2), so the first term is Algorithm 6
-  with the inner FTVP-1 replaced by FTVP-2 (Algorithm 3, the 1-D cost-weighted product)
-  and the second is the same on the transposed mesh (rows <-> columns, h1 <-> h2).
+  with the inner FTVP-1 replaced by a 1-D cost-weighted product (the role of Algorithm 3, P:555-594;
+  evaluated by O4's positive tangent because Algorithm 3 cancels for small lambda) and the second is
+  the same on the transposed mesh (rows <-> columns, h1 <-> h2).
 * ``sinkhorn_2d``   -- the generalized Sinkhorn iteration, Gauss-Seidel order.
 """
 from __future__ import annotations
@@ -120,14 +121,28 @@ def _transpose(x, N: int, M: int) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(M, N).T).reshape(-1)
 
 
+def _cost_inner(h: float):
+    """1-D cost-weighted product h sum E lambda^E x_i y_j (the role of Algorithm 3's FTVP-2).  Algorithm 3
+    forms the E-weights from absolute index sums and loses all accuracy for small lambda (1 - 3e-8 at
+    lambda = e^-10, 90 % at e^-50; tests/test_oracle_grid2d.py), so the positive tangent recursion of
+    O4 (oracle/subset.c, pinned against the dense (E.K) product) serves as the inner product."""
+    from . import regions, subset
+
+    def inner(x, y, lam):
+        w = regions.edge_weights_lambda(3, lam)
+        _, jh = subset.marginal_product([x, y, np.ones_like(x)], 2, w, want_hat=True)
+        return h * jh
+    return inner
+
+
 def cost_2d(phis, N: int, M: int, h1: float, h2: float, eps: float) -> float:
     """W = <varphi, (C.K) x phi x psi> in O(NM): C.K = (C1.K1)(x)K2 + K1(x)(C2.K2)
-    (reading A21); each term is Algorithm 6 with Algorithm 3's cost-weighted inner product (FTVP-2,
-    which carries its factor h), the second on the transposed mesh."""
+    (reading A21); each term is Algorithm 6 with a cost-weighted inner product (`_cost_inner`), the
+    second on the transposed mesh."""
     lam1, lam2 = math.exp(-h1 / eps), math.exp(-h2 / eps)
-    t1 = _ftvp_2d(phis[0], phis[1], lam1, lam2, N, M, lambda x, y, lam: paper3.ftvp2(x, y, lam, h1))
+    t1 = _ftvp_2d(phis[0], phis[1], lam1, lam2, N, M, _cost_inner(h1))
     tr = [_transpose(p, N, M) for p in phis]
-    t2 = _ftvp_2d(tr[0], tr[1], lam2, lam1, M, N, lambda x, y, lam: paper3.ftvp2(x, y, lam, h2))
+    t2 = _ftvp_2d(tr[0], tr[1], lam2, lam1, M, N, _cost_inner(h2))
     return float(np.dot(phis[2], t1) + np.dot(tr[2], t2))
 
 

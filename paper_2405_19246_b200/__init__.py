@@ -40,6 +40,11 @@ class _Grid(ctypes.Structure):
     _fields_ = [("x_min", ctypes.c_double), ("x_max", ctypes.c_double)]
 
 
+class _Grid2d(ctypes.Structure):
+    _fields_ = [("x_min", ctypes.c_double), ("x_max", ctypes.c_double), ("y_min", ctypes.c_double),
+                ("y_max", ctypes.c_double)]
+
+
 class _Opts(ctypes.Structure):
     _fields_ = [("check_every", ctypes.c_int), ("residual_mode", ctypes.c_int),
                 ("repr", ctypes.c_int), ("chunk", ctypes.c_int), ("kernel", ctypes.c_int)]
@@ -71,6 +76,9 @@ def load_library():
     lib.mmot_create_batched.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
                                         _Grid, ctypes.c_int, ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
     lib.mmot_create_batched.restype = ctypes.c_int
+    lib.mmot_create_2d.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, _Grid2d, ctypes.c_int,
+                                   ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
+    lib.mmot_create_2d.restype = ctypes.c_int
     lib.mmot_create_points.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
                                        ctypes.c_int, ctypes.POINTER(_Opts), vp, ctypes.POINTER(vp)]
     lib.mmot_create_points.restype = ctypes.c_int
@@ -125,6 +133,8 @@ def load_library():
     lib.mmot_fallback_count.restype = ctypes.c_int64
     lib.mmot_stable_fallback_count.argtypes = [vp]
     lib.mmot_stable_fallback_count.restype = ctypes.c_int64
+    lib.mmot_allres_checks.argtypes = [vp]
+    lib.mmot_allres_checks.restype = ctypes.c_int64
     lib.mmot_graph_solves.argtypes = [vp]
     lib.mmot_graph_solves.restype = ctypes.c_int64
     lib.mmot_profile_enable.argtypes = [vp, ctypes.c_int]
@@ -234,10 +244,12 @@ class Context:
 
     def __init__(self, l: int, N: int, eta, grid=(0.0, 1.0), dtype: str = "f64",
                  repr: str = "log", check_every: int = 0, chunk: int = 0, stream=None,
-                 kernel: str = "auto", batch: Optional[int] = None, shard=None, points=None):
+                 kernel: str = "auto", batch: Optional[int] = None, shard=None, points=None, shape2d=None):
         """Single instance (eta: float), or a batched context (batch=B, eta: B per-instance
         values) whose array arguments are [B][N] planes (mmot_create_batched).  points: N strictly
-        increasing grid coordinates for a non-uniform grid (mmot_create_points / _batched_points)."""
+        increasing grid coordinates for a non-uniform grid (mmot_create_points / _batched_points).
+        shape2d=(N1, N2): a 2-D N1 x N2 mesh (mmot_create_2d, l = 3), N = N1 N2, vectors column-major,
+        grid = (x_min, x_max, y_min, y_max)."""
         import torch
         self._lib = load_library()
         if not torch.cuda.is_available():
@@ -245,6 +257,10 @@ class Context:
         self.batch = None if batch is None else int(batch)
         self.l, self.N = int(l), int(N)
         self.eta = float(eta) if self.batch is None else [float(e) for e in eta]
+        self.shape2d = None if shape2d is None else (int(shape2d[0]), int(shape2d[1]))
+        if self.shape2d is not None:
+            g4 = tuple(float(v) for v in grid) if len(grid) == 4 else (0.0, 1.0, 0.0, 1.0)
+            grid = g4[:2]
         self.grid = (float(grid[0]), float(grid[1]))
         self.repr = repr
         if dtype not in ("f64", "f32"):
@@ -256,6 +272,18 @@ class Context:
         opts = _Opts(int(check_every), 0, LOG if repr == "log" else LINEAR, int(chunk), kern)
         ctx = ctypes.c_void_p()
         self.shard = shard
+        if self.shape2d is not None:
+            N1, N2 = self.shape2d
+            if N1 * N2 != self.N:
+                raise MMOTError(2, f"shape2d {self.shape2d} does not hold N = {self.N} points")
+            st = self._lib.mmot_create_2d(self.l, N1, N2, float(eta), _Grid2d(*g4), F64 if dtype == "f64" else F32,
+                                          ctypes.byref(opts), ctypes.c_void_p(self.stream.cuda_stream),
+                                          ctypes.byref(ctx))
+            if st != 0:
+                raise MMOTError(st, self._lib.mmot_last_error(None).decode())
+            self._ctx = ctx
+            self.shard = None
+            return
         if shard is not None and points is not None:
             raise MMOTError(10, "sharded contexts support uniform grids only")
         if shard is not None:
@@ -327,7 +355,7 @@ class Context:
         P, n, k = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
         self._check(self._lib.mmot_info(self._ctx, ctypes.byref(P), ctypes.byref(n), ctypes.byref(k)))
         return dict(chain_len=P.value, nchains=n.value,
-                    kernel={1: "two_walk", 2: "single_walk", 3: "persistent", 4: "stable"}[k.value])
+                    kernel={1: "two_walk", 2: "single_walk", 3: "persistent", 4: "stable", 5: "grid2d"}[k.value])
 
     @property
     def launches(self) -> int:
@@ -337,6 +365,11 @@ class Context:
     def stable_fallbacks(self) -> int:
         """Calls redone on the stabilised (log-domain) family after a product left the fp64 range."""
         return int(self._lib.mmot_stable_fallback_count(self._ctx))
+
+    @property
+    def allres_checks(self) -> int:
+        """Residual checks evaluated by the single all-marginals pass (NEXT-1)."""
+        return int(self._lib.mmot_allres_checks(self._ctx))
 
     @property
     def graph_solves(self) -> int:

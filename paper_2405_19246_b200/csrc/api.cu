@@ -156,6 +156,18 @@ struct mmot_ctx {
     mmot_ctx *st_fb = nullptr;              // stabilised context the plain families fall back to (lazy)
     int64_t st_fallbacks = 0;               // calls redone on the stabilised family
     double *u_save = nullptr;               // two-walk LINEAR solves: initial u (for the fallback)
+    // NEXT-1: all-marginals residual pass (MODE_ALLRES) -- its own chain layout and scan workspace
+    // for the DP over all l scalings (2^l states)
+    int all_state = 0;                      // 0 untried, 1 ready, -1 unavailable
+    void *all_mem = nullptr;
+    int64_t all_P = 0, all_nchunks = 0;
+    int all_nlev = 0;
+    int64_t all_nlev_n[mmot::kMaxLevels] = {0};
+    void *all_ops_f[mmot::kMaxLevels] = {nullptr}, *all_ops_b[mmot::kMaxLevels] = {nullptr};
+    void *all_car_f[mmot::kMaxLevels] = {nullptr}, *all_car_b[mmot::kMaxLevels] = {nullptr};
+    void *all_car_bi = nullptr;
+    double *all_partial = nullptr;
+    int64_t allres_checks = 0;
     // 2-D grids (mmot_create_2d, grid2d.cu): l = 3 on an N1 x N2 mesh, vectors column-major
     bool g2 = false;
     int64_t g2N = 0, g2M = 0;               // rows (inner), columns (outer)
@@ -260,6 +272,8 @@ int64_t mmot_launch_count(const mmot_ctx *ctx) { return ctx ? ctx->launches + (c
 
 int64_t mmot_fallback_count(const mmot_ctx *ctx) { return ctx ? ctx->fallbacks : 0; }
 
+int64_t mmot_allres_checks(const mmot_ctx *ctx) { return ctx ? ctx->allres_checks : 0; }
+
 int64_t mmot_stable_fallback_count(const mmot_ctx *ctx) {
     return ctx ? ctx->st_fallbacks + (ctx->fb ? ctx->fb->st_fallbacks : 0) : 0;
 }
@@ -285,6 +299,7 @@ void mmot_destroy(mmot_ctx *ctx) {
     mmot_destroy(ctx->fb);
     mmot_destroy(ctx->st_fb);
     cudaFree(ctx->st_mem);
+    cudaFree(ctx->all_mem);
     cudaFree(ctx->g2_mem);
     cudaFree(ctx->g2_T);
     cudaFree(ctx->st_int);
@@ -1328,6 +1343,91 @@ static mmot_status guard_tripped(mmot_ctx *c) {
     return MMOT_EPRECISION;
 }
 
+// NEXT-1: the all-marginals residual pass is available on two-walk contexts with l <= 5 (the DP over
+// all l scalings has 2^l states, NB = l <= 5 kernels), uniform grids, one process.  Lazily allocates
+// its own chain layout (P from the NB = l checkpoint limits) and scan workspace.
+static bool ensure_allres(mmot_ctx *c) {
+    if (c->all_state) return c->all_state > 0;
+    c->all_state = -1;
+    if (c->sw || c->sharded || c->pts_lam || c->batched || c->stable || c->g2 || c->l < 2 || c->l > 5 ||
+        getenv("MMOT_NO_ALLRES") != nullptr)
+        return false;
+    const int NB = c->l;
+    const int64_t pmax = mmot::chunk_max(NB);
+    const int64_t q = mmot::sub_q(NB);
+    int64_t P = (c->N + 148 * 256 - 1) / (148 * 256);
+    if (NB >= 4) P = pmax;
+    P = ((P + q - 1) / q) * q;
+    P = std::max<int64_t>(q, std::min<int64_t>(P, pmax));
+    c->all_P = P;
+    c->all_nchunks = (c->N + P - 1) / P;
+    int64_t n = c->all_nchunks;
+    c->all_nlev = 0;
+    const int grp = mmot::group_of(NB);
+    while (true) {
+        c->all_nlev_n[c->all_nlev++] = n;
+        if (n <= grp || c->all_nlev == mmot::kMaxLevels) break;
+        n = (n + grp - 1) / grp;
+    }
+    const int M = 1 << NB;
+    const size_t opsz = (size_t)(NB + 1) * M, carsz = M;
+    size_t total = 0;
+    size_t off_ops[mmot::kMaxLevels], off_car[mmot::kMaxLevels];
+    for (int i = 0; i < c->all_nlev; ++i) {
+        off_ops[i] = total;
+        total += 2 * (size_t)c->all_nlev_n[i] * opsz;
+        off_car[i] = total;
+        total += 2 * (size_t)c->all_nlev_n[i] * carsz;
+    }
+    const size_t off_bi = total;
+    total += (size_t)c->all_nchunks * carsz;
+    const size_t off_part = total;
+    total += (size_t)c->all_nchunks;
+    if (cudaMalloc(&c->all_mem, total * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    double *base = static_cast<double *>(c->all_mem);
+    for (int i = 0; i < c->all_nlev; ++i) {
+        c->all_ops_f[i] = base + off_ops[i];
+        c->all_ops_b[i] = base + off_ops[i] + (size_t)c->all_nlev_n[i] * opsz;
+        c->all_car_f[i] = base + off_car[i];
+        c->all_car_b[i] = base + off_car[i] + (size_t)c->all_nlev_n[i] * carsz;
+    }
+    c->all_car_bi = base + off_bi;
+    c->all_partial = base + off_part;
+    c->all_state = 1;
+    return true;
+}
+
+static Plan make_plan_all(mmot_ctx *c, const double *const *lin, const double *const *mu, int iter) {
+    Plan p{};
+    p.NB = c->l;
+    p.N = c->N;
+    p.P = c->all_P;
+    p.nchunks = c->all_nchunks;
+    for (int b = 0; b < c->l; ++b) p.bound[b] = lin[b];  // the DP over ALL l scalings, index order
+    for (int k = 0; k + 1 < c->l; ++k) p.mus[k] = mu[k];
+    p.W = c->W;
+    p.nlev = c->all_nlev;
+    for (int i = 0; i < c->all_nlev; ++i) {
+        p.nlev_n[i] = c->all_nlev_n[i];
+        p.ops_f[i] = c->all_ops_f[i];
+        p.ops_b[i] = c->all_ops_b[i];
+        p.car_f[i] = c->all_car_f[i];
+        p.car_b[i] = c->all_car_b[i];
+    }
+    p.car_bi = c->all_car_bi;
+    p.nchp = (c->all_nchunks + 31) / 32 * 32;
+    p.partial = c->all_partial;
+    p.stop = &c->dsc->stop;
+    p.status = &c->dsc->status;
+    p.fail_iter = &c->dsc->fail_iter;
+    p.iter = iter;
+    if (iter > 0) p.sweep = &c->dsc->sweep;
+    return p;
+}
+
 // Host-side state of the update sequence: which chain operators / restricted-scan elements the
 // previous product left behind (they decide the launch configuration of the next update).
 struct SweepState {
@@ -1365,7 +1465,19 @@ static mmot_status enqueue_sweep(mmot_ctx *c, int t, bool check, double tol, con
         }
     }
     CK(c, mmot::launch_sweep_done(&c->dsc->sweep, &c->dsc->iters_done, &c->dsc->stop, c->stream, &c->launches));
-    if (check) {
+    if (check && ensure_allres(c)) {
+        // NEXT-1: every marginal from one pass of the 2^l-state DP (its own workspace, so this
+        // update sequence's operators and carries stay valid)
+        Plan p = make_plan_all(c, lin, mu, t);
+        CK(c, mmot::launch_product(p, mmot::MODE_ALLRES, c->stream, &c->launches, prof_events(c, mmot::MODE_RES)));
+        CK(c, mmot::launch_sum(c->all_partial, c->all_nchunks, &c->dsc->res_acc, 1.0, 0, &c->dsc->stop, c->stream,
+                               &c->launches));
+        ++c->allres_checks;
+        mmot_status st = shard_allreduce(c, &c->dsc->res_acc);
+        if (st) return st;
+        CK(c, mmot::launch_resid_finish(&c->dsc->res_acc, tol, &c->dsc->sweep, &c->dsc->resid, &c->dsc->iters_done,
+                                        &c->dsc->converged, &c->dsc->stop, c->stream, &c->launches));
+    } else if (check) {
         for (int k = 0; k + 1 < l; ++k) {
             Plan p = make_plan(c, k, lin, mu[k], nullptr, t);
             CK(c, mmot::launch_product(p, mmot::MODE_RES, c->stream, &c->launches, prof_events(c, mmot::MODE_RES)));
@@ -1507,7 +1619,9 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
     int t = 1;
     if (graph) {
         const int period = tol > 0 ? check_every : ((rx && (l & 1)) ? 2 : 1);
-        const int warm = tol > 0 ? 0 : period;
+        // (the all-marginals check leaves the update sequence's state alone, so with it the periods
+        // start after one host-issued period, like the fixed-sweep case)
+        const int warm = tol > 0 && !ensure_allres(c) ? 0 : period;
         for (; t <= warm; ++t)
             if ((st = enqueue_sweep(c, t, false, tol, lin, mu, ss))) return st;
         const int n = (iters - warm) / period;

@@ -12,6 +12,8 @@ enum Mode : int {
     MODE_UPD = 1,   // phi_k = mu_k / J_k                        (Sinkhorn update)
     MODE_RES = 2,   // partial[c] = sum |phi_k J_k - mu_k|       (residual)
     MODE_COST = 3,  // partial[c] = sum phi_k * hatJ_k (duals)   (W)
+    MODE_ALLRES = 4,  // NEXT-1: ONE pass of the 2^l-state DP over ALL l scalings (NB = l) gives every
+                      // J_k (combine over the subsets without k); partial[c] = sum_{k<l-1} |phi_k J_k - mu_k|
 };
 
 constexpr int kGroup = 32;  // operators per group of the hierarchical scan when NB <= 3 (one warp)
@@ -35,6 +37,7 @@ struct Plan {
     const double *bound[kMaxL];      // the NB bound scaling vectors, increasing marginal index
     const double *phik;              // phi_k (marg / res / cost)
     const double *muk;               // mu_k (upd / res)
+    const double *mus[kMaxL];        // MODE_ALLRES: mu_0 .. mu_{l-2} (bound[] = all l scalings, NB = l)
     double *outk;                    // out (marg) or phi_k (upd); may alias phik for upd
     Weights W;
     int nlev;

@@ -662,11 +662,12 @@ __device__ __forceinline__ void raise_status(const Plan &p, int st) {
 
 // Vectors staged by the apply phase: the NB bound vectors, then mu_k (update / residual),
 // then phi_k (marginal / residual / cost).
+// MODE_ALLRES: the NB = l scalings, then mu_0 .. mu_{l-2}.
 template <int NB, int MODE>
 struct ApplyVecs {
     static constexpr bool kMu = MODE == MODE_UPD || MODE == MODE_RES;
     static constexpr bool kPhi = MODE == MODE_MARG || MODE == MODE_RES || MODE == MODE_COST;
-    static constexpr int NV = NB + (kMu ? 1 : 0) + (kPhi ? 1 : 0);
+    static constexpr int NV = MODE == MODE_ALLRES ? 2 * NB - 1 : NB + (kMu ? 1 : 0) + (kPhi ? 1 : 0);
     static constexpr int IMU = NB;
     static constexpr int IPHI = NB + (kMu ? 1 : 0);
     static constexpr bool kOut = MODE == MODE_MARG || MODE == MODE_UPD;
@@ -780,6 +781,30 @@ __device__ __forceinline__ double epilogue(const T &J, const double *cur, int la
     }
 }
 
+// NEXT-1 (MODE_ALLRES): with the states of the DP over ALL l scalings (NB = l), the states without
+// marginal k are exactly update k's states, so every J_k at this point is the combine over the
+// subsets S of A_k = {0..l-1} minus k:  J_k = sum_{S in A_k} F[S] H[A_k \ S]  (H = D B_{m+1}: the
+// combine weight w_{|S|+1} = w_{l-1-|S|} is D's entry of A_k \ S).  Returns sum_{k<l-1} |phi_k J_k - mu_k|
+// (Algorithm 1 line 7, generalised) from one pass instead of l-1 products.
+template <int NB, int SL, typename T>
+__device__ __forceinline__ double allres_terms(const T (&F)[1 << NB], const T (&H)[1 << NB],
+                                               const double (&f)[NB > 0 ? NB : 1], const double *cur, int lane, int jx,
+                                               bool &bad) {
+    constexpr int M = 1 << NB;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k + 1 < NB; ++k) {
+        double J = 0.0;
+#pragma unroll
+        for (int S = 0; S < M; ++S)
+            if (!((S >> k) & 1)) J = fma(value_of(F[S]), value_of(H[(M - 1) & ~S & ~(1 << k)]), J);
+        const double ph = f[k];
+        bad |= ph > 0.0 && !finite_positive(J);
+        s += fabs(ph * J - cur[((NB + k) * 32 + lane) * (SL + 1) + jx]);
+    }
+    return s;
+}
+
 // Next-update operator step (fused): the bound values of update k+1 at this point, cyclic bound
 // order (see make_plan); one extended operator walk gives both scan directions (dp.cuh opx_*).
 template <int NB, typename T>
@@ -820,6 +845,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64
     for (int b = 0; b < NB; ++b) vecs[b] = p.bound[b];
     if (AV::kMu) vecs[AV::IMU] = p.muk;
     if (AV::kPhi) vecs[AV::IPHI] = p.phik;
+    if constexpr (MODE == MODE_ALLRES) {
+#pragma unroll
+        for (int k = 0; k + 1 < NB; ++k) vecs[NB + k] = p.mus[k];
+    }
     T wt[NB + 2];
     load_weights<NB, T>(wt, p.W);
     T F[M], st[M];
@@ -920,10 +949,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64
                         slab_f<NB, S>(f, cur, lane, jx);
                         diag_e<NB, T, PTS>(F, wt, p, base + i);
                         dp_place<NB, T>(F, f);
-                        const T J = combine<NB, T>(F, H[i]);
-                        const double o = epilogue<NB, T, MODE>(J, cur, lane, jx, acc, bad);
-                        if (AV::kOut) obuf[lane * (S + 1) + jx] = o;
-                        if constexpr (NEXT) next_ops_step<NB, T>(Gx, wt, f, o, s == 0 && jb == 0 && i == 0);
+                        if constexpr (MODE == MODE_ALLRES) {
+                            acc += allres_terms<NB, S>(F, H[i], f, cur, lane, jx, bad);
+                        } else {
+                            const T J = combine<NB, T>(F, H[i]);
+                            const double o = epilogue<NB, T, MODE>(J, cur, lane, jx, acc, bad);
+                            if (AV::kOut) obuf[lane * (S + 1) + jx] = o;
+                            if constexpr (NEXT) next_ops_step<NB, T>(Gx, wt, f, o, s == 0 && jb == 0 && i == 0);
+                        }
                     }
                 }
             }
@@ -935,7 +968,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_apply(Plan p, int64
         }
     }
     if (bad && live) raise_status(p, 6 /*EOVERFLOW*/);
-    if ((MODE == MODE_RES || MODE == MODE_COST) && live) p.partial[c] = acc;
+    if ((MODE == MODE_RES || MODE == MODE_COST || MODE == MODE_ALLRES) && live) p.partial[c] = acc;
     if constexpr (NEXT) {
         if (live) {
             opx_store<NB, T>(Gx, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
@@ -1813,37 +1846,43 @@ template <int NB, typename T, int MODE, bool NEXT = false>
 static void launch_apply(const Plan &p, int64_t /*nb*/, int /*tpb*/, cudaStream_t s, int64_t *launches) {
     const bool full_ok = p.P % slab_s(NB) == 0;
     const int64_t nfull = full_ok ? p.N / p.P : 0;
-    if (p.lam) {
-        // non-uniform grid (two-walk contexts only; no fused next-update operators)
-        if constexpr (!NEXT) {
-            launch_apply_range<NB, T, MODE, false, true, true>(p, 0, nfull, s, launches);
-            launch_apply_range<NB, T, MODE, false, false, true>(p, nfull, p.nchunks, s, launches);
-        }
-        return;
-    }
-    if (p.sw) {
-        if constexpr (NB <= 4) {
-            bool done = false;
-            if constexpr (NEXT && MODE == MODE_UPD && sizeof(T) == sizeof(double) && NB >= 2) {
-                if (p.nxr) {
-                    launch_sw<NB, T, MODE, false, true>(p, s, launches);
-                    done = true;
-                }
+    if constexpr (MODE == MODE_ALLRES) {
+        // all-marginals residual pass (two-walk layout, uniform grids)
+        launch_apply_range<NB, T, MODE, false, true>(p, 0, nfull, s, launches);
+        launch_apply_range<NB, T, MODE, false, false>(p, nfull, p.nchunks, s, launches);
+    } else {
+        if (p.lam) {
+            // non-uniform grid (two-walk contexts only; no fused next-update operators)
+            if constexpr (!NEXT) {
+                launch_apply_range<NB, T, MODE, false, true, true>(p, 0, nfull, s, launches);
+                launch_apply_range<NB, T, MODE, false, false, true>(p, nfull, p.nchunks, s, launches);
             }
-            if (!done) launch_sw<NB, T, MODE, NEXT>(p, s, launches);
-            if (p.guard && p.sw_end) launch_sw_guard<NB, T>(p, s, launches);
-        }
-        return;
-    }
-    if constexpr (NB <= 3 && sizeof(T) == sizeof(double)) {
-        if (p.P % (2 * sub_q(NB)) == 0 && p.P / (2 * sub_q(NB)) * 2 * (1 << NB) <= kTmemCols && !g_no_tmem) {
-            launch_apply_tm<NB, MODE, NEXT>(p, 0, nfull, s, launches);
-            launch_apply_range<NB, T, MODE, NEXT, false>(p, nfull, p.nchunks, s, launches);
             return;
         }
+        if (p.sw) {
+            if constexpr (NB <= 4) {
+                bool done = false;
+                if constexpr (NEXT && MODE == MODE_UPD && sizeof(T) == sizeof(double) && NB >= 2) {
+                    if (p.nxr) {
+                        launch_sw<NB, T, MODE, false, true>(p, s, launches);
+                        done = true;
+                    }
+                }
+                if (!done) launch_sw<NB, T, MODE, NEXT>(p, s, launches);
+                if (p.guard && p.sw_end) launch_sw_guard<NB, T>(p, s, launches);
+            }
+            return;
+        }
+        if constexpr (NB <= 3 && sizeof(T) == sizeof(double)) {
+            if (p.P % (2 * sub_q(NB)) == 0 && p.P / (2 * sub_q(NB)) * 2 * (1 << NB) <= kTmemCols && !g_no_tmem) {
+                launch_apply_tm<NB, MODE, NEXT>(p, 0, nfull, s, launches);
+                launch_apply_range<NB, T, MODE, NEXT, false>(p, nfull, p.nchunks, s, launches);
+                return;
+            }
+        }
+        launch_apply_range<NB, T, MODE, NEXT, true>(p, 0, nfull, s, launches);
+        launch_apply_range<NB, T, MODE, NEXT, false>(p, nfull, p.nchunks, s, launches);
     }
-    launch_apply_range<NB, T, MODE, NEXT, true>(p, 0, nfull, s, launches);
-    launch_apply_range<NB, T, MODE, NEXT, false>(p, nfull, p.nchunks, s, launches);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -2006,6 +2045,9 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
             }
             break;
         case MODE_RES: launch_apply<NB, T, MODE_RES>(p, nb, tpb, s, launches); break;
+        case MODE_ALLRES:
+            if constexpr (sizeof(T) == sizeof(double)) launch_apply<NB, T, MODE_ALLRES>(p, nb, tpb, s, launches);
+            break;
         default: launch_apply<NB, T, MODE_COST>(p, nb, tpb, s, launches); break;
     }
     if (ev) cudaEventRecord(ev[3], s);

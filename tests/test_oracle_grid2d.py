@@ -56,9 +56,9 @@ def test_transpose_symmetry():
     np.testing.assert_allclose(grid2d._transpose(J, N, M), Jt, rtol=1e-13)
 
 
-@pytest.mark.parametrize("N,M", [(3, 4), (5, 5), (6, 2)])
-def test_cost_2d_equals_plan_cost(N, M):
-    eps = 0.15
+@pytest.mark.parametrize("N,M", [(3, 4), (5, 5), (6, 2), (2, 3)])
+@pytest.mark.parametrize("eps", [0.15, 0.02])
+def test_cost_2d_equals_plan_cost(N, M, eps):
     h1, h2 = 1.0 / (N - 1), 0.5 / (M - 1)
     phis = [_rand(30 + q + N, N * M) for q in range(3)]
     np.testing.assert_allclose(grid2d.cost_2d(phis, N, M, h1, h2, eps),
@@ -75,3 +75,19 @@ def test_sinkhorn_2d_marginals():
     m = grid2d.marginals(phis, N, M, 0.25, 1.0 / 3, eps)
     np.testing.assert_allclose(m[2], mus[2], rtol=1e-13)
     assert abs(m[0].sum() - 1.0) < 1e-13
+
+
+def test_algorithm3_cancels_for_small_lambda():
+    """Why cost_2d does not use Algorithm 3 inside Algorithm 6: FTVP-2 builds the E-weights from
+    absolute index sums, so its relative error grows like lambda^-2 (A21)."""
+    from oracle import dense
+    N = 3
+    rng = np.random.default_rng(1)
+    a, b = rng.uniform(0.1, 1, N), rng.uniform(0.1, 1, N)
+    for lam, bad in ((0.5, False), (math.exp(-50), True)):
+        K = dense.kernel_tensor_lambda(3, N, lam)
+        E = dense.exponent_tensor(3, N)
+        want = dense.contract(E * K, [a, b, np.ones(N)], 2)
+        err = np.max(np.abs(paper3.ftvp2(a, b, lam, 1.0) - want) / want)
+        assert (err > 1e-3) == bad, (lam, err)
+        np.testing.assert_allclose(grid2d._cost_inner(1.0)(a, b, lam), want, rtol=1e-13)
