@@ -198,6 +198,7 @@ struct mmot_ctx {
     cudaGraph_t g_graph = nullptr;
     const void *g_key[2 * mmot::kMaxL + 4] = {nullptr};
     int64_t g_launches = 0;     // kernels per graph period (launch accounting)
+    int64_t g_allres = 0;       // all-marginals residual checks per graph period
     int64_t graph_solves = 0;
     bool graph_broken = false;  // capture failed once: host loop from then on
     cudaStream_t cap_stream = nullptr;  // private stream the loop graph is captured on
@@ -1527,7 +1528,7 @@ static mmot_status run_graph_loop(mmot_ctx *c, int period, int n, bool check, do
         cudaGraphNode_t node;
         CK(c, cudaGraphAddNode(&node, g, nullptr, 0, &np));
         cudaGraph_t body = np.conditional.phGraph_out[0];
-        const int64_t l0 = c->launches;
+        const int64_t l0 = c->launches, a0 = c->allres_checks;
         // capture on a private stream (the caller's may be the legacy default stream, which cannot
         // be captured); the graph is launched on the context stream
         if (!c->cap_stream) CK(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
@@ -1555,6 +1556,8 @@ static mmot_status run_graph_loop(mmot_ctx *c, int period, int n, bool check, do
         if (!(ss == ss0)) { set_err(c, "internal: graph period does not return to its start state"); return MMOT_ECUDA; }
         c->g_launches = c->launches - l0;
         c->launches = l0;
+        c->g_allres = c->allres_checks - a0;  // all-marginals checks per period
+        c->allres_checks = a0;
         CK(c, cudaGraphInstantiate(&c->g_exec, g, 0));
         memcpy(c->g_key, key, sizeof key);
     }
@@ -1563,6 +1566,7 @@ static mmot_status run_graph_loop(mmot_ctx *c, int period, int n, bool check, do
     CK(c, cudaMemcpyAsync(&c->dsc->g_n, &c->hstop[1], sizeof(int), cudaMemcpyHostToDevice, c->stream));
     CK(c, cudaGraphLaunch(c->g_exec, c->stream));
     c->launches += c->g_launches * n;  // upper bound: periods after a stop exit at the condition
+    c->allres_checks += c->g_allres * n;
     ++c->graph_solves;
     return MMOT_OK;
 }
@@ -1623,7 +1627,7 @@ static mmot_status sinkhorn_impl(mmot_ctx *c, const double *const *mu, int iters
         // start after one host-issued period, like the fixed-sweep case)
         const int warm = tol > 0 && !ensure_allres(c) ? 0 : period;
         for (; t <= warm; ++t)
-            if ((st = enqueue_sweep(c, t, false, tol, lin, mu, ss))) return st;
+            if ((st = enqueue_sweep(c, t, tol > 0 && (t % check_every == 0 || t == iters), tol, lin, mu, ss))) return st;
         const int n = (iters - warm) / period;
         if (n >= 1) {
             st = run_graph_loop(c, period, n, tol > 0, tol, lin, mu, ss);

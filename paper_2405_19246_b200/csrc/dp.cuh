@@ -186,8 +186,9 @@ __device__ __forceinline__ void opx_step(T (&G)[NB + 1][1 << NB], const T *wt, c
 }
 
 // Store the prefix operator (w_c Gt_c) and the suffix operator (w_c Gt_{l-c-|V|}) in op_store
-// layout.
-template <int NB, typename T>
+// layout.  LW = l, the marginal count of the weights w_a = lambda^{a(l-a)} = w_{l-a}: NB + 1 for a
+// product's bound set (NB = l - 1), NB for the DP over all l scalings (MODE_ALLRES, NB = l).
+template <int NB, typename T, int LW = NB + 1>
 __device__ __forceinline__ void opx_store(const T (&G)[NB + 1][1 << NB], const T *wt, T *pf, T *pb) {
     constexpr int M = 1 << NB;
 #pragma unroll
@@ -195,7 +196,7 @@ __device__ __forceinline__ void opx_store(const T (&G)[NB + 1][1 << NB], const T
 #pragma unroll
         for (int V = 0; V < M; ++V)
             if (c + pc(V) <= NB) {
-                const int cp = NB + 1 - c - pc(V);
+                const int cp = LW - c - pc(V);
                 pf[c * M + V] = c == 0 ? G[0][V] : mul(wt[c], G[c][V]);
                 const T r = cp > NB ? one_of(T{}) : G[cp][V];
                 pb[c * M + V] = c == 0 ? r : mul(wt[c], r);

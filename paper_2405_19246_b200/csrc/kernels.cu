@@ -54,7 +54,7 @@ __device__ __forceinline__ void diag_e(T (&st)[1 << NB], const T (&wt)[NB + 2], 
     }
 }
 
-template <int NB, typename T, bool PTS = false>
+template <int NB, typename T, bool PTS = false, bool ALL = false>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_ops(Plan p) {
     constexpr int M = 1 << NB;
     constexpr int S = slab_s(NB);
@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_ops(Plan p) {
             opx_store_pts<NB, T>(G, win, wout, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
                                  static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
         } else {
-            opx_store<NB, T>(G, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
-                             static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
+            opx_store<NB, T, ALL ? NB : NB + 1>(G, wt, static_cast<T *>(p.ops_f[0]) + c * OpShape<NB>::SZ,
+                                                static_cast<T *>(p.ops_b[0]) + c * OpShape<NB>::SZ);
         }
     }
 }
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_chunk_ops(Plan p) {
 // threads per chunk walk slices {0,1,2} and {3,4,5} (96 doubles each instead of 192, which spill);
 // the slices meet in shared memory for the store (the suffix operator reads slice l-c-|V|).
 constexpr int kOpsSplitChunks = 32;  // chunks per block (64 threads)
-template <int NB>
+template <int NB, bool ALL = false>
 __global__ void __launch_bounds__(2 * kOpsSplitChunks) k_chunk_ops_split(Plan p) {
     constexpr int M = 1 << NB;
     constexpr int L = NB + 1;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(2 * kOpsSplitChunks) k_chunk_ops_split(Plan p)
 #pragma unroll
         for (int V = 0; V < M; ++V)
             if (cc + pc(V) <= NB) {
-                const int cp = NB + 1 - cc - pc(V);
+                const int cp = (ALL ? NB : NB + 1) - cc - pc(V);
                 pf[cc * M + V] = cc == 0 ? Gs[ci][0][V] : wt[cc] * Gs[ci][cc][V];
                 const double r = cp > NB ? 1.0 : Gs[ci][cp][V];
                 pb[cc * M + V] = cc == 0 ? r : wt[cc] * r;
@@ -1916,16 +1916,25 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
         }
     } else if (with_ops && NB == 5 && sizeof(T) == sizeof(double) && !p.lam) {
         if constexpr (NB == 5 && sizeof(T) == sizeof(double)) {
-            k_chunk_ops_split<NB><<<(unsigned)((p.nchunks + kOpsSplitChunks - 1) / kOpsSplitChunks), 2 * kOpsSplitChunks, 0,
-                                    s>>>(p);
+            const unsigned g = (unsigned)((p.nchunks + kOpsSplitChunks - 1) / kOpsSplitChunks);
+            if (mode == MODE_ALLRES) k_chunk_ops_split<NB, true><<<g, 2 * kOpsSplitChunks, 0, s>>>(p);
+            else k_chunk_ops_split<NB><<<g, 2 * kOpsSplitChunks, 0, s>>>(p);
             ++*launches;
         }
     } else if (with_ops) {
         const size_t sm = ops_smem<NB, T>();
         smem_attr((const void *)k_chunk_ops<NB, T>, sm);
         smem_attr((const void *)k_chunk_ops<NB, T, true>, sm);
-        if (p.lam) k_chunk_ops<NB, T, true><<<(unsigned)nb, tpb, sm, s>>>(p);
-        else k_chunk_ops<NB, T><<<(unsigned)nb, tpb, sm, s>>>(p);
+        if (mode == MODE_ALLRES) {
+            if constexpr (sizeof(T) == sizeof(double)) {
+                smem_attr((const void *)k_chunk_ops<NB, T, false, true>, sm);
+                k_chunk_ops<NB, T, false, true><<<(unsigned)nb, tpb, sm, s>>>(p);
+            }
+        } else if (p.lam) {
+            k_chunk_ops<NB, T, true><<<(unsigned)nb, tpb, sm, s>>>(p);
+        } else {
+            k_chunk_ops<NB, T><<<(unsigned)nb, tpb, sm, s>>>(p);
+        }
         ++*launches;
     }
     if (ev) cudaEventRecord(ev[1], s);
