@@ -355,7 +355,8 @@ class Context:
         P, n, k = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
         self._check(self._lib.mmot_info(self._ctx, ctypes.byref(P), ctypes.byref(n), ctypes.byref(k)))
         return dict(chain_len=P.value, nchains=n.value,
-                    kernel={1: "two_walk", 2: "single_walk", 3: "persistent", 4: "stable", 5: "grid2d"}[k.value])
+                    kernel={1: "two_walk", 2: "single_walk", 3: "persistent", 4: "stable", 5: "grid2d",
+                            6: "lanes"}[k.value])
 
     @property
     def launches(self) -> int:

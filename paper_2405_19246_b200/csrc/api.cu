@@ -156,6 +156,10 @@ struct mmot_ctx {
     mmot_ctx *st_fb = nullptr;              // stabilised context the plain families fall back to (lazy)
     int64_t st_fallbacks = 0;               // calls redone on the stabilised family
     double *u_save = nullptr;               // two-walk LINEAR solves: initial u (for the fallback)
+    // l = 6 lane-state family (lanes.cu)
+    mmot::LsWork ls{};
+    double *ls_mem = nullptr;
+    bool ls_on = false;
     // NEXT-1: all-marginals residual pass (MODE_ALLRES) -- its own chain layout and scan workspace
     // for the DP over all l scalings (2^l states)
     int all_state = 0;                      // 0 untried, 1 ready, -1 unavailable
@@ -285,7 +289,7 @@ mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t *nchains,
     if (!ctx) { set_err(nullptr, "NULL context"); return MMOT_EINVAL; }
     if (chain_len) *chain_len = ctx->g2 ? ctx->g2N : ctx->stable ? ctx->N : ctx->batched ? ctx->ba.P : ctx->P;
     if (nchains) *nchains = ctx->g2 ? ctx->g2M : ctx->stable ? ctx->batch : ctx->batched ? 32 * ctx->batch : ctx->nchunks;
-    if (kernel) *kernel = ctx->g2 ? 5 : ctx->stable ? MMOT_KERNEL_STABLE
+    if (kernel) *kernel = ctx->g2 ? 5 : ctx->ls_on ? 6 : ctx->stable ? MMOT_KERNEL_STABLE
                           : ctx->batched ? MMOT_KERNEL_PERSISTENT : (ctx->sw ? MMOT_KERNEL_SINGLE_WALK : MMOT_KERNEL_TWO_WALK);
     return MMOT_OK;
 }
@@ -301,6 +305,7 @@ void mmot_destroy(mmot_ctx *ctx) {
     mmot_destroy(ctx->st_fb);
     cudaFree(ctx->st_mem);
     cudaFree(ctx->all_mem);
+    cudaFree(ctx->ls_mem);
     cudaFree(ctx->g2_mem);
     cudaFree(ctx->g2_T);
     cudaFree(ctx->st_int);
@@ -583,6 +588,35 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
                 mmot_destroy(c);
                 return MMOT_ENOMEM;
             }
+        }
+    }
+    if (l == 6 && !c->sw && c->opts.chunk == 0 && getenv("MMOT_NO_LANES") == nullptr) {
+        // lane-state family: chains of 32 points (its own operator / scan workspace)
+        mmot::LsWork &w = c->ls;
+        w.P = 32;
+        w.C = (N + 31) / 32;
+        w.nlev = 0;
+        const int64_t B = mmot::kLsB;
+        for (int64_t n = w.C;; n = (n + B - 1) / B) {
+            w.lv_n[w.nlev++] = n;
+            if (n <= B || w.nlev == mmot::kLsMaxLv) break;
+        }
+        size_t nd = 2 * (size_t)w.C * 192 + 2 * (size_t)((w.C + B - 1) / B) * B * 192;
+        for (int lv = 0; lv < w.nlev; ++lv) nd += 2 * (size_t)w.lv_n[lv] * (192 + 32) + 2 * (size_t)((w.lv_n[lv] + B - 1) / B) * 192;
+        if (w.lv_n[w.nlev - 1] <= B && cudaMalloc(&c->ls_mem, nd * sizeof(double)) == cudaSuccess) {
+            double *q = c->ls_mem;
+            w.ops_f = q; q += (size_t)w.C * 192;
+            w.ops_b = q; q += (size_t)w.C * 192;
+            w.scr = q; q += 2 * (size_t)((w.C + B - 1) / B) * B * 192;
+            for (int lv = 0; lv < w.nlev; ++lv)
+                for (int d = 0; d < 2; ++d) {
+                    w.lv_excl[lv][d] = q; q += (size_t)w.lv_n[lv] * 192;
+                    w.lv_car[lv][d] = q; q += (size_t)w.lv_n[lv] * 32;
+                    w.lv_agg[lv][d] = q; q += (size_t)((w.lv_n[lv] + B - 1) / B) * 192;
+                }
+            c->ls_on = mmot::ls_init_tables() == cudaSuccess;
+        } else {
+            cudaGetLastError();
         }
     }
     if (cudaMallocHost(&c->hsc, sizeof(DevScalars)) != cudaSuccess ||
@@ -1292,6 +1326,7 @@ static Plan make_plan(mmot_ctx *c, int k, const double *const *lin, const double
         p.sw_end = c->sw_end;
         p.guard = &c->dsc->guard;
     }
+    if (c->ls_on) p.ls = &c->ls;
     return p;
 }
 
@@ -1485,8 +1520,9 @@ static mmot_status enqueue_sweep(mmot_ctx *c, int t, bool check, double tol, con
             ss.ops_for = -1;      // the residual products overwrote the chain operators
             ss.rx_ready = false;  // ... and the level-0 carries: the next update starts from a full scan
             ss.cur = 0;
-            CK(c, mmot::launch_sum(c->partial, c->nchunks, &c->dsc->res_acc, 1.0, k > 0, &c->dsc->stop, c->stream,
-                                   &c->launches));
+            // (the lane-state family leaves one partial per 32-point chain)
+            CK(c, mmot::launch_sum(c->partial, c->ls_on ? c->ls.C : c->nchunks, &c->dsc->res_acc, 1.0, k > 0,
+                                   &c->dsc->stop, c->stream, &c->launches));
         }
         mmot_status st = shard_allreduce(c, &c->dsc->res_acc);
         if (st) return st;

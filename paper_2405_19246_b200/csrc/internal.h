@@ -31,6 +31,20 @@ __host__ __device__ constexpr int nsub_max(int NB) { return 256 >> NB; }
 __host__ __device__ constexpr int chunk_max(int NB) { return sub_q(NB) * nsub_max(NB); }
 __host__ __device__ constexpr int slab_s(int NB) { return NB <= 2 ? 16 : 8; }
 
+// Lane-state family (lanes.cu, l = 6): chains of 32 points, warp per chain, lane = subset state.
+constexpr int kLsB = 16;             // items per block of the lane-state operator scan (one warp each)
+constexpr int kLsMaxLv = 7;          // scan levels: 16^7 chains
+struct LsWork {
+    int64_t P, C;                    // chain length (32), chains
+    double *ops_f, *ops_b;           // [C][192] chain operators (chain order)
+    int nlev;                        // scan levels (level 0 = chains)
+    int64_t lv_n[kLsMaxLv];          // items per level
+    double *lv_excl[kLsMaxLv][2];    // [n][192] exclusive in-block prefix per item, per direction
+    double *lv_agg[kLsMaxLv][2];     // [n/16][192] block aggregates (= items of the next level)
+    double *lv_car[kLsMaxLv][2];     // [n][32] state entering each item (scan order)
+    double *scr;                     // [2][ceil(C/16)][16][192] composition scratch
+};
+
 struct Plan {
     int NB;                          // l - 1
     int64_t N, P, nchunks;
@@ -74,6 +88,7 @@ struct Plan {
     // a componentwise relative difference above kSwGuardTol sets *guard
     void *sw_end = nullptr;
     int *guard = nullptr;
+    const LsWork *ls = nullptr;      // l = 6: the lane-state family's workspace (null: two-walk kernels)
     const double *lam = nullptr;     // non-uniform grid: per-edge decays [nchunks P + 1] (null: uniform)
     const double *hx = nullptr;      // non-uniform grid: edge lengths (cost duals)
 };
@@ -86,6 +101,10 @@ struct Plan {
 cudaError_t launch_product(const Plan &p, int mode, cudaStream_t s, int64_t *launches,
                            cudaEvent_t *ev = nullptr /* 4 events: before ops, after ops, after scan, after apply */,
                            bool with_ops = true, bool next = false);
+
+// Lane-state family (l = 6): ops -> two-level scan -> apply, modes UPD / MARG / RES.
+cudaError_t launch_ls_product(const Plan &p, const LsWork &w, int mode, cudaStream_t s, int64_t *launches);
+cudaError_t ls_init_tables();  // composition term table on the current device (once; not capturable)
 
 // Resident CTAs (of kWarpsPerCta warps) per SM of the single-walk update kernel.
 int sw_blocks_per_sm(int NB);

@@ -2066,6 +2066,14 @@ static cudaError_t product_nb(const Plan &p, int mode, cudaStream_t s, int64_t *
 cudaError_t launch_product(const Plan &p, int mode, cudaStream_t s, int64_t *launches, cudaEvent_t *ev,
                            bool with_ops, bool next) {
     const bool dual = mode == MODE_COST;
+    if (p.ls && p.NB == 5 && (mode == MODE_UPD || mode == MODE_MARG || mode == MODE_RES)) {
+        if (ev) cudaEventRecord(ev[0], s);
+        if (ev) cudaEventRecord(ev[1], s);
+        if (ev) cudaEventRecord(ev[2], s);
+        cudaError_t e = launch_ls_product(p, *p.ls, mode, s, launches);
+        if (ev) cudaEventRecord(ev[3], s);
+        return e;
+    }
     switch (p.NB) {
         case 1: return dual ? product_nb<1, Dual>(p, mode, s, launches, ev, with_ops, next) : product_nb<1, double>(p, mode, s, launches, ev, with_ops, next);
         case 2: return dual ? product_nb<2, Dual>(p, mode, s, launches, ev, with_ops, next) : product_nb<2, double>(p, mode, s, launches, ev, with_ops, next);
