@@ -276,7 +276,7 @@ MMOT_API int mmot_version(void);
 /* Launch plan of a context: grid points per chain P, number of chains, kernel family actually
  * used (MMOT_KERNEL_* value; 5 = 2-D grid, with chain_len = N1 and nchains = N2; 6 = the l = 6
  * lane-state family, one warp per 32-point chain with the 32 subset states on its lanes, which
- * AUTO / TWO_WALK l = 6 contexts use for updates, marginals and residuals (MMOT_NO_LANES=1: the
+ * AUTO l = 6 contexts use for updates, marginals and residuals (MMOT_KERNEL_TWO_WALK or MMOT_NO_LANES=1: the
  * two-walk kernels); chain_len / nchains then describe the two-walk layout the cost uses).  Any
  * output pointer may be NULL. */
 MMOT_API mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t *nchains, int *kernel);

@@ -590,7 +590,7 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
             }
         }
     }
-    if (l == 6 && !c->sw && c->opts.chunk == 0 && getenv("MMOT_NO_LANES") == nullptr) {
+    if (l == 6 && !c->sw && c->opts.chunk == 0 && c->opts.kernel == MMOT_KERNEL_AUTO && getenv("MMOT_NO_LANES") == nullptr) {
         // lane-state family: chains of 32 points (its own operator / scan workspace)
         mmot::LsWork &w = c->ls;
         w.P = 32;
