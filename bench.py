@@ -297,7 +297,9 @@ def run_batched(args, cfg):
     achieved = flop / (sk / 1e3) / 1e12
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK, "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK, "traffic": None,
-                "kernel": "k_bat_sinkhorn (all sweeps of all instances of the rank, one launch)",
+                "kernel": ("k_pair_sinkhorn (pair family: all sweeps of all instances of the rank, one launch, "
+                           "plus the layout conversions)" if ctx.pair_solves else
+                           "k_bat_sinkhorn (all sweeps of all instances of the rank, one launch)"),
                 "alg_flop_per_launch": flop, "ms_per_launch": sk,
                 "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5)"}
     cpu = None
@@ -338,7 +340,10 @@ def run_batched(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"C5: {cfg.batch} instances x (l={l}, N={N}), eta_b ~ logU[1e-3,1e-1], "
-                                   f"T={T}, f64 arithmetic with per-chain exponents", "l": l, "N": N,
+                                   f"T={T}, f64 arithmetic", "l": l, "N": N,
+                       "family": ("pair (two threads per instance, no chain operators; mantissas with one "
+                                  "exponent per 8 points, " + ("fp32" if io32 else "fp64") + " storage)")
+                       if ctx.pair_solves else "persistent (warp per instance, 32 chains, per-chain exponents)",
                        "io_dtype": "f32 marginals (MMOT_F32 context), fp64 u[]" if io32 else "f64",
                        "batch": cfg.batch, "iters": T, "parallelism": f"instances sharded over {ws} GPU(s)",
                        "l2": "per-instance working set L2/SMEM resident; no flush (ALU-bound)"},

@@ -323,6 +323,16 @@ MMOT_API int64_t mmot_allres_checks(const mmot_ctx *ctx);
  * Returns how many solves of this context used the graph. */
 MMOT_API int64_t mmot_graph_solves(const mmot_ctx *ctx);
 
+/* Pair family (batched contexts).  A batched Sinkhorn with a fixed sweep count (tol <= 0), a
+ * uniform grid and a batch of at least MMOT_PAIR_MIN instances (default 4096) runs on two threads
+ * per instance with no chain operators: each half of the grid is walked from its open end (where
+ * the carry is the empty-set state), the halves' end states are swapped, and each half then walks
+ * the other direction with the combine.  Scalings are stored as mantissas with one
+ * exponent per 8 grid points (fp64 mantissas; fp32 mantissas and marginals in MMOT_F32 contexts).
+ * MMOT_NO_PAIR=1 keeps the one-warp-per-instance kernel.  Returns how many solves of this context
+ * used the pair family. */
+MMOT_API int64_t mmot_pair_solves(const mmot_ctx *ctx);
+
 /* Benchmark instrumentation.  While enabled, every tensor-vector product records CUDA events
  * on the context stream around its phases.  mmot_profile_read synchronises the stream and
  * returns, accumulated since the last read, the device milliseconds and product counts of

@@ -137,6 +137,8 @@ def load_library():
     lib.mmot_allres_checks.restype = ctypes.c_int64
     lib.mmot_graph_solves.argtypes = [vp]
     lib.mmot_graph_solves.restype = ctypes.c_int64
+    lib.mmot_pair_solves.argtypes = [vp]
+    lib.mmot_pair_solves.restype = ctypes.c_int64
     lib.mmot_profile_enable.argtypes = [vp, ctypes.c_int]
     lib.mmot_profile_enable.restype = ctypes.c_int
     dp = ctypes.POINTER(ctypes.c_double)
@@ -376,6 +378,11 @@ class Context:
     def graph_solves(self) -> int:
         """Solves whose sweep loop ran as one device-resident CUDA graph launch."""
         return int(self._lib.mmot_graph_solves(self._ctx))
+
+    @property
+    def pair_solves(self) -> int:
+        """Batched solves that ran on the pair family (two threads per instance, no chain operators)."""
+        return int(self._lib.mmot_pair_solves(self._ctx))
 
     @property
     def fallbacks(self) -> int:

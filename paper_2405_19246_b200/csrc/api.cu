@@ -183,6 +183,11 @@ struct mmot_ctx {
     int64_t batch = 1;
     mmot::BatchArgs ba{};
     double *bat_mem = nullptr;              // eta, phit, scratch, wout (one allocation)
+    // pair family (pair.cu): large batches, tol <= 0 -- its own layout, allocated on first use
+    mmot::PairPlan pp{};
+    void *pair_mem = nullptr;
+    int pair_state = 0;                     // 0 unknown, 1 available, -1 not for this context
+    int64_t pair_solves = 0;
     double *pts_mem = nullptr;              // non-uniform grids: hx [ne], lambda [batch][ne]
     double *f32_mem = nullptr;              // MMOT_F32 I/O: widened marginals [l][n] + output [n] (lazy)
     float *f32_stage = nullptr;             // MMOT_F32 host calls: float staging [l][n] (lazy)
@@ -284,6 +289,7 @@ int64_t mmot_stable_fallback_count(const mmot_ctx *ctx) {
 }
 
 int64_t mmot_graph_solves(const mmot_ctx *ctx) { return ctx ? ctx->graph_solves + (ctx->fb ? ctx->fb->graph_solves : 0) : 0; }
+int64_t mmot_pair_solves(const mmot_ctx *ctx) { return ctx ? ctx->pair_solves : 0; }
 
 mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t *nchains, int *kernel) {
     if (!ctx) { set_err(nullptr, "NULL context"); return MMOT_EINVAL; }
@@ -317,6 +323,7 @@ void mmot_destroy(mmot_ctx *ctx) {
     cudaFree(ctx->out_t);
     cudaFree(ctx->sw_end);
     cudaFree(ctx->bat_mem);
+    cudaFree(ctx->pair_mem);
     cudaFree(ctx->pts_mem);
     cudaFree(ctx->f32_mem);
     cudaFree(ctx->f32_stage);
@@ -1105,6 +1112,57 @@ static bool can_stabilise(const mmot_ctx *c) {
     return !c->sharded && !c->pts_lam && !c->ba.lam && !c->stable && getenv("MMOT_NO_STABLE") == nullptr;
 }
 
+// Pair family (pair.cu): batched contexts with uniform grids and a fixed sweep count (tol <= 0)
+// whose batch fills the GPU (>= MMOT_PAIR_MIN instances, default 4096: two threads per instance,
+// so smaller batches leave SMs idle and the one-warp-per-instance kernel is faster).  MMOT_NO_PAIR=1
+// disables it.  The workspace (its own layout: mantissas + slab exponents, checkpoints) is
+// allocated on first use.
+static bool ensure_pair(mmot_ctx *c) {
+    if (c->pair_state) return c->pair_state > 0;
+    c->pair_state = -1;
+    const char *mn = getenv("MMOT_PAIR_MIN");
+    const int64_t pmin = mn ? atoll(mn) : 4096;
+    if (!c->batched || c->ba.lam || c->l < 2 || c->l > 5 || c->batch < pmin || getenv("MMOT_NO_PAIR") != nullptr)
+        return false;
+    mmot::PairPlan &p = c->pp;
+    p.l = c->l;
+    p.batch = c->batch;
+    p.N = c->N;
+    p.nA = (int)((c->N + 1) / 2);
+    p.nB = (int)(c->N / 2);
+    p.nslab = (p.nA + 7) / 8;
+    p.nblk = (c->batch + 15) / 16;
+    p.h = c->h;
+    p.eta = c->ba.eta;
+    p.f32 = c->dt == MMOT_F32 ? 1 : 0;
+    p.slots = (std::min<int64_t>(p.nblk, mmot::pair_slots()) + 1) / 2 * 2;
+    const size_t es = p.f32 ? sizeof(float) : sizeof(double);
+    const size_t nv = (size_t)c->l * p.nblk * p.nslab * 8 * 32;
+    const size_t ne = (size_t)c->l * p.nblk * p.nslab * 32;
+    const size_t nck = (size_t)p.slots * p.nslab * (1u << (c->l - 1)) * 32;
+    const size_t bytes = nck * sizeof(double) + 2 * nv * es + ne * sizeof(int);
+    if (cudaMalloc(&c->pair_mem, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        c->pair_mem = nullptr;
+        return false;  // the persistent kernel runs instead
+    }
+    char *q = static_cast<char *>(c->pair_mem);
+    p.ckpt = reinterpret_cast<double *>(q);
+    q += nck * sizeof(double);
+    p.phit = q;
+    q += nv * es;
+    p.mu = q;
+    q += nv * es;
+    p.E = reinterpret_cast<int *>(q);
+    p.status = c->ba.status;
+    p.fail_iter = c->ba.fail_iter;
+    p.iters_done = c->ba.iters_done;
+    p.converged = c->ba.converged;
+    p.resid = c->ba.resid;
+    c->pair_state = 1;
+    return true;
+}
+
 static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters, double tol, void *const *u,
                                 mmot_report *rep) {
     mmot_status st = reset_scalars(c);
@@ -1126,14 +1184,27 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
         set_err(c, "%s", mmot_strerror((mmot_status)c->hsc->status));
         return (mmot_status)c->hsc->status;
     }
-    st = bat_import(c, u);
-    if (st) return st;
-    mmot::BatchArgs a = c->ba;
-    for (int q = 0; q < c->l; ++q) a.mu[q] = mu[q];
-    a.iters = iters;
-    a.tol = tol;
-    a.check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
-    CK(c, mmot::launch_batched(a, 0, c->stream, &c->launches));
+    const bool pair = tol <= 0 && ensure_pair(c);
+    if (pair) {
+        // pair family: u and mu into its layout, all sweeps in one launch
+        if ((st = bat_upload_ptrs(c, u, 0))) return st;
+        if ((st = bat_upload_ptrs(c, reinterpret_cast<const void *const *>(mu), 1))) return st;
+        CK(c, mmot::launch_pair_convert(c->pp, c->bat_ptrs, 0, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
+        CK(c, mmot::launch_pair_convert(c->pp, c->bat_ptrs + mmot::kMaxL, 2, 0, c->stream, &c->launches));
+        mmot::PairPlan p = c->pp;
+        p.iters = iters;
+        CK(c, mmot::launch_pair_sinkhorn(p, c->stream, &c->launches));
+        ++c->pair_solves;
+    } else {
+        st = bat_import(c, u);
+        if (st) return st;
+        mmot::BatchArgs a = c->ba;
+        for (int q = 0; q < c->l; ++q) a.mu[q] = mu[q];
+        a.iters = iters;
+        a.tol = tol;
+        a.check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
+        CK(c, mmot::launch_batched(a, 0, c->stream, &c->launches));
+    }
     CK(c, cudaMemcpyAsync(c->bat_shost, c->ba.status, 4 * (size_t)c->batch * sizeof(int), cudaMemcpyDeviceToHost,
                           c->stream));
     CK(c, cudaMemcpyAsync(c->bat_rhost, c->ba.resid, (size_t)c->batch * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1158,7 +1229,8 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
     }
     st = bat_upload_ptrs(c, const_cast<const void *const *>(u), 0);
     if (st) return st;
-    CK(c, mmot::launch_bat_convert(c->ba, c->bat_ptrs, 0, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
+    if (pair) CK(c, mmot::launch_pair_convert(c->pp, c->bat_ptrs, 1, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
+    else CK(c, mmot::launch_bat_convert(c->ba, c->bat_ptrs, 0, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
     if (redo) {
         mmot_ctx *sc = c->st_fb;
         CK(c, cudaMemsetAsync(sc->st_int, 0, 4 * (size_t)B * sizeof(int), c->stream));

@@ -161,6 +161,33 @@ cudaError_t launch_batched(const BatchArgs &a, int what, cudaStream_t s, int64_t
 cudaError_t launch_bat_convert(const BatchArgs &a, void *const *u_dev_ptrs, int import, int is_log, cudaStream_t s,
                                int64_t *launches);
 
+// Pair family (pair.cu): large batches, two threads per instance (halves A = [0, nA), B mirrored),
+// no chain operators; scalings as mantissas + one exponent per 8 positions.
+struct PairPlan {
+    int l;
+    int64_t batch, N;
+    int nA, nB;        // positions of the left half (ceil(N/2)) and of the mirrored right half
+    int nslab;         // slabs of 8 positions per half: ceil(nA / 8)
+    int64_t nblk;      // blocks of 16 instances (one warp each)
+    double h;
+    const double *eta; // [batch]
+    void *phit;        // [l][nblk][nslab * 8][32] mantissas (double, or float if f32)
+    void *mu;          // [l][nblk][nslab * 8][32] marginals (double, or float if f32)
+    int *E;            // [l][nblk][nslab][32] slab exponents
+    double *ckpt;      // [slots][nslab][2^(l-1)][32] (own state before each slab)
+    int64_t slots;     // resident warps (checkpoint slots)
+    int iters;
+    int f32;           // fp32 storage of mantissas and marginals (MMOT_F32 contexts)
+    int *status, *fail_iter, *iters_done, *converged;  // [batch]
+    double *resid;     // [batch]
+};
+int64_t pair_slots();
+cudaError_t launch_pair_sinkhorn(const PairPlan &pp, cudaStream_t s, int64_t *launches);
+// op 0: u -> mantissas + exponents; 1: -> u; 2: mu (fp64 [batch][N]) -> the pair layout.
+// u_dev: DEVICE array of l device pointers.
+cudaError_t launch_pair_convert(const PairPlan &pp, void *const *u_dev, int op, int log_repr, cudaStream_t s,
+                                int64_t *launches);
+
 // Allow `bytes` of dynamic shared memory for kernel `func` on the CURRENT device.  The attribute is
 // per device, so it is set once per (kernel, device, size) (thread-safe cache).
 void smem_attr(const void *func, size_t bytes);

@@ -128,6 +128,7 @@ def test_batched_c5_full_batch_sampled_instances():
     ctx.init_uniform(u)
     rep = ctx.sinkhorn(mu_d, T, 0.0, u)
     assert rep["status"] == 0 and rep["iters_done"] == T
+    assert ctx.pair_solves == 1
     picks = [int(np.argmin(etas)), int(np.argsort(etas)[B // 2]), int(np.argmax(etas))]
     g = np.stack([x[picks].cpu().numpy() for x in u])               # [l][3][N]
     marg = [ctx.marginal(k, u)[picks].cpu().numpy() for k in range(l)]
@@ -214,6 +215,7 @@ def test_batched_c5_full_run_stratified_instances():
     ctx.init_uniform(u)
     rep = ctx.sinkhorn(mu_d, T, 0.0, u)
     assert rep["status"] == 0 and rep["iters_done"] == T
+    assert ctx.pair_solves == 1  # the bench's family (pair.cu) at the bench's batch size
     le = np.log10(etas)
     edges = np.linspace(-3.0, -1.0, 9)
     picks = []
