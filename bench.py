@@ -459,7 +459,9 @@ def run_mmot(args, cfg):
             traffic = None
     step_frac = alg_bytes * iters_done * l / (ms / 1e3) / 1e9 / peak
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "fused update (ops + scan + apply of one J_k)",
+                "traffic": traffic,
+                "kernel": ("k_cta_sinkhorn (whole solve in one launch; per-update time = step / updates)"
+                           if ctx.cta_solves else "fused update (ops + scan + apply of one J_k)"),
                 "alg_bytes_per_launch": alg_bytes, "ms_per_launch": upd_ms, "peak_source": peak_src,
                 "ms_per_launch_source": "CUDA events around each update of one profiled step after the timed region",
                 "step_level_frac": step_frac,
@@ -508,7 +510,8 @@ def run_mmot(args, cfg):
                        "global_batch": 1,
                        "parallelism": (f"grid sharded over {ws} GPUs (contiguous chunks, NCCL all-gather of "
                                        f"whole-shard operators per update)") if ws > 1 else "single GPU",
-                       "kernel": ctx.info["kernel"], "chain_len": ctx.info["chain_len"],
+                       "kernel": "cta" if ctx.cta_solves else ctx.info["kernel"],
+                       "chain_len": ctx.info["chain_len"],
                        "l2": "inputs (l*N*8*2 B) exceed the 126 MB L2; no flush needed" if N >= 5_000_000 else
                              "working set L2-resident (latency-bound config)"},
             "roofline": roofline,
@@ -517,6 +520,8 @@ def run_mmot(args, cfg):
             "clocks": clk,
             "gpu_launches": int(launches),
             "device_loop": ("CUDA graph, conditional WHILE node (one graph launch per solve)" if graph_solves
+                            else "CTA family: one thread block per instance, the whole solve in one launch"
+                            if ctx.cta_solves
                             else "persistent kernel" if ctx.info["kernel"] == "persistent" else "host-issued launches"),
             "iters_per_s": iters_done / (ms / 1e3),
             "iters_done": iters_done,

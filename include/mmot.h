@@ -333,6 +333,15 @@ MMOT_API int64_t mmot_graph_solves(const mmot_ctx *ctx);
  * used the pair family. */
 MMOT_API int64_t mmot_pair_solves(const mmot_ctx *ctx);
 
+/* CTA family (batched contexts, and the single-instance contexts mmot_create gives small problems).
+ * A batched Sinkhorn whose batch fits one wave (<= the SM count) with l <= 4, N <= 4096, a uniform
+ * grid and every instance inside (l-1)(x_max - x_min)/eta <= 500 runs one thread block per instance:
+ * 256 chains, warp-level operator scans, all sweeps and residual checks in one launch (DESIGN.md
+ * §5).  Scalings are plain fp64; a product that leaves the range reports EOVERFLOW and the instance
+ * is redone on the stabilised family.  MMOT_NO_CTA=1 keeps the one-warp-per-instance kernel.
+ * Returns how many solves of this context used the CTA family. */
+MMOT_API int64_t mmot_cta_solves(const mmot_ctx *ctx);
+
 /* Benchmark instrumentation.  While enabled, every tensor-vector product records CUDA events
  * on the context stream around its phases.  mmot_profile_read synchronises the stream and
  * returns, accumulated since the last read, the device milliseconds and product counts of

@@ -139,6 +139,8 @@ def load_library():
     lib.mmot_graph_solves.restype = ctypes.c_int64
     lib.mmot_pair_solves.argtypes = [vp]
     lib.mmot_pair_solves.restype = ctypes.c_int64
+    lib.mmot_cta_solves.argtypes = [vp]
+    lib.mmot_cta_solves.restype = ctypes.c_int64
     lib.mmot_profile_enable.argtypes = [vp, ctypes.c_int]
     lib.mmot_profile_enable.restype = ctypes.c_int
     dp = ctypes.POINTER(ctypes.c_double)
@@ -383,6 +385,11 @@ class Context:
     def pair_solves(self) -> int:
         """Batched solves that ran on the pair family (two threads per instance, no chain operators)."""
         return int(self._lib.mmot_pair_solves(self._ctx))
+
+    @property
+    def cta_solves(self) -> int:
+        """Batched / small-instance solves that ran on the CTA family (a thread block per instance)."""
+        return int(self._lib.mmot_cta_solves(self._ctx))
 
     @property
     def fallbacks(self) -> int:

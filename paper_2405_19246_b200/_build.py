@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRCS = ["csrc/api.cu", "csrc/kernels.cu", "csrc/batched.cu", "csrc/stable.cu", "csrc/grid2d.cu", "csrc/lanes.cu",
-        "csrc/pair.cu"]
+        "csrc/pair.cu", "csrc/cta.cu"]
 DEPS = SRCS + ["csrc/dp.cuh", "csrc/walk.cuh", "csrc/internal.h", "../include/mmot.h"]
 LIB = os.path.join(HERE, "libmmot.so")
 

@@ -188,6 +188,10 @@ struct mmot_ctx {
     void *pair_mem = nullptr;
     int pair_state = 0;                     // 0 unknown, 1 available, -1 not for this context
     int64_t pair_solves = 0;
+    // CTA family (cta.cu): small instances, a thread block each
+    mmot::CtaPlan cp{};
+    int cta_state = 0;
+    int64_t cta_solves = 0;
     double *pts_mem = nullptr;              // non-uniform grids: hx [ne], lambda [batch][ne]
     double *f32_mem = nullptr;              // MMOT_F32 I/O: widened marginals [l][n] + output [n] (lazy)
     float *f32_stage = nullptr;             // MMOT_F32 host calls: float staging [l][n] (lazy)
@@ -290,6 +294,7 @@ int64_t mmot_stable_fallback_count(const mmot_ctx *ctx) {
 
 int64_t mmot_graph_solves(const mmot_ctx *ctx) { return ctx ? ctx->graph_solves + (ctx->fb ? ctx->fb->graph_solves : 0) : 0; }
 int64_t mmot_pair_solves(const mmot_ctx *ctx) { return ctx ? ctx->pair_solves : 0; }
+int64_t mmot_cta_solves(const mmot_ctx *ctx) { return ctx ? ctx->cta_solves : 0; }
 
 mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t *nchains, int *kernel) {
     if (!ctx) { set_err(nullptr, "NULL context"); return MMOT_EINVAL; }
@@ -1163,6 +1168,37 @@ static bool ensure_pair(mmot_ctx *c) {
     return true;
 }
 
+// CTA family (cta.cu): batched contexts of at most one wave of instances (batch <= SM count) with
+// l <= 4, N <= 4096, a uniform grid, and every instance inside kCtaRange (plain fp64 scalings).
+// MMOT_NO_CTA=1 disables it.
+static bool ensure_cta(mmot_ctx *c) {
+    if (c->cta_state) return c->cta_state > 0;
+    c->cta_state = -1;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    if (!c->batched || c->ba.lam || c->l < 2 || c->l > 4 || c->N > 4096 || c->batch > sms ||
+        getenv("MMOT_NO_CTA") != nullptr)
+        return false;
+    const double span = c->grid.x_max - c->grid.x_min;
+    for (double e : c->eta_host)
+        if ((c->l - 1) * span / e > mmot::kCtaRange) return false;
+    mmot::CtaPlan &p = c->cp;
+    p.l = c->l;
+    p.N = c->N;
+    p.batch = c->batch;
+    p.P = mmot::cta_chain_len(c->N);
+    p.h = c->h;
+    p.eta = c->ba.eta;
+    for (int q = 0; q < c->l; ++q) p.phi[q] = c->ba.phit[q];
+    p.status = c->ba.status;
+    p.fail_iter = c->ba.fail_iter;
+    p.iters_done = c->ba.iters_done;
+    p.converged = c->ba.converged;
+    p.resid = c->ba.resid;
+    c->cta_state = 1;
+    return true;
+}
+
 static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters, double tol, void *const *u,
                                 mmot_report *rep) {
     mmot_status st = reset_scalars(c);
@@ -1185,7 +1221,19 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
         return (mmot_status)c->hsc->status;
     }
     const bool pair = tol <= 0 && ensure_pair(c);
-    if (pair) {
+    const bool cta = !pair && ensure_cta(c);
+    if (cta) {
+        // CTA family: linear scalings, all sweeps (and residual checks) in one launch
+        if ((st = bat_upload_ptrs(c, u, 0))) return st;
+        CK(c, mmot::launch_cta_convert(c->cp, c->bat_ptrs, 0, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
+        mmot::CtaPlan p = c->cp;
+        for (int q = 0; q < c->l; ++q) p.mu[q] = mu[q];
+        p.iters = iters;
+        p.tol = tol;
+        p.check_every = c->opts.check_every > 0 ? c->opts.check_every : 1;
+        CK(c, mmot::launch_cta_sinkhorn(p, c->stream, &c->launches));
+        ++c->cta_solves;
+    } else if (pair) {
         // pair family: u and mu into its layout, all sweeps in one launch
         if ((st = bat_upload_ptrs(c, u, 0))) return st;
         if ((st = bat_upload_ptrs(c, reinterpret_cast<const void *const *>(mu), 1))) return st;
@@ -1229,7 +1277,8 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
     }
     st = bat_upload_ptrs(c, const_cast<const void *const *>(u), 0);
     if (st) return st;
-    if (pair) CK(c, mmot::launch_pair_convert(c->pp, c->bat_ptrs, 1, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
+    if (cta) CK(c, mmot::launch_cta_convert(c->cp, c->bat_ptrs, 1, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
+    else if (pair) CK(c, mmot::launch_pair_convert(c->pp, c->bat_ptrs, 1, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
     else CK(c, mmot::launch_bat_convert(c->ba, c->bat_ptrs, 0, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
     if (redo) {
         mmot_ctx *sc = c->st_fb;

@@ -182,6 +182,28 @@ struct PairPlan {
     double *resid;     // [batch]
 };
 int64_t pair_slots();
+
+// CTA family (cta.cu): one thread block per small instance (l <= 4, N <= 4096), 256 chains,
+// warp-level operator scans; plain fp64 scalings (instances inside kCtaRange).
+constexpr double kCtaRange = 500.0;  // max (l-1) (x_max - x_min) / eta of an instance
+struct CtaPlan {
+    int l;
+    int64_t N, batch;
+    int P;                          // chain length: cta_chain_len(N)
+    double h;
+    const double *eta;              // [batch]
+    double *phi[kMaxL];             // [batch][N] linear scalings
+    const double *mu[kMaxL];        // [batch][N]
+    int iters, check_every;
+    double tol;
+    int *status, *fail_iter, *iters_done, *converged;  // [batch]
+    double *resid;                  // [batch]
+};
+int cta_chain_len(int64_t N);
+cudaError_t launch_cta_sinkhorn(const CtaPlan &cp, cudaStream_t s, int64_t *launches);
+// op 0: u -> phi, 1: phi -> u (u_dev: DEVICE array of l device pointers)
+cudaError_t launch_cta_convert(const CtaPlan &cp, void *const *u_dev, int op, int log_repr, cudaStream_t s,
+                               int64_t *launches);
 cudaError_t launch_pair_sinkhorn(const PairPlan &pp, cudaStream_t s, int64_t *launches);
 // op 0: u -> mantissas + exponents; 1: -> u; 2: mu (fp64 [batch][N]) -> the pair layout.
 // u_dev: DEVICE array of l device pointers.
