@@ -1634,27 +1634,39 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_sw_ops(Plan p) {
 // One CTA per 32 chains x 32 offsets tile (blockIdx.y = chain group).
 // flags != nullptr: the input check of launch_check fused into the pass (bit0 NaN/Inf, bit1
 // negative; -inf allowed when allow_neg_inf) and, if mass != nullptr, the sum of the inputs.
-__global__ void k_to_t(const double *__restrict__ src, double *__restrict__ dst, int64_t N, int64_t P, int64_t nchains,
-                       int op, int *flags, double *mass, int allow_neg_inf) {
+// Tile = 32 chains x 32 offsets, 128 threads: each thread loads its 8 elements before any use (8
+// loads in flight per thread), then the tile is written transposed.  The natural-layout side reads
+// 32 rows of 256 contiguous bytes, the chain-blocked side writes 8 KB contiguous.
+constexpr int kTR = 4;  // thread rows per tile (blockDim.y)
+__global__ void __launch_bounds__(32 * kTR) k_to_t(const double *__restrict__ src, double *__restrict__ dst, int64_t N,
+                                                  int64_t P, int64_t nchains, int op, int *flags, double *mass,
+                                                  int allow_neg_inf) {
     __shared__ double tile[32][33];
-    __shared__ double msum[8];
+    __shared__ double msum[kTR];
     const int64_t t0 = (int64_t)blockIdx.x * 32, g = blockIdx.y, c0 = g * 32;
+    constexpr int R = 32 / kTR;
+    double v[R];
+    const int64_t t = t0 + threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {  // r = chain within the tile, threadIdx.x = offset t
+        const int64_t c = c0 + threadIdx.y + i * kTR;
+        const int64_t x = c * P + t;
+        v[i] = (c < nchains && t < P && x < N) ? __ldcs(src + x) : 0.0;
+    }
     int fl = 0;
     double a = 0.0;
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {  // r: chain within tile, threadIdx.x: offset t
-        const int64_t c = c0 + r, t = t0 + threadIdx.x;
-        const int64_t x = c * P + t;
-        double v = 0.0;
-        if (c < nchains && t < P && x < N) {
-            v = src[x];
-            if (flags) {
-                if (isnan(v) || (isinf(v) && !(allow_neg_inf && v < 0))) fl |= 1;
-                else if (v < 0 && !allow_neg_inf) fl |= 2;
-                else if (!allow_neg_inf) a += v;
-            }
-            if (op == 1) v = exp(v);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int64_t c = c0 + threadIdx.y + i * kTR;
+        const bool in = c < nchains && t < P && c * P + t < N;
+        double x = v[i];
+        if (flags && in) {
+            if (isnan(x) || (isinf(x) && !(allow_neg_inf && x < 0))) fl |= 1;
+            else if (x < 0 && !allow_neg_inf) fl |= 2;
+            else if (!allow_neg_inf) a += x;
         }
-        tile[r][threadIdx.x] = v;
+        if (op == 1 && in) x = exp(x);
+        tile[threadIdx.y + i * kTR][threadIdx.x] = x;
     }
     if (flags) {
         if (fl) atomicOr(flags, fl);
@@ -1667,31 +1679,40 @@ __global__ void k_to_t(const double *__restrict__ src, double *__restrict__ dst,
     __syncthreads();
     if (flags && mass && threadIdx.y == 0 && threadIdx.x == 0) {
         double b = 0.0;
-        for (int i = 0; i < (int)blockDim.y; ++i) b += msum[i];
+#pragma unroll
+        for (int i = 0; i < kTR; ++i) b += msum[i];
         atomicAdd(mass, b);
     }
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {  // r: offset within tile, threadIdx.x: chain
-        const int64_t t = t0 + r;
-        if (t < P) dst[g * 32 * P + t * 32 + threadIdx.x] = tile[threadIdx.x][r];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {  // r = offset within the tile, threadIdx.x = chain
+        const int64_t tt = t0 + threadIdx.y + i * kTR;
+        if (tt < P) __stcs(dst + g * 32 * P + tt * 32 + threadIdx.x, tile[threadIdx.x][threadIdx.y + i * kTR]);
     }
 }
 
-__global__ void k_from_t(const double *__restrict__ src, double *__restrict__ dst, int64_t N, int64_t P, int64_t nchains,
-                         int op) {
+__global__ void __launch_bounds__(32 * kTR) k_from_t(const double *__restrict__ src, double *__restrict__ dst,
+                                                    int64_t N, int64_t P, int64_t nchains, int op) {
     __shared__ double tile[32][33];
     const int64_t t0 = (int64_t)blockIdx.x * 32, g = blockIdx.y, c0 = g * 32;
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {  // r: offset, threadIdx.x: chain
-        const int64_t t = t0 + r;
-        tile[r][threadIdx.x] = t < P ? src[g * 32 * P + t * 32 + threadIdx.x] : 0.0;
+    constexpr int R = 32 / kTR;
+    double v[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {  // r = offset, threadIdx.x = chain
+        const int64_t tt = t0 + threadIdx.y + i * kTR;
+        v[i] = tt < P ? __ldcs(src + g * 32 * P + tt * 32 + threadIdx.x) : 0.0;
     }
+#pragma unroll
+    for (int i = 0; i < R; ++i) tile[threadIdx.y + i * kTR][threadIdx.x] = v[i];
     __syncthreads();
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {  // r: chain, threadIdx.x: offset
-        const int64_t c = c0 + r, t = t0 + threadIdx.x;
+    const int64_t t = t0 + threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {  // r = chain, threadIdx.x = offset
+        const int64_t c = c0 + threadIdx.y + i * kTR;
         const int64_t x = c * P + t;
         if (c < nchains && t < P && x < N) {
-            double v = tile[threadIdx.x][r];
-            if (op == 2) v = log(v);
-            dst[x] = v;
+            double y = tile[threadIdx.x][threadIdx.y + i * kTR];
+            if (op == 2) y = log(y);
+            __stcs(dst + x, y);
         }
     }
 }
@@ -1699,7 +1720,7 @@ __global__ void k_from_t(const double *__restrict__ src, double *__restrict__ ds
 cudaError_t launch_to_t(const double *src, double *dst, int64_t N, int64_t P, int64_t nchains, int64_t nchp, int op,
                         cudaStream_t s, int64_t *launches, int *flags, double *mass, int allow_neg_inf) {
     dim3 grid((unsigned)((P + 31) / 32), (unsigned)(nchp / 32));
-    k_to_t<<<grid, dim3(32, 8), 0, s>>>(src, dst, N, P, nchains, op, flags, mass, allow_neg_inf);
+    k_to_t<<<grid, dim3(32, kTR), 0, s>>>(src, dst, N, P, nchains, op, flags, mass, allow_neg_inf);
     ++*launches;
     return cudaGetLastError();
 }
@@ -1707,7 +1728,7 @@ cudaError_t launch_from_t(const double *src, double *dst, int64_t N, int64_t P, 
                           cudaStream_t s, int64_t *launches) {
     dim3 grid((unsigned)((P + 31) / 32), (unsigned)((nchains + 31) / 32));
     (void)nchp;
-    k_from_t<<<grid, dim3(32, 8), 0, s>>>(src, dst, N, P, nchains, op);
+    k_from_t<<<grid, dim3(32, kTR), 0, s>>>(src, dst, N, P, nchains, op);
     ++*launches;
     return cudaGetLastError();
 }
