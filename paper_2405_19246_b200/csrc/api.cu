@@ -190,6 +190,7 @@ struct mmot_ctx {
     int64_t pair_solves = 0;
     // CTA family (cta.cu): small instances, a thread block each
     mmot::CtaPlan cp{};
+    double *cta_mem = nullptr;
     int cta_state = 0;
     int64_t cta_solves = 0;
     double *pts_mem = nullptr;              // non-uniform grids: hx [ne], lambda [batch][ne]
@@ -329,6 +330,7 @@ void mmot_destroy(mmot_ctx *ctx) {
     cudaFree(ctx->sw_end);
     cudaFree(ctx->bat_mem);
     cudaFree(ctx->pair_mem);
+    cudaFree(ctx->cta_mem);
     cudaFree(ctx->pts_mem);
     cudaFree(ctx->f32_mem);
     cudaFree(ctx->f32_stage);
@@ -1190,6 +1192,12 @@ static bool ensure_cta(mmot_ctx *c) {
     p.h = c->h;
     p.eta = c->ba.eta;
     for (int q = 0; q < c->l; ++q) p.phi[q] = c->ba.phit[q];
+    if (cudaMalloc(&c->cta_mem, (size_t)c->batch * c->N * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        c->cta_mem = nullptr;
+        return false;
+    }
+    p.scr = c->cta_mem;
     p.status = c->ba.status;
     p.fail_iter = c->ba.fail_iter;
     p.iters_done = c->ba.iters_done;

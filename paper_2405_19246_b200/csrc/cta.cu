@@ -57,7 +57,9 @@ __device__ __forceinline__ void op_shfl_down(double (&D)[NB + 1][1 << NB], const
 
 // One product of update / residual slot k for the block's instance.
 //   MODE_UPD: phi_k <- mu_k / J_k;  MODE_RES: returns this thread's sum |phi_k J_k - mu_k|
-template <int NB, int P, int MODE>
+//   DEFER (MODE_UPD, k = 0 after a check sweep): the new phi_0 goes to cp.scr and the product also
+//   returns the deferred residual term |phi_0 J_0 - mu_0| of the previous sweep (same bound vectors)
+template <int NB, int P, int MODE, bool DEFER = false>
 __device__ __forceinline__ double cta_product(const CtaPlan &cp, int64_t inst, int k, const double (&wt)[NB + 2],
                                               double (*aggF)[(NB + 1) << NB], double (*aggB)[(NB + 1) << NB],
                                               bool &bad) {
@@ -208,7 +210,12 @@ __device__ __forceinline__ double cta_product(const CtaPlan &cp, int64_t inst, i
                     const double qv = div_nr1(mu, J);
                     const bool nz = nonzero(mu);
                     bad |= nz && !finite_positive(qv);
-                    phik[x] = nz ? qv : 0.0;
+                    if (DEFER) {
+                        acc += fabs(phik[x] * J - mu);
+                        cp.scr[inst * N + x] = nz ? qv : 0.0;
+                    } else {
+                        phik[x] = nz ? qv : 0.0;
+                    }
                 } else {
                     acc += fabs(phik[x] * J - mu);
                 }
@@ -224,7 +231,6 @@ __global__ void __launch_bounds__(kCtaT, 1) k_cta_sinkhorn(CtaPlan cp) {
     constexpr int L = NB + 1, SZ = (NB + 1) << NB;
     __shared__ double aggF[kCtaW][SZ], aggB[kCtaW][SZ];
     __shared__ double red[kCtaW];
-    __shared__ int flag;
     const int64_t inst = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double wt[NB + 2];
@@ -236,34 +242,68 @@ __global__ void __launch_bounds__(kCtaT, 1) k_cta_sinkhorn(CtaPlan cp) {
     int done = 0, fail = -1;
     bool conv = false;
     double res = __longlong_as_double(0x7ff8000000000000ll);
+    // block sum of one value per thread
+    auto block_sum = [&](double a) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) red[w] = a;
+        __syncthreads();
+        double r = 0.0;
+#pragma unroll
+        for (int i = 0; i < kCtaW; ++i) r += red[i];
+        __syncthreads();
+        return r;
+    };
+    // Residual of a check sweep t < iters: the k = 0 term rides on sweep t+1's first update (its
+    // bound vectors are sweep t's end-of-sweep ones), which writes phi_0 to scratch; if the total
+    // meets tol the solve stops at sweep t and the scratch is dropped (l + l-2 products per check
+    // sweep instead of l + l-1, as in the persistent kernel).
+    bool pend = false;
+    double pres = 0.0;
+    int pt = 0;
+    const int64_t x0 = (int64_t)threadIdx.x * P;
     for (int t = 1; t <= cp.iters; ++t) {
         bool bad = false;
-        for (int k = 0; k < L; ++k) cta_product<NB, P, MODE_UPD>(cp, inst, k, wt, aggF, aggB, bad);
-        if (threadIdx.x == 0) flag = 0;
-        __syncthreads();
-        if (bad) flag = 1;
-        __syncthreads();
-        if (flag) {
+        for (int k = 0; k < L; ++k) {
+            if (k == 0 && pend) {
+                const double r0 = block_sum(cta_product<NB, P, MODE_UPD, true>(cp, inst, 0, wt, aggF, aggB, bad));
+                pend = false;
+                res = pres + r0;
+                if (res <= cp.tol && !__syncthreads_or(bad)) {
+                    conv = true;
+                    done = pt;
+                    break;
+                }
+#pragma unroll
+                for (int j = 0; j < P; ++j)
+                    if (x0 + j < cp.N) cp.phi[0][inst * cp.N + x0 + j] = cp.scr[inst * cp.N + x0 + j];
+                __syncthreads();
+            } else {
+                cta_product<NB, P, MODE_UPD>(cp, inst, k, wt, aggF, aggB, bad);
+            }
+        }
+        if (conv) break;
+        if (__syncthreads_or(bad)) {
             fail = t;
             break;
         }
         done = t;
         if (cp.tol > 0 && (t % cp.check_every == 0 || t == cp.iters)) {
             // Res_t = sum_{k < l-1} ||phi_k J_k - mu_k||_1 on the end-of-sweep scalings
+            const bool defer = t < cp.iters;
             double a = 0.0;
-            for (int k = 0; k + 1 < L; ++k) a += cta_product<NB, P, MODE_RES>(cp, inst, k, wt, aggF, aggB, bad);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-            if (lane == 0) red[w] = a;
-            __syncthreads();
-            double r = 0.0;
-#pragma unroll
-            for (int i = 0; i < kCtaW; ++i) r += red[i];
-            __syncthreads();
-            res = r;
-            if (r <= cp.tol) {
-                conv = true;
-                break;
+            for (int k = defer ? 1 : 0; k + 1 < L; ++k) a += cta_product<NB, P, MODE_RES>(cp, inst, k, wt, aggF, aggB, bad);
+            const double r = block_sum(a);
+            if (defer) {
+                pend = true;
+                pres = r;
+                pt = t;
+            } else {
+                res = r;
+                if (r <= cp.tol) {
+                    conv = true;
+                    break;
+                }
             }
         }
     }

@@ -194,6 +194,7 @@ struct CtaPlan {
     const double *eta;              // [batch]
     double *phi[kMaxL];             // [batch][N] linear scalings
     const double *mu[kMaxL];        // [batch][N]
+    double *scr;                    // [batch][N] deferred-residual update of phi_0
     int iters, check_every;
     double tol;
     int *status, *fail_iter, *iters_done, *converged;  // [batch]
