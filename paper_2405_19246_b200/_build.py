@@ -14,6 +14,7 @@ LIB = os.path.join(HERE, "libmmot.so")
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17",
+] + os.environ.get("MMOT_NVCC_DEFS", "").split() + [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
     "-Xcompiler", "-fvisibility=hidden",

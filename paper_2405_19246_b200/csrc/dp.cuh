@@ -127,6 +127,18 @@ __device__ __forceinline__ void dp_diag_inv(T (&st)[1 << NB], const T *winv) {
     for (int S = 1; S < (1 << NB); ++S) st[S] = mul(winv[pc(S)], st[S]);
 }
 
+// Per-level diag in a frame scaled by w_1 per grid step (single-walk kernels, fp64): st[S] *= c[|S|]
+// except for the levels whose multiplier is exactly 1 (|S| = 1 and |S| = NB: w_{l-1} = w_1, l = NB+1),
+// which are skipped at compile time.  DESIGN.md §5 (scaled frames).
+template <int NB>
+__device__ __forceinline__ void dp_diag_lvl(double (&st)[1 << NB], const double (&c)[NB + 2]) {
+#pragma unroll
+    for (int S = 0; S < (1 << NB); ++S) {
+        const int a = pc(S);
+        if (a != 1 && a != NB) st[S] *= c[a];
+    }
+}
+
 // Operator storage: G[c][S], c = 0..NB, S = 0..2^NB-1 (entries with pc(S) > NB-c unused).
 template <int NB>
 struct OpShape {
@@ -339,6 +351,27 @@ __device__ __forceinline__ void rx_L_step(double (&L)[Rx<NB>::MO], const double 
     constexpr int MO = Rx<NB>::MO;
 #pragma unroll
     for (int U = 0; U < MO; ++U) L[U] *= wt[pc(U) + 1];
+#pragma unroll
+    for (int j = 0; j < NB - 1; ++j)
+#pragma unroll
+        for (int U = MO - 1; U >= 0; --U)
+            if ((U >> j) & 1) L[U] = fma(f[j + 1], L[U ^ (1 << j)], L[U]);
+#pragma unroll
+    for (int U = 0; U < MO; ++U) L[U] = fma(o, F[U << 1], L[U]);
+}
+
+// rx_L_step on L scaled by w_1^{-t} (the prefix frame of the scaled single walk, F~ = F w_1^{-t}):
+// L~ <- place_old(D' L~) + o F~_old with D' = D / w_1 (wr[a] = w_a / w_1; levels a = |U| + 1 in
+// {1, NB} need no multiply).  The caller unscales once at the chain end.
+template <int NB>
+__device__ __forceinline__ void rx_L_step_scl(double (&L)[Rx<NB>::MO], const double *wr, const double (&f)[NB],
+                                              double o, const double (&F)[1 << NB]) {
+    constexpr int MO = Rx<NB>::MO;
+#pragma unroll
+    for (int U = 0; U < MO; ++U) {
+        const int a = pc(U) + 1;
+        if (a != 1 && a != NB) L[U] *= wr[a];
+    }
 #pragma unroll
     for (int j = 0; j < NB - 1; ++j)
 #pragma unroll

@@ -1160,7 +1160,16 @@ __device__ __forceinline__ void load_winv(T (&wi)[NB + 2], const Weights &W) {
 // that is used.
 // ---------------------------------------------------------------------------------------
 constexpr int kSwS = 8;      // offsets per slab
-constexpr int kSwStages = 3; // slab stages per warp (two in flight while one is consumed)
+#ifndef MMOT_SW_STAGES
+#define MMOT_SW_STAGES 3
+#endif
+#ifndef MMOT_SW_MINB3
+#define MMOT_SW_MINB3 2
+#endif
+#ifndef MMOT_SW_SCL
+#define MMOT_SW_SCL 1
+#endif
+constexpr int kSwStages = MMOT_SW_STAGES; // slab stages per warp (two in flight while one is consumed)
 
 // Issue slab s (offsets s*S .. s*S+S-1) of NV vectors for the warp's 32 chains (block base
 // offset wbase = chain0 * P) into stage buffer sbuf [NV][S][32]: NV bulk copies of S*256 bytes.
@@ -1193,7 +1202,7 @@ __device__ __forceinline__ void rx_shfl(double (&D)[Rx<NB>::SZE], const double (
 }
 
 template <int NB, typename T, int MODE, bool NEXT, bool NXR = false>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply(Plan p) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : (NB == 3 ? MMOT_SW_MINB3 : 2)) k_sw_apply(Plan p) {
     using AV = ApplyVecs<NB, MODE>;
     constexpr int M = 1 << NB;
     constexpr int S = kSwS;
@@ -1300,6 +1309,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
             }
         }
     }
+    // Scaled frames (fp64): the prefix states are kept as F~ = F w_1^{-t} and the suffix states as
+    // B~ = B w_1^{t} (t = points walked, counting the diag of the edge entering the chain), so the
+    // per-level diag multipliers become w_a / w_1 and w_1 / w_a -- exactly 1 for |S| in {1, l-1}
+    // (w_{l-1} = w_1): those states need no multiply -- while the combine sum_S F~[S] U~[S^c] is J
+    // itself (the scales cancel).  DESIGN.md §5.
+    constexpr bool SCL = MMOT_SW_SCL && sizeof(T) == sizeof(double);
+    double cF[NB + 2], cB[NB + 2];
+    if constexpr (SCL) {
+        const double w1 = value_of(wt[1]);
+#pragma unroll
+        for (int a = 0; a <= NB + 1; ++a) {
+            cF[a] = a == 0 ? rw1inv : rwr[a];
+            cB[a] = a == 0 ? w1 : 1.0 / rwr[a];
+        }
+#pragma unroll
+        for (int S = 0; S < M; ++S) reinterpret_cast<double &>(B[S]) *= w1;
+    }
     // the next-update operator step of point m is issued after the scans of point m+1
     // (software pipelining: the division of point m overlaps the scans of point m+1)
     double fprev[NB > 0 ? NB : 1], oprev = 0.0;
@@ -1323,7 +1349,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
             double f[NB > 0 ? NB : 1];
 #pragma unroll
             for (int b = 0; b < NB; ++b) f[b] = cur[(b * S + j) * 32 + lane];
-            dp_diag<NB, T, true>(F, wt);
+            if constexpr (SCL) dp_diag_lvl<NB>(reinterpret_cast<double(&)[M]>(F), cF);
+            else dp_diag<NB, T, true>(F, wt);
             dp_place<NB, T>(F, f);
             double Bo[MO];
             if constexpr (NXR) {
@@ -1332,7 +1359,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
             }
             dp_unplace<NB, T>(B, f);          // B := U_m = D B_{m+1}
             const T J = combine<NB, T>(F, B);
-            dp_diag_inv<NB, T>(B, wi);        // B := B_{m+1}
+            if constexpr (SCL) dp_diag_lvl<NB>(reinterpret_cast<double(&)[M]>(B), cB);
+            else dp_diag_inv<NB, T>(B, wi);   // B := B_{m+1}
             if constexpr (NEXT) {
                 if (j > 0 || have_prev) next_ops_step<NB, T>(Gx, wt, fprev, oprev, j == 1 && s == 0);
             }
@@ -1366,10 +1394,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
             if constexpr (NXR) {
                 if constexpr (sizeof(T) == sizeof(double)) {
                     const bool first = j == 0 && s == 0;
-                    rx_M_acc_scaled<NB>(rM, rG, rwr, rw1inv, o * rgs, Bo, first);  // rM kept as M / w_1
+                    if constexpr (SCL) {
+                        // Bo is B~ = B w_1^{t}: o * Bo = w_1^2 (o * rgs * B) -- rM kept as M w_1
+                        rx_M_acc_scaled<NB>(rM, rG, rwr, 1.0, o, Bo, first);
+                    } else {
+                        rx_M_acc_scaled<NB>(rM, rG, rwr, rw1inv, o * rgs, Bo, first);  // rM kept as M / w_1
+                    }
                     rx_G_step_scaled<NB>(rG, rwr, f, first);
                     if (!first) rgs *= reinterpret_cast<const double *>(wt)[1];
-                    rx_L_step<NB>(rL, reinterpret_cast<const double *>(wt), f, o, reinterpret_cast<const double(&)[M]>(F));
+                    if constexpr (SCL)  // L kept as L w_1^{-t}, like F
+                        rx_L_step_scl<NB>(rL, rwr, f, o, reinterpret_cast<const double(&)[M]>(F));
+                    else
+                        rx_L_step<NB>(rL, reinterpret_cast<const double *>(wt), f, o, reinterpret_cast<const double(&)[M]>(F));
                 }
             }
         }
@@ -1387,10 +1423,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
     if (live && p.sw_end) {
         // walked suffix state after the chain's last point and the prefix state at that point
         T *e = static_cast<T *>(p.sw_end) + c * 2 * M;
+        if constexpr (SCL) {
+            // t = P at the chain end: F = F~ w_1^P, B = B~ w_1^{-(P+1)}
+            const double w1 = value_of(wt[1]);
+            const double wp = pow(w1, (double)p.P), wpi = 1.0 / (wp * w1);
 #pragma unroll
-        for (int R = 0; R < M; ++R) {
-            e[R] = B[R];
-            e[M + R] = F[R];
+            for (int R = 0; R < M; ++R) {
+                e[R] = reinterpret_cast<const double &>(B[R]) * wpi;
+                e[M + R] = reinterpret_cast<const double &>(F[R]) * wp;
+            }
+        } else {
+#pragma unroll
+            for (int R = 0; R < M; ++R) {
+                e[R] = B[R];
+                e[M + R] = F[R];
+            }
         }
     }
     if constexpr (NEXT) {
@@ -1405,8 +1452,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, NB >= 4 ? 1 : 2) k_sw_apply
         for (int c = 0; c < NB; ++c)
 #pragma unroll
             for (int U = 0; U < MO; ++U) rG[c][U] *= rgs;  // unscale the running operator
+        if constexpr (SCL) {
+            const double wp = rgs * value_of(wt[1]);  // w_1^P
 #pragma unroll
-        for (int U = 0; U < MO; ++U) rM[U] *= value_of(wt[1]);  // and the suffix offset
+            for (int U = 0; U < MO; ++U) {
+                rM[U] *= rw1inv;  // rM was kept as M w_1
+                rL[U] *= wp;      // rL as L w_1^{-P}
+            }
+        } else {
+#pragma unroll
+            for (int U = 0; U < MO; ++U) rM[U] *= value_of(wt[1]);  // and the suffix offset
+        }
         rx_store<NB>(rG, rL, rM, reinterpret_cast<const double *>(wt), ef, eb);
         if (!live) {
             rx_identity<NB>(ef);
