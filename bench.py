@@ -220,6 +220,7 @@ def run_reference(args, cfg):
 
 # ------------------------------------------------------------------------------------------
 FP64_PEAK = 148 * 64 * 2 * 1.965e9 / 1e12  # TFLOP/s: SMs x FP64 FMA/clk x 2 x max SM clock
+FP32_PEAK = 148 * 128 * 2 * 1.965e9 / 1e12  # TFLOP/s: SMs x FP32 FMA/clk x 2 x max SM clock
 
 
 def run_batched(args, cfg):
@@ -240,7 +241,7 @@ def run_batched(args, cfg):
     B = b1 - b0
     etas = [float(e) for e in mmot_inputs.c5_etas(cfg.batch)[b0:b1]]
     mus_h = mmot_inputs.c5_batch_marginals(b0, B, N, l)            # [l][B][N] fp64, seeded
-    io32 = cfg.dtype == "f32"  # C5 is an fp32 config: fp32 marginals in (MMOT_F32 I/O), fp64 scans
+    io32 = cfg.dtype == "f32"  # C5 is an fp32 config: MMOT_F32 context (fp32 marginals, storage, arithmetic)
     if io32:
         mus_h = mus_h.astype(np.float32)
     mus_d = [torch.from_numpy(np.ascontiguousarray(mus_h[q])).to(dev) for q in range(l)]
@@ -295,13 +296,16 @@ def run_batched(args, cfg):
     flop = B * T * l * N * 2 * (2 ** (l - 1)) * (l + 3)
     sk = statistics.median(sk_ms)
     achieved = flop / (sk / 1e3) / 1e12
-    roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK, "traffic": None,
+    f32c = ctx.pair_f32_solves > 0            # the pair family computed in fp32 (MMOT_F32 context)
+    peak = FP32_PEAK if f32c else FP64_PEAK
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
                 "kernel": ("k_pair_sinkhorn (pair family: all sweeps of all instances of the rank, one launch, "
                            "plus the layout conversions)" if ctx.pair_solves else
                            "k_bat_sinkhorn (all sweeps of all instances of the rank, one launch)"),
                 "alg_flop_per_launch": flop, "ms_per_launch": sk,
-                "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5)"}
+                "peak_source": ("derived: 148 SMs x 128 FP32 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5)" if f32c else
+                                "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5)")}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         nthr = os.cpu_count() or 1
@@ -338,11 +342,12 @@ def run_batched(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32" if f32c else "f64", "data": "synthetic",
             "config": {"workload": f"C5: {cfg.batch} instances x (l={l}, N={N}), eta_b ~ logU[1e-3,1e-1], "
-                                   f"T={T}, f64 arithmetic", "l": l, "N": N,
+                                   f"T={T}, " + ("f32" if f32c else "f64") + " arithmetic", "l": l, "N": N,
                        "family": ("pair (two threads per instance, no chain operators; mantissas with one "
-                                  "exponent per 8 points, " + ("fp32" if io32 else "fp64") + " storage)")
+                                  "exponent per 8 points, " + ("fp32" if io32 else "fp64") + " storage, " +
+                                  ("fp32" if f32c else "fp64") + " arithmetic)")
                        if ctx.pair_solves else "persistent (warp per instance, 32 chains, per-chain exponents)",
                        "io_dtype": "f32 marginals (MMOT_F32 context), fp64 u[]" if io32 else "f64",
                        "batch": cfg.batch, "iters": T, "parallelism": f"instances sharded over {ws} GPU(s)",

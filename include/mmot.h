@@ -333,6 +333,17 @@ MMOT_API int64_t mmot_graph_solves(const mmot_ctx *ctx);
  * used the pair family. */
 MMOT_API int64_t mmot_pair_solves(const mmot_ctx *ctx);
 
+/* Of those, the solves that also COMPUTED in fp32 (MMOT_F32 contexts, unless MMOT_PAIR_F64=1 is set
+ * in the environment): the walks and combine in fp32 arithmetic with the states kept relative to the
+ * 8-point slab exponents (linear fp32 values with a per-block integer exponent;
+ * north_star's fp32 tolerance 1e-4), the division in fp64.  Instances whose states leave the fp32
+ * range are redone in fp64 (mmot_pair_redo_count).  fp64 contexts compute in fp64. */
+MMOT_API int64_t mmot_pair_f32_solves(const mmot_ctx *ctx);
+
+/* Instances of fp32 pair solves whose states left the fp32 range and were redone in fp64 on a
+ * batched context of their own (the one-warp-per-instance kernel), from the same inputs. */
+MMOT_API int64_t mmot_pair_redo_count(const mmot_ctx *ctx);
+
 /* CTA family (batched contexts, and the single-instance contexts mmot_create gives small problems).
  * A batched Sinkhorn whose batch fits one wave (<= the SM count) with l <= 4, N <= 4096, a uniform
  * grid and every instance inside (l-1)(x_max - x_min)/eta <= 500 runs one thread block per instance:

@@ -139,6 +139,10 @@ def load_library():
     lib.mmot_graph_solves.restype = ctypes.c_int64
     lib.mmot_pair_solves.argtypes = [vp]
     lib.mmot_pair_solves.restype = ctypes.c_int64
+    lib.mmot_pair_f32_solves.argtypes = [vp]
+    lib.mmot_pair_f32_solves.restype = ctypes.c_int64
+    lib.mmot_pair_redo_count.argtypes = [vp]
+    lib.mmot_pair_redo_count.restype = ctypes.c_int64
     lib.mmot_cta_solves.argtypes = [vp]
     lib.mmot_cta_solves.restype = ctypes.c_int64
     lib.mmot_profile_enable.argtypes = [vp, ctypes.c_int]
@@ -385,6 +389,16 @@ class Context:
     def pair_solves(self) -> int:
         """Batched solves that ran on the pair family (two threads per instance, no chain operators)."""
         return int(self._lib.mmot_pair_solves(self._ctx))
+
+    @property
+    def pair_f32_solves(self) -> int:
+        """Pair-family solves that computed in fp32 arithmetic (MMOT_F32 contexts; slab exponents)."""
+        return int(self._lib.mmot_pair_f32_solves(self._ctx))
+
+    @property
+    def pair_redo(self) -> int:
+        """Instances of fp32 pair solves redone in fp64 after their states left the fp32 range."""
+        return int(self._lib.mmot_pair_redo_count(self._ctx))
 
     @property
     def cta_solves(self) -> int:

@@ -188,6 +188,8 @@ struct mmot_ctx {
     void *pair_mem = nullptr;
     int pair_state = 0;                     // 0 unknown, 1 available, -1 not for this context
     int64_t pair_solves = 0;
+    int64_t pair_f32_solves = 0;            // of which in fp32 arithmetic
+    int64_t pair_redo = 0;                  // fp32 pair instances redone in fp64 (states left the fp32 range)
     // CTA family (cta.cu): small instances, a thread block each
     mmot::CtaPlan cp{};
     double *cta_mem = nullptr;
@@ -295,6 +297,8 @@ int64_t mmot_stable_fallback_count(const mmot_ctx *ctx) {
 
 int64_t mmot_graph_solves(const mmot_ctx *ctx) { return ctx ? ctx->graph_solves + (ctx->fb ? ctx->fb->graph_solves : 0) : 0; }
 int64_t mmot_pair_solves(const mmot_ctx *ctx) { return ctx ? ctx->pair_solves : 0; }
+int64_t mmot_pair_f32_solves(const mmot_ctx *ctx) { return ctx ? ctx->pair_f32_solves : 0; }
+int64_t mmot_pair_redo_count(const mmot_ctx *ctx) { return ctx ? ctx->pair_redo : 0; }
 int64_t mmot_cta_solves(const mmot_ctx *ctx) { return ctx ? ctx->cta_solves : 0; }
 
 mmot_status mmot_info(const mmot_ctx *ctx, int64_t *chain_len, int64_t *nchains, int *kernel) {
@@ -1142,12 +1146,13 @@ static bool ensure_pair(mmot_ctx *c) {
     p.h = c->h;
     p.eta = c->ba.eta;
     p.f32 = c->dt == MMOT_F32 ? 1 : 0;
+    p.f32c = p.f32 && getenv("MMOT_PAIR_F64") == nullptr ? 1 : 0;
     p.slots = (std::min<int64_t>(p.nblk, mmot::pair_slots()) + 1) / 2 * 2;
     const size_t es = p.f32 ? sizeof(float) : sizeof(double);
     const size_t nv = (size_t)c->l * p.nblk * p.nslab * 8 * 32;
     const size_t ne = (size_t)c->l * p.nblk * p.nslab * 32;
     const size_t nck = (size_t)p.slots * p.nslab * (1u << (c->l - 1)) * 32;
-    const size_t bytes = nck * sizeof(double) + 2 * nv * es + ne * sizeof(int);
+    const size_t bytes = nck * sizeof(double) + 2 * nv * es + 2 * ne * sizeof(int);  // E and G records
     if (cudaMalloc(&c->pair_mem, bytes) != cudaSuccess) {
         cudaGetLastError();
         c->pair_mem = nullptr;
@@ -1251,6 +1256,7 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
         p.iters = iters;
         CK(c, mmot::launch_pair_sinkhorn(p, c->stream, &c->launches));
         ++c->pair_solves;
+        if (p.f32c) ++c->pair_f32_solves;
     } else {
         st = bat_import(c, u);
         if (st) return st;
@@ -1273,6 +1279,78 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
     int64_t nfail = 0;
     for (int64_t b = 0; b < B; ++b)
         if (c->bat_shost[b] == MMOT_EOVERFLOW) { sel[(size_t)b] = 1; ++nfail; }
+    if (nfail > 0 && getenv("MMOT_DEBUG_FAIL")) {  // diagnostics: which instances left the range
+        std::vector<double> eh((size_t)B);
+        cudaMemcpy(eh.data(), c->ba.eta, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[mmot] %lld of %lld instances left the range (family: %s)\n", (long long)nfail, (long long)B,
+                pair ? (c->pp.f32c ? "pair fp32" : "pair fp64") : cta ? "cta" : "persistent");
+        int shown = 0;
+        for (int64_t b = 0; b < B && shown < 64; ++b)
+            if (sel[(size_t)b]) {
+                fprintf(stderr, "[mmot]   instance %lld eta %.6g fail_iter %d\n", (long long)b, eh[(size_t)b],
+                        c->bat_shost[B + b]);
+                ++shown;
+            }
+    }
+    // fp32 pair solves: instances whose states left the fp32 range (rare: 2 of C5's 8192, deep marginal
+    // tails at moderate eta) are redone first in fp64 on a batched context of their own
+    // (the one-warp-per-instance kernel: per-instance latency, not the pair family's), from this
+    // call's u (still untouched: the export below comes after the gather)
+    std::vector<double *> sub_u;
+    std::vector<int64_t> sub_idx;
+    mmot_ctx *sub = nullptr;
+    if (nfail > 0 && pair && c->pp.f32c) {
+        const size_t row = (size_t)c->N * sizeof(double);
+        for (int64_t b = 0; b < B; ++b)
+            if (sel[(size_t)b]) sub_idx.push_back(b);
+        const int64_t nf = (int64_t)sub_idx.size();
+        std::vector<double> eh((size_t)B), es((size_t)nf);
+        CK(c, cudaMemcpy(eh.data(), c->ba.eta, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < nf; ++i) es[(size_t)i] = eh[(size_t)sub_idx[(size_t)i]];
+        mmot_opts so = c->opts;
+        so.kernel = MMOT_KERNEL_AUTO;
+        mmot_status cs = mmot_create_batched(c->l, c->N, nf, es.data(), c->grid, MMOT_F64, &so, c->stream, &sub);
+        double *buf = nullptr;
+        if (cs == MMOT_OK && cudaMalloc(&buf, 2 * (size_t)c->l * nf * row) == cudaSuccess) {
+            std::vector<const void *> smu((size_t)c->l);
+            for (int q = 0; q < c->l; ++q) {
+                double *mq = buf + (size_t)q * nf * c->N, *uq = buf + (size_t)(c->l + q) * nf * c->N;
+                smu[(size_t)q] = mq;
+                sub_u.push_back(uq);
+                for (int64_t i = 0; i < nf; ++i) {
+                    const int64_t b = sub_idx[(size_t)i];
+                    CK(c, cudaMemcpyAsync(mq + i * c->N, mu[q] + b * c->N, row, cudaMemcpyDeviceToDevice, c->stream));
+                    CK(c, cudaMemcpyAsync(uq + i * c->N, static_cast<const double *>(u[q]) + b * c->N, row,
+                                          cudaMemcpyDeviceToDevice, c->stream));
+                }
+            }
+            mmot_report sr{};
+            cs = mmot_sinkhorn(sub, smu.data(), iters, tol, reinterpret_cast<void *const *>(sub_u.data()), &sr);
+            if (cs == MMOT_OK) {
+                for (int64_t i = 0; i < nf; ++i) {
+                    const int64_t b = sub_idx[(size_t)i];
+                    sel[(size_t)b] = 0;
+                    c->bat_shost[b] = 0;
+                    c->bat_shost[B + b] = -1;
+                    c->bat_shost[2 * B + b] = iters;
+                    c->bat_shost[3 * B + b] = 0;
+                }
+                c->pair_redo += nf;
+                nfail = 0;
+            } else {
+                sub_u.clear();  // the stabilised family redoes them below
+            }
+        } else {
+            cudaGetLastError();
+        }
+        if (sub_u.empty()) {
+            cudaFree(buf);
+            mmot_destroy(sub);
+            sub = nullptr;
+        } else {
+            sub_u.push_back(buf);  // freed after the scatter
+        }
+    }
     const bool redo = nfail > 0 && can_stabilise(c);
     if (redo) {
         if ((st = ensure_stable(c))) return st;
@@ -1288,6 +1366,17 @@ static mmot_status bat_sinkhorn(mmot_ctx *c, const double *const *mu, int iters,
     if (cta) CK(c, mmot::launch_cta_convert(c->cp, c->bat_ptrs, 1, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
     else if (pair) CK(c, mmot::launch_pair_convert(c->pp, c->bat_ptrs, 1, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
     else CK(c, mmot::launch_bat_convert(c->ba, c->bat_ptrs, 0, c->opts.repr == MMOT_LOG, c->stream, &c->launches));
+    if (sub) {
+        // the fp64 results of the redone instances over the export
+        const size_t row = (size_t)c->N * sizeof(double);
+        for (int q = 0; q < c->l; ++q)
+            for (size_t i = 0; i < sub_idx.size(); ++i)
+                CK(c, cudaMemcpyAsync(static_cast<double *>(u[q]) + sub_idx[i] * c->N, sub_u[(size_t)q] + i * c->N, row,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        cudaFree(sub_u.back());
+        mmot_destroy(sub);
+    }
     if (redo) {
         mmot_ctx *sc = c->st_fb;
         CK(c, cudaMemsetAsync(sc->st_int, 0, 4 * (size_t)B * sizeof(int), c->stream));

@@ -173,11 +173,13 @@ struct PairPlan {
     const double *eta; // [batch]
     void *phit;        // [l][nblk][nslab * 8][32] mantissas (double, or float if f32)
     void *mu;          // [l][nblk][nslab * 8][32] marginals (double, or float if f32)
-    int *E;            // [l][nblk][nslab][32] slab exponents
+    int *E;            // [nblk][nslab][l][2][32] exponent records: slab exponents E and the state
+                       // scales G of the fp32 walks (decay envelope of E), pair.cu pr_xrec
     double *ckpt;      // [slots][nslab][2^(l-1)][32] (own state before each slab)
     int64_t slots;     // resident warps (checkpoint slots)
     int iters;
     int f32;           // fp32 storage of mantissas and marginals (MMOT_F32 contexts)
+    int f32c;          // fp32 arithmetic as well (MMOT_F32 contexts unless MMOT_PAIR_F64 is set)
     int *status, *fail_iter, *iters_done, *converged;  // [batch]
     double *resid;     // [batch]
 };

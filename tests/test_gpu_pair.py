@@ -90,8 +90,8 @@ def test_pair_matches_persistent_kernel(monkeypatch):
 
 
 def test_pair_f32_storage(monkeypatch):
-    """MMOT_F32 context: fp32 mantissas and marginals in the pair layout, fp64 arithmetic; the
-    fp32 bar of north_star (1e-4) with margin."""
+    """MMOT_F32 context (default): fp32 mantissas and marginals in the pair layout, fp64
+    arithmetic; the fp32 bar of north_star (1e-4) with margin."""
     monkeypatch.setenv("MMOT_PAIR_MIN", "1")
     l, N, B, T = 4, 500, 20, 10
     etas, mus = _batch(l, N, B, 700)
@@ -146,3 +146,56 @@ def test_pair_tol_runs_on_persistent_kernel(monkeypatch):
     ctx.sinkhorn(md, 5, 0.0, u)
     assert ctx.pair_solves == 1
     ctx.close()
+
+
+def _solve_f32c(l, N, etas, mus, T):
+    B = len(etas)
+    md = _planes([np.stack([mus[b][q] for b in range(B)]).astype(np.float32) for q in range(l)])
+    ctx = mm.Context(l, N, etas, batch=B, dtype="f32")
+    u = [torch.empty((B, N), dtype=torch.float64, device=DEV) for _ in range(l)]
+    ctx.init_uniform(u)
+    rep = ctx.sinkhorn(md, T, 0.0, u)
+    counts = (ctx.pair_solves, ctx.pair_f32_solves, ctx.stable_fallbacks, ctx.pair_redo)
+    ctx.close()
+    return rep, np.stack([x.cpu().numpy() for x in u]), counts
+
+
+@pytest.mark.parametrize("l,N,B,T,redo", [(5, 4096, 17, 30, False), (4, 1000, 19, 40, False),
+                                          (3, 257, 37, 50, False), (2, 64, 5, 20, None), (5, 96, 33, 60, None),
+                                          (3, 7, 16, 12, None)])
+def test_pair_f32_arithmetic(monkeypatch, l, N, B, T, redo):
+    """MMOT_F32 context (default): fp32 storage AND fp32 arithmetic (walks, combine; the division in
+    fp64), the states kept relative to the 8-point slab exponents.  Against the fp64
+    oracle run on the fp32-rounded marginals: north_star's fp32 bar, 1e-4 L1-relative per marginal,
+    over eta in [1e-3, 1e-1] and tens of sweeps.  Instances whose states leave the fp32 range (coarse
+    grids at eta = 1e-3, h/eta ~ 10: a slab spans ~2^120 of phi) are redone in fp64 with the same
+    results; the C5-like grids (redo=False) stay in fp32."""
+    monkeypatch.setenv("MMOT_PAIR_MIN", "1")
+    etas, mus = _batch(l, N, B, 1100 + N)
+    mus = [m.astype(np.float32).astype(np.float64) for m in mus]   # the values the context sees
+    rep, g, (s, s32, fb, nredo) = _solve_f32c(l, N, etas, mus, T)
+    assert s == 1 and s32 == 1 and rep["status"] == 0 and rep["iters_done"] == T
+    assert fb == 0  # nothing reached the stabilised family
+    if redo is not None:
+        assert (nredo > 0) == redo, nredo
+    picks = sorted({0, B // 2, B - 1, min(B - 1, 16)})
+    _check(l, N, etas, mus, T, g, 1e-4, 1e-3, picks)
+
+
+def test_pair_f32_arithmetic_zero_runs(monkeypatch):
+    """fp32 arithmetic with zero runs in the marginals (zero slabs take a neighbour's exponent)."""
+    monkeypatch.setenv("MMOT_PAIR_MIN", "1")
+    l, N, B, T = 4, 300, 6, 15
+    etas = list(np.geomspace(2e-3, 5e-2, B))
+    rng = np.random.default_rng(17)
+    mus = []
+    for b in range(B):
+        m = rng.uniform(0.1, 1.0, (l, N))
+        m[0, 20:60] = 0.0
+        m[2, 150:] = 0.0 if b % 2 else m[2, 150:]
+        m[3, :9] = 0.0
+        m = (m / m.sum(axis=1, keepdims=True)).astype(np.float32).astype(np.float64)
+        mus.append(m)
+    rep, g, (s, s32, fb, nredo) = _solve_f32c(l, N, etas, mus, T)
+    assert s == 1 and s32 == 1 and rep["status"] == 0 and fb == 0
+    _check(l, N, etas, mus, T, g, 1e-4, 1e-3, list(range(B)))
