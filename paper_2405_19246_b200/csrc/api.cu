@@ -619,13 +619,12 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
             w.lv_n[w.nlev++] = n;
             if (n <= B || w.nlev == mmot::kLsMaxLv) break;
         }
-        size_t nd = 2 * (size_t)w.C * 192 + 2 * (size_t)((w.C + B - 1) / B) * B * 192;
+        size_t nd = 2 * (size_t)w.C * 192;
         for (int lv = 0; lv < w.nlev; ++lv) nd += 2 * (size_t)w.lv_n[lv] * (192 + 32) + 2 * (size_t)((w.lv_n[lv] + B - 1) / B) * 192;
         if (w.lv_n[w.nlev - 1] <= B && cudaMalloc(&c->ls_mem, nd * sizeof(double)) == cudaSuccess) {
             double *q = c->ls_mem;
             w.ops_f = q; q += (size_t)w.C * 192;
             w.ops_b = q; q += (size_t)w.C * 192;
-            w.scr = q; q += 2 * (size_t)((w.C + B - 1) / B) * B * 192;
             for (int lv = 0; lv < w.nlev; ++lv)
                 for (int d = 0; d < 2; ++d) {
                     w.lv_excl[lv][d] = q; q += (size_t)w.lv_n[lv] * 192;

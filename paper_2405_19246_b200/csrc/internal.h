@@ -42,7 +42,6 @@ struct LsWork {
     double *lv_excl[kLsMaxLv][2];    // [n][192] exclusive in-block prefix per item, per direction
     double *lv_agg[kLsMaxLv][2];     // [n/16][192] block aggregates (= items of the next level)
     double *lv_car[kLsMaxLv][2];     // [n][32] state entering each item (scan order)
-    double *scr;                     // [2][ceil(C/16)][16][192] composition scratch
 };
 
 struct Plan {

@@ -10,13 +10,14 @@
 //   place  for each bound b: st[S] += f_b * st[S ^ b]      (S containing b; one shuffle + FMA)
 //   combine J = sum_S F[S] H[S^c]                         (one shuffle + a warp reduction)
 // and the chain operators (the extended walk of dp.cuh opx_*, slices c = 0..5) are 6 registers per
-// lane.  Chains of 32 points (3 125 chains at N = 1e5) and a two-level scan:
+// lane.  Chains of 32 points (3 125 chains at N = 1e5) and a multi-level scan:
 //   k_ls_ops    warp per chain: extended operator walk -> prefix / suffix operators (OpShape layout)
-//   k_ls_scan1  CTA per group of 32 chains (one warp each): Kogge-Stone over the group in shared
-//               memory, compositions driven by a balanced term table (648 terms over 32 lanes);
-//               stores each chain's inclusive in-group operator and the group aggregate
-//   k_ls_scan2  one CTA per direction: scan of the group aggregates -> the state vector entering
-//               every group (an operator applied to e_empty is its slice c = 0)
+//   k_ls_blockscan  per level, CTA per block of 16 items (one warp each): Kogge-Stone over the block
+//               in shared memory (two buffers), compositions driven by a balanced term table (648
+//               terms over 32 lanes); stores each item's exclusive in-block prefix and the block
+//               aggregate (the items of the next level)
+//   k_ls_down   per level, top first: carry(item) = excl(item) applied to carry(block) (an operator
+//               applied to e_empty is its slice c = 0)
 //   k_ls_apply  warp per chain: carries (in-group operator applied to the group carry), suffix walk
 //               with 8-point checkpoints, prefix walk with 8-point suffix rebuild, combine, epilogue.
 // Suffix direction: the same scan over the reversed chain order (the chain to the right is applied
@@ -39,9 +40,11 @@ constexpr int kLsNB = 5;
 constexpr int kLsM = 1 << kLsNB;              // 32 states = 32 lanes
 constexpr int kLsSZ = (kLsNB + 1) * kLsM;     // 192 operator entries
 constexpr int kLsZero = kLsSZ;                // zero slot index in shared operator buffers
-constexpr int kLsStride = kLsSZ + 1;
+constexpr int kLsSplit = kLsSZ + 1;            // scratch slot: second half of the split destination
+constexpr int kLsStride = kLsSZ + 2;
 constexpr int kLsMaxTerms = 40;                // per lane (648 terms / 32 lanes ~ 20.3 after balancing)
-constexpr int kLsT = 32;                       // terms per lane after balancing (the largest destination has 32)
+constexpr int kLsT = 24;                       // term slots per lane after balancing (multiple of 8)
+constexpr int kLsBig = kLsNB;                  // C_0[all bounds] (32 terms) is split into two 16-term halves
 
 // identity operator (G_c[V] = [V empty]): applying it returns the state unchanged
 __device__ double g_ls_ident[kLsSZ];
@@ -67,6 +70,13 @@ cudaError_t ls_init_tables() {
             Dst d{c * kLsM + V, {}};
             for (int U = 0; U < kLsM; ++U)
                 if ((U & V) == U) d.terms.push_back({c * kLsM + U, (c + ls_popc(U)) * kLsM + (V ^ U)});
+            if (c == 0 && V == kLsM - 1) {
+                // the only 32-term destination: two halves, the second summed into the scratch slot
+                // and added by ls_fix_split after the composition (keeps every lane at <= kLsT terms)
+                Dst h{kLsSplit, std::vector<std::pair<int, int>>(d.terms.begin() + 16, d.terms.end())};
+                d.terms.resize(16);
+                dsts.push_back(h);
+            }
             dsts.push_back(d);
         }
     std::sort(dsts.begin(), dsts.end(), [](const Dst &a, const Dst &b) { return a.terms.size() > b.terms.size(); });
@@ -98,49 +108,15 @@ cudaError_t ls_init_tables() {
 // This lane's terms of the composition table, loaded once per kernel into registers.
 
 
-// C = compose(A first, B second) in shared memory (stride kLsStride, zero slot at kLsZero); one warp.
-// Fully unrolled over the lane's terms: the shared loads of all terms are independent (only the
-// accumulation chains of one destination are sequential).
 extern __shared__ double ls_sm[];  // the scan kernels' dynamic shared memory (indexed, so every
                                    // access compiles to LDS / STS rather than generic loads)
 
 __shared__ uint32_t ls_tbl_sm[kLsT * 32];  // the composition term table, staged once per CTA
 
-// Cg = compose(A first, B second); A, B are offsets (in doubles) of operators in ls_sm, Cg a
-// GLOBAL scratch operator: the result stores cannot alias the shared operand loads, so the compiler
-// issues all of a lane's operand loads ahead of its accumulation chains.  The caller copies Cg back
-// (after __syncwarp + __threadfence_block).
 __device__ __forceinline__ double ls_lds(uint32_t a) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
     return v;
-}
-__device__ __forceinline__ void ls_compose_g(int A, int B, double *__restrict__ Cg) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(ls_sm + A);
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(ls_sm + B);
-    uint32_t e[kLsT];
-#pragma unroll
-    for (int t = 0; t < kLsT; ++t) e[t] = ls_tbl_sm[t * 32 + lane];
-    double acc = 0.0;
-#pragma unroll
-    for (int t0 = 0; t0 < kLsT; t0 += 16) {
-        // volatile shared loads keep their program order: all 32 are issued before the FMA chains
-        double a[16], b[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            a[k] = ls_lds(sa + 8u * (e[t0 + k] & 0xff));
-            b[k] = ls_lds(sb + 8u * ((e[t0 + k] >> 8) & 0xff));
-        }
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            asm volatile("fma.rn.f64 %0, %1, %2, %0;" : "+d"(acc) : "d"(a[k]), "d"(b[k]));
-            if (e[t0 + k] >> 24) {
-                __stcg(Cg + ((e[t0 + k] >> 16) & 0xff), acc);
-                acc = 0.0;
-            }
-        }
-    }
 }
 
 // y = G(x) for a state vector held one entry per lane (x: this lane's x[S]); G in memory (global or
@@ -192,10 +168,12 @@ __global__ void __launch_bounds__(128) k_ls_ops(Plan p, LsWork w) {
     }
 #pragma unroll
     for (int b = 0; b < NB; ++b) mb[b] = ((lane >> b) & 1) ? 1.0 : 0.0;
-    double stg[NB];
+    __shared__ double fsm[4][NB][kLsP];  // the chain's bound values (broadcast loads)
+    double (*fw)[kLsP] = fsm[(threadIdx.x >> 5) & 3];
     const int64_t xi = x0 + lane;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) stg[b] = xi < p.N ? p.bound[b][xi] : 0.0;
+    for (int b = 0; b < NB; ++b) fw[b][lane] = xi < p.N ? p.bound[b][xi] : 0.0;
+    __syncwarp();
     double G[NB + 1];
 #pragma unroll
     for (int cc = 0; cc <= NB; ++cc) G[cc] = lane == 0 ? 1.0 : 0.0;
@@ -203,7 +181,7 @@ __global__ void __launch_bounds__(128) k_ls_ops(Plan p, LsWork w) {
     for (int j = 0; j < kLsP; ++j) {
         double fm[NB];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) fm[b] = __shfl_sync(0xffffffffu, stg[b], j) * mb[b];
+        for (int b = 0; b < NB; ++b) fm[b] = fw[b][j] * mb[b];
         if (j > 0) {
 #pragma unroll
             for (int cc = 0; cc <= NB; ++cc) G[cc] *= wl[cc];
@@ -211,7 +189,16 @@ __global__ void __launch_bounds__(128) k_ls_ops(Plan p, LsWork w) {
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
 #pragma unroll
-            for (int cc = 0; cc <= NB; ++cc) G[cc] = fma(fm[b], __shfl_xor_sync(0xffffffffu, G[cc], 1 << b), G[cc]);
+            for (int cc = 0; cc < NB; ++cc) G[cc] = fma(fm[b], __shfl_xor_sync(0xffffffffu, G[cc], 1 << b), G[cc]);
+        }
+        // slice NB: entries in range are V = {} and V = {b} (c + |V| <= l), and place never changes
+        // G[{}], so G_NB[{b}] += f_b G_NB[{}] (the other lanes are out of range: diag 0 each step)
+        {
+            const double g0 = __shfl_sync(0xffffffffu, G[NB], 0);
+            double fs = 0.0;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) fs += fm[b];
+            G[NB] = fma(fs, g0, G[NB]);
         }
     }
     // prefix operator w_c Gt_c, suffix operator w_c Gt_{l-c-|V|} (Gt_l[{}] = 1)
@@ -231,7 +218,7 @@ __global__ void __launch_bounds__(128) k_ls_ops(Plan p, LsWork w) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Scan: a multi-level work-efficient (Blelloch) block scan over the operators, 32 items per CTA
+// Scan: a multi-level block scan over the operators, kLsB = 16 items per CTA
 // (one warp each), per direction (blockIdx.y; direction 1 runs over the reversed chain order).
 // Level L reads the items of level L (level 0: the chain operators), writes each item's exclusive
 // prefix within its block (excl: the composition of the block's earlier items) and the block
@@ -273,56 +260,87 @@ struct LsLevel {
     const double *in[2];
     double *excl[2];
     double *agg[2];
-    double *scr;  // global scratch [2][blocks][32][192] (composition results)
     int64_t n;
     int rev1;  // direction 1 reads `in` reversed (level 0: chain order)
 };
 
-__global__ void __launch_bounds__(kLsB * 32, 1) k_ls_blockscan(LsLevel L, const int *stop) {
+// Kogge-Stone over the kLsB items of a block (log2 kLsB = 4 dependent compositions instead of the
+// 2 log2 kLsB of a work-efficient tree), ping-ponging between two shared buffers: step d writes
+// buf[s^1][w] = compose(buf[s][w - d], buf[s][w]) (w >= d) or copies buf[s][w], so every
+// composition reads one buffer and stores into the other (no global round trip, no aliasing).
+__device__ __forceinline__ void ls_sts(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v));
+}
+// C = compose(A first, B second), A, B, C offsets (doubles) in ls_sm; C must not overlap A or B.
+__device__ __forceinline__ void ls_compose_s(int A, int B, int C) {
+    constexpr int TB = 8;  // terms per batch (kLsT % TB == 0): table entries, then all operand loads, then the FMAs
+    const int lane = threadIdx.x & 31;
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(ls_sm + A);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(ls_sm + B);
+    const uint32_t sc = (uint32_t)__cvta_generic_to_shared(ls_sm + C);
+    double acc = 0.0;
+#pragma unroll
+    for (int t0 = 0; t0 < kLsT; t0 += TB) {
+        uint32_t e[TB];
+        double a[TB], b[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) e[k] = ls_tbl_sm[(t0 + k) * 32 + lane];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+            a[k] = ls_lds(sa + 8u * (e[k] & 0xff));
+            b[k] = ls_lds(sb + 8u * ((e[k] >> 8) & 0xff));
+        }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+            asm volatile("fma.rn.f64 %0, %1, %2, %0;" : "+d"(acc) : "d"(a[k]), "d"(b[k]));
+            if (e[k] >> 24) {
+                ls_sts(sc + 8u * ((e[k] >> 16) & 0xff), acc);
+                acc = 0.0;
+            }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) ls_sts(sc + 8u * (kLsM - 1), ls_lds(sc + 8u * (kLsM - 1)) + ls_lds(sc + 8u * kLsSplit));
+}
+
+__global__ void __launch_bounds__(kLsB * 32, 2) k_ls_blockscan(LsLevel L, const int *stop) {
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
     const int dir = blockIdx.y;
     const int64_t item = (int64_t)blockIdx.x * kLsB + wi;
     if (*stop) return;
     ls_tbl_to_smem(ls_tbl_sm);
+    const int buf = kLsB * kLsStride;  // offset of the second buffer
     const int me = wi * kLsStride;
-    double *cg = L.scr + (((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * kLsB + wi) * kLsSZ;
+    const double *in = dir ? L.in[1] : L.in[0];
     if (item < L.n) {
         const int64_t src = (dir == 1 && L.rev1) ? L.n - 1 - item : item;
-        ls_load_op(me, L.in[dir] + src * kLsSZ, lane);
+        ls_load_op(me, in + src * kLsSZ, lane);
     } else {
         ls_set_identity(me, lane);
     }
+    if (lane == 0) ls_sm[buf + me + kLsZero] = 0.0;
     __syncthreads();
-    // up-sweep: buf[w] <- compose(buf[w - d], buf[w]) for w = 2d-1, 4d-1, ...
+    int cur = 0;
+#pragma unroll
     for (int d = 1; d < kLsB; d <<= 1) {
-        if (((wi + 1) & (2 * d - 1)) == 0) {
-            ls_compose_g(me - d * kLsStride, me, cg);
-            __syncwarp();
-            __threadfence_block();
-            ls_load_op(me, cg, lane);
-        }
+        const int src = cur, dst = cur ^ buf;
+        if (wi >= d) ls_compose_s(src + me - d * kLsStride, src + me, dst + me);
+        else ls_copy_op(dst + me, src + me, lane);
+        cur = dst;
         __syncthreads();
     }
-    if (wi == kLsB - 1) {
-        if (L.agg[dir]) ls_store_op(L.agg[dir] + (int64_t)blockIdx.x * kLsSZ, me, lane);
-        __syncwarp();
-        ls_set_identity(me, lane);
-    }
-    __syncthreads();
-    // down-sweep: (left, right) <- (right, compose(right, left)) -- the parent's prefix first
-    for (int d = kLsB / 2; d >= 1; d >>= 1) {
-        if (((wi + 1) & (2 * d - 1)) == 0) {
-            const int left = me - d * kLsStride;
-            ls_compose_g(me, left, cg);
-            __syncwarp();
-            __threadfence_block();
-            ls_copy_op(left, me, lane);
-            __syncwarp();
-            ls_load_op(me, cg, lane);
+    // cur holds the inclusive in-block prefixes; exclusive = the previous item's inclusive
+    double *ex = dir ? L.excl[1] : L.excl[0];
+    double *ag = dir ? L.agg[1] : L.agg[0];
+    if (item < L.n) {
+        if (wi == 0) {
+#pragma unroll
+            for (int cc = 0; cc <= kLsNB; ++cc) ex[item * kLsSZ + cc * kLsM + lane] = lane == 0 ? 1.0 : 0.0;
+        } else {
+            ls_store_op(ex + item * kLsSZ, cur + me - kLsStride, lane);
         }
-        __syncthreads();
     }
-    if (item < L.n) ls_store_op(L.excl[dir] + item * kLsSZ, me, lane);
+    if (wi == kLsB - 1 && ag) ls_store_op(ag + (int64_t)blockIdx.x * kLsSZ, cur + me, lane);
 }
 
 // carry[item] = excl[item](carry_parent[item / 32]) (e_empty above the top level), per direction.
@@ -359,15 +377,24 @@ __global__ void __launch_bounds__(128) k_ls_apply(Plan p, LsWork w) {
     for (int b = 0; b < NB; ++b) mb[b] = ((lane >> b) & 1) ? 1.0 : 0.0;
     // carries: prefix state entering the chain, suffix state after its last point
     // carries (level 0 of the scan, in scan order: direction 1 is reversed)
-    double F = w.lv_car[0][0][c * M + lane], B = w.lv_car[0][1][(w.C - 1 - c) * M + lane];
-    // the chain's bound values in registers (lane j: point x0 + j), padded with zeros beyond N
-    double stg[NB];
+    // (level 0 of the down pass, fused here: the chain's exclusive in-block prefix applied to the
+    // state entering its block; e_empty when the scan has a single level)
+    const int64_t rb = w.C - 1 - c;
+    const double pf0 = w.nlev > 1 ? w.lv_car[1][0][(c / kLsB) * M + lane] : (lane == 0 ? 1.0 : 0.0);
+    const double pb0 = w.nlev > 1 ? w.lv_car[1][1][(rb / kLsB) * M + lane] : (lane == 0 ? 1.0 : 0.0);
+    double F = ls_apply(w.lv_excl[0][0] + c * kLsSZ, pf0, lane);
+    double B = ls_apply(w.lv_excl[0][1] + rb * kLsSZ, pb0, lane);
+    // the chain's bound values (lane j: point x0 + j), padded with zeros beyond N, staged in shared
+    // memory: f_b at a point is then one broadcast load instead of two shuffles
+    __shared__ double fsm[4][NB][kLsP];
+    double (*fw)[kLsP] = fsm[(threadIdx.x >> 5) & 3];
     const int64_t xi = x0 + lane;
     const bool in = xi < p.N;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) stg[b] = in ? p.bound[b][xi] : 0.0;
+    for (int b = 0; b < NB; ++b) fw[b][lane] = in ? p.bound[b][xi] : 0.0;
     const double vmu = (MODE == MODE_UPD || MODE == MODE_RES) && in ? p.muk[xi] : 0.0;
     const double vph = (MODE == MODE_MARG || MODE == MODE_RES) && in ? p.phik[xi] : 0.0;
+    __syncwarp();
     // walk 1 (right to left): checkpoints ck[q] = B at x0 + Q (q+1)
     double ck[NQ];
 #pragma unroll
@@ -378,14 +405,16 @@ __global__ void __launch_bounds__(128) k_ls_apply(Plan p, LsWork w) {
             for (int m = Q - 1; m >= 0; --m) {
                 double f[NB];
 #pragma unroll
-                for (int b = 0; b < NB; ++b) f[b] = __shfl_sync(0xffffffffu, stg[b], q * Q + m);
+                for (int b = 0; b < NB; ++b) f[b] = fw[b][q * Q + m];
                 B *= wl;                   // edge (m, m+1)
                 B = ls_place(B, f, mb);
             }
         }
     }
-    // walk 2 (left to right): rebuild the Q suffix states of each block, prefix step, combine
-    double tj = 0.0;  // J of this lane's point (lane j <-> x0 + j), selected without branches
+    // walk 2 (left to right): rebuild the Q suffix states of each block, prefix step, the terms
+    // F[S] H[S^c] of the block's Q points, then one reduce-scatter of the Q sums over the lanes
+    const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
+    double tj = 0.0;  // J of this lane's point (lane j <-> x0 + j)
 #pragma unroll 1
     for (int q = 0; q < NQ; ++q) {
         double H[Q];
@@ -397,23 +426,40 @@ __global__ void __launch_bounds__(128) k_ls_apply(Plan p, LsWork w) {
             if (i > 0) {
                 double f[NB];
 #pragma unroll
-                for (int b = 0; b < NB; ++b) f[b] = __shfl_sync(0xffffffffu, stg[b], q * Q + i);
+                for (int b = 0; b < NB; ++b) f[b] = fw[b][q * Q + i];
                 st = ls_place(st, f, mb);
             }
         }
+        double v[Q];
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
-            const int m = q * Q + i;
             double f[NB];
 #pragma unroll
-            for (int b = 0; b < NB; ++b) f[b] = __shfl_sync(0xffffffffu, stg[b], m);
+            for (int b = 0; b < NB; ++b) f[b] = fw[b][q * Q + i];
             F *= wl;
             F = ls_place(F, f, mb);
-            double t = F * __shfl_xor_sync(0xffffffffu, H[i], M - 1);  // F[S] H[S^c]
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
-            tj = lane == m ? t : tj;
+            v[i] = F * __shfl_xor_sync(0xffffffffu, H[i], M - 1);  // F[S] H[S^c]
         }
+        // reduce-scatter: after the three halving steps lane L holds the partial sum of point
+        // q Q + (L >> 2) over its 4-lane group's share; two butterflies finish it
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double snd = b4 ? v[k] : v[k + 4], kp = b4 ? v[k + 4] : v[k];
+            v[k] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const double snd = b3 ? v[k] : v[k + 2], kp = b3 ? v[k + 2] : v[k];
+            v[k] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+        }
+        {
+            const double snd = b2 ? v[0] : v[1], kp = b2 ? v[1] : v[0];
+            v[0] = kp + __shfl_xor_sync(0xffffffffu, snd, 4);
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        const double x = __shfl_sync(0xffffffffu, v[0], 4 * (lane & 7));
+        tj = (lane >> 3) == q ? x : tj;
     }
     bool bad = false;
     double acc = 0.0, o_mine = 0.0;
@@ -448,7 +494,7 @@ cudaError_t launch_ls_product(const Plan &p, const LsWork &w, int mode, cudaStre
     const unsigned wb = (unsigned)((w.C + 3) / 4);
     k_ls_ops<<<wb, 128, 0, s>>>(p, w);
     int nl = 0;
-    const size_t smb = kLsB * (size_t)kLsStride * sizeof(double);
+    const size_t smb = 2 * kLsB * (size_t)kLsStride * sizeof(double);
     smem_attr((const void *)k_ls_blockscan, smb);
     // up: level 0 = chains (direction 1 reversed), then block aggregates until one block remains
     for (int lv = 0; lv < w.nlev; ++lv) {
@@ -461,12 +507,11 @@ cudaError_t launch_ls_product(const Plan &p, const LsWork &w, int mode, cudaStre
         L.excl[1] = w.lv_excl[lv][1];
         L.agg[0] = lv + 1 < w.nlev ? w.lv_agg[lv][0] : nullptr;
         L.agg[1] = lv + 1 < w.nlev ? w.lv_agg[lv][1] : nullptr;
-        L.scr = w.scr;
         k_ls_blockscan<<<dim3((unsigned)((L.n + kLsB - 1) / kLsB), 2), kLsB * 32, smb, s>>>(L, p.stop);
         ++nl;
     }
     // down: carries of every level from the top; level 0's are the chain carries (scan order)
-    for (int lv = w.nlev - 1; lv >= 0; --lv) {
+    for (int lv = w.nlev - 1; lv >= 1; --lv) {  // level 0: inside k_ls_apply
         const int64_t n = w.lv_n[lv];
         const double *par0 = lv + 1 < w.nlev ? w.lv_car[lv + 1][0] : nullptr;
         const double *par1 = lv + 1 < w.nlev ? w.lv_car[lv + 1][1] : nullptr;
