@@ -25,6 +25,7 @@
 // op_compose) and apply as y[S] = sum_{U in S} x[U] G_{|U|}[S \ U] (op_apply).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
@@ -303,6 +304,11 @@ __device__ __forceinline__ void ls_compose_s(int A, int B, int C) {
     if (lane == 0) ls_sts(sc + 8u * (kLsM - 1), ls_lds(sc + 8u * (kLsM - 1)) + ls_lds(sc + 8u * kLsSplit));
 }
 
+// TREE = false: Kogge-Stone (depth log2 kLsB, 49 compositions per block; the upper levels, where a
+// few CTAs run alone and latency decides); TREE = true: work-efficient up / down sweep (depth
+// 2 log2 kLsB, 30 compositions; level 0, where hundreds of CTAs share the SMs' shared-memory
+// bandwidth), its results staged in the second buffer and copied back by the composing warp.
+template <bool TREE>
 __global__ void __launch_bounds__(kLsB * 32, 2) k_ls_blockscan(LsLevel L, const int *stop) {
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
     const int dir = blockIdx.y;
@@ -320,6 +326,40 @@ __global__ void __launch_bounds__(kLsB * 32, 2) k_ls_blockscan(LsLevel L, const 
     }
     if (lane == 0) ls_sm[buf + me + kLsZero] = 0.0;
     __syncthreads();
+    double *ex = dir ? L.excl[1] : L.excl[0];
+    double *ag = dir ? L.agg[1] : L.agg[0];
+    if (TREE) {
+        // up-sweep: buf[w] <- compose(buf[w - d], buf[w]) for w = 2d-1, 4d-1, ...
+#pragma unroll
+        for (int d = 1; d < kLsB; d <<= 1) {
+            if (((wi + 1) & (2 * d - 1)) == 0) {
+                ls_compose_s(me - d * kLsStride, me, buf + me);
+                __syncwarp();
+                ls_copy_op(me, buf + me, lane);
+            }
+            __syncthreads();
+        }
+        if (wi == kLsB - 1) {
+            if (ag) ls_store_op(ag + (int64_t)blockIdx.x * kLsSZ, me, lane);
+            __syncwarp();
+            ls_set_identity(me, lane);
+        }
+        __syncthreads();
+        // down-sweep: (left, right) <- (right, compose(right, left)) -- the parent's prefix first
+#pragma unroll
+        for (int d = kLsB / 2; d >= 1; d >>= 1) {
+            if (((wi + 1) & (2 * d - 1)) == 0) {
+                const int left = me - d * kLsStride;
+                ls_compose_s(me, left, buf + me);
+                __syncwarp();
+                ls_copy_op(left, me, lane);
+                ls_copy_op(me, buf + me, lane);
+            }
+            __syncthreads();
+        }
+        if (item < L.n) ls_store_op(ex + item * kLsSZ, me, lane);
+        return;
+    }
     int cur = 0;
 #pragma unroll
     for (int d = 1; d < kLsB; d <<= 1) {
@@ -330,8 +370,6 @@ __global__ void __launch_bounds__(kLsB * 32, 2) k_ls_blockscan(LsLevel L, const 
         __syncthreads();
     }
     // cur holds the inclusive in-block prefixes; exclusive = the previous item's inclusive
-    double *ex = dir ? L.excl[1] : L.excl[0];
-    double *ag = dir ? L.agg[1] : L.agg[0];
     if (item < L.n) {
         if (wi == 0) {
 #pragma unroll
@@ -495,7 +533,9 @@ cudaError_t launch_ls_product(const Plan &p, const LsWork &w, int mode, cudaStre
     k_ls_ops<<<wb, 128, 0, s>>>(p, w);
     int nl = 0;
     const size_t smb = 2 * kLsB * (size_t)kLsStride * sizeof(double);
-    smem_attr((const void *)k_ls_blockscan, smb);
+    smem_attr((const void *)k_ls_blockscan<false>, smb);
+    smem_attr((const void *)k_ls_blockscan<true>, smb);
+    static const int tree0 = getenv("MMOT_LS_KS0") ? 0 : 1;  // level 0: tree (default) or Kogge-Stone
     // up: level 0 = chains (direction 1 reversed), then block aggregates until one block remains
     for (int lv = 0; lv < w.nlev; ++lv) {
         LsLevel L{};
@@ -507,7 +547,9 @@ cudaError_t launch_ls_product(const Plan &p, const LsWork &w, int mode, cudaStre
         L.excl[1] = w.lv_excl[lv][1];
         L.agg[0] = lv + 1 < w.nlev ? w.lv_agg[lv][0] : nullptr;
         L.agg[1] = lv + 1 < w.nlev ? w.lv_agg[lv][1] : nullptr;
-        k_ls_blockscan<<<dim3((unsigned)((L.n + kLsB - 1) / kLsB), 2), kLsB * 32, smb, s>>>(L, p.stop);
+        const dim3 g((unsigned)((L.n + kLsB - 1) / kLsB), 2);
+        if (lv == 0 && tree0) k_ls_blockscan<true><<<g, kLsB * 32, smb, s>>>(L, p.stop);
+        else k_ls_blockscan<false><<<g, kLsB * 32, smb, s>>>(L, p.stop);
         ++nl;
     }
     // down: carries of every level from the top; level 0's are the chain carries (scan order)
