@@ -381,6 +381,52 @@ __global__ void __launch_bounds__(kLsB * 32, 2) k_ls_blockscan(LsLevel L, const 
     if (wi == kLsB - 1 && ag) ls_store_op(ag + (int64_t)blockIdx.x * kLsSZ, cur + me, lane);
 }
 
+// Upper levels (a few hundred items at most): one CTA per OUTPUT instead of per block.  CTA j < n
+// reduces the items of j's block before j (its exclusive in-block prefix), CTA n + b the whole block
+// b (the aggregate, when the level has a parent); each by a pairwise tree of depth <= log2 kLsB in
+// its own shared memory.  About 2.5x the compositions of a block scan, but spread over the GPU's
+// SMs instead of 16 warps on one SM, so the level costs one tree depth of latency.
+__global__ void __launch_bounds__(kLsB * 32, 2) k_ls_prefix_red(LsLevel L, const int *stop) {
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const int dir = blockIdx.y;
+    const int64_t j = blockIdx.x;
+    if (*stop) return;
+    int64_t first, cnt;
+    if (j < L.n) {
+        first = (j / kLsB) * kLsB;
+        cnt = j - first;
+    } else {
+        first = (j - L.n) * kLsB;
+        cnt = L.n - first < kLsB ? L.n - first : kLsB;
+    }
+    ls_tbl_to_smem(ls_tbl_sm);
+    const int buf = kLsB * kLsStride;
+    const int me = wi * kLsStride;
+    const double *in = dir ? L.in[1] : L.in[0];
+    if (wi < cnt) {
+        const int64_t it = first + wi;
+        const int64_t src = (dir == 1 && L.rev1) ? L.n - 1 - it : it;
+        ls_load_op(me, in + src * kLsSZ, lane);
+    } else if (wi == 0) {
+        ls_set_identity(me, lane);
+    }
+    if (lane == 0) ls_sm[buf + me + kLsZero] = 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int d = 1; d < kLsB; d <<= 1) {
+        if ((wi & (2 * d - 1)) == 0 && wi + d < cnt) {
+            ls_compose_s(me, me + d * kLsStride, buf + me);
+            __syncwarp();
+            ls_copy_op(me, buf + me, lane);
+        }
+        __syncthreads();
+    }
+    if (wi == 0) {
+        if (j < L.n) ls_store_op((dir ? L.excl[1] : L.excl[0]) + j * kLsSZ, 0, lane);
+        else ls_store_op((dir ? L.agg[1] : L.agg[0]) + (j - L.n) * kLsSZ, 0, lane);
+    }
+}
+
 // carry[item] = excl[item](carry_parent[item / 32]) (e_empty above the top level), per direction.
 __global__ void __launch_bounds__(128) k_ls_down(const double *excl0, const double *excl1, const double *par0,
                                                  const double *par1, double *car0, double *car1, int64_t n,
@@ -535,7 +581,9 @@ cudaError_t launch_ls_product(const Plan &p, const LsWork &w, int mode, cudaStre
     const size_t smb = 2 * kLsB * (size_t)kLsStride * sizeof(double);
     smem_attr((const void *)k_ls_blockscan<false>, smb);
     smem_attr((const void *)k_ls_blockscan<true>, smb);
+    smem_attr((const void *)k_ls_prefix_red, smb);
     static const int tree0 = getenv("MMOT_LS_KS0") ? 0 : 1;  // level 0: tree (default) or Kogge-Stone
+    static const int red_up = getenv("MMOT_LS_KS_UP") ? 0 : 1;  // upper levels: per-output trees
     // up: level 0 = chains (direction 1 reversed), then block aggregates until one block remains
     for (int lv = 0; lv < w.nlev; ++lv) {
         LsLevel L{};
@@ -549,7 +597,8 @@ cudaError_t launch_ls_product(const Plan &p, const LsWork &w, int mode, cudaStre
         L.agg[1] = lv + 1 < w.nlev ? w.lv_agg[lv][1] : nullptr;
         const dim3 g((unsigned)((L.n + kLsB - 1) / kLsB), 2);
         if (lv == 0 && tree0) k_ls_blockscan<true><<<g, kLsB * 32, smb, s>>>(L, p.stop);
-        else k_ls_blockscan<false><<<g, kLsB * 32, smb, s>>>(L, p.stop);
+        else if (lv == 0 || !red_up) k_ls_blockscan<false><<<g, kLsB * 32, smb, s>>>(L, p.stop);
+        else k_ls_prefix_red<<<dim3((unsigned)(L.n + (L.agg[0] ? g.x : 0)), 2), kLsB * 32, smb, s>>>(L, p.stop);
         ++nl;
     }
     // down: carries of every level from the top; level 0's are the chain carries (scan order)
