@@ -37,7 +37,10 @@ extern "C" {
 
 #define MMOT_VERSION_MAJOR 0
 #define MMOT_VERSION_MINOR 1
-#define MMOT_MAX_L 6          /* supported marginal counts: 2..MMOT_MAX_L */
+#define MMOT_MAX_L 8          /* supported marginal counts: 2..MMOT_MAX_L; l = 7, 8 (64 / 128 subset
+                               * states) run on the stabilised log-domain family only: MMOT_F64,
+                               * MMOT_KERNEL_AUTO or _STABLE, mmot_create / mmot_create_batched;
+                               * every other request returns MMOT_EUNSUPPORTED */
 
 #if defined(__GNUC__)
 #define MMOT_API __attribute__((visibility("default")))

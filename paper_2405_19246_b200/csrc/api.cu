@@ -33,11 +33,11 @@ struct DevScalars {
     int guard;          // single-walk precision guard tripped (k_sw_guard)
     int sweep;          // completed sweeps of the current solve (device counter)
     int g_done, g_n;    // device-resident loop: periods done / to do
-    int flags[2 * mmot::kMaxL];
+    int flags[2 * mmot::kStMaxL];
     double resid;
     double res_acc;
     double W;
-    double mass[mmot::kMaxL];
+    double mass[mmot::kStMaxL];
 };
 
 char g_err[256] = "";
@@ -205,8 +205,8 @@ struct mmot_ctx {
     double *bat_whost = nullptr;            // pinned [batch]
     int *bat_shost = nullptr;               // pinned [4*batch]: status, fail_iter, iters_done, converged
     double *bat_rhost = nullptr;            // pinned [batch]: last residual
-    double *stage_mu[mmot::kMaxL] = {nullptr};
-    double *stage_u[mmot::kMaxL] = {nullptr};
+    double *stage_mu[mmot::kStMaxL] = {nullptr};
+    double *stage_u[mmot::kStMaxL] = {nullptr};
     int *hstop = nullptr;       // pinned, async stop polling (hstop[1]: loop period count for the graph)
     cudaEvent_t poll_ev = nullptr;
     // device-resident Sinkhorn loop: cached graph (a WHILE node whose body is `period` sweeps)
@@ -350,6 +350,8 @@ void mmot_destroy(mmot_ctx *ctx) {
     for (int q = 0; q < mmot::kMaxL; ++q) {
         cudaFree(ctx->lin[q]);
         cudaFree(ctx->mu_t[q]);
+    }
+    for (int q = 0; q < mmot::kStMaxL; ++q) {
         cudaFree(ctx->stage_mu[q]);
         cudaFree(ctx->stage_u[q]);
     }
@@ -405,6 +407,15 @@ static mmot_status create_single(int l, int64_t N, double eta, mmot_grid grid, m
         return MMOT_EINVAL;
     }
     if (l > MMOT_MAX_L) { set_err(nullptr, "l=%d > MMOT_MAX_L=%d in this build", l, MMOT_MAX_L); return MMOT_EUNSUPPORTED; }
+    if (l > mmot::kMaxL) {
+        // l = 7, 8 (2^(l-1) = 64 / 128 subset states): the stabilised family only (stable.cu)
+        const int kreq = opts ? opts->kernel : MMOT_KERNEL_AUTO;
+        if (!allow_persistent || dt != MMOT_F64 || (kreq != MMOT_KERNEL_AUTO && kreq != MMOT_KERNEL_STABLE)) {
+            set_err(nullptr, "l=%d > %d runs on the stabilised family only (MMOT_F64, MMOT_KERNEL_AUTO or _STABLE, not sharded)", l, mmot::kMaxL);
+            return MMOT_EUNSUPPORTED;
+        }
+        return create_stable(l, N, 1, &eta, grid, dt, opts, cuda_stream, out);
+    }
     // small instances: the persistent batched kernel with one instance (all sweeps in one launch,
     // no per-update kernel latency)
     const int kern = opts ? opts->kernel : MMOT_KERNEL_AUTO;
@@ -739,7 +750,11 @@ mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *e
         set_err(nullptr, "bad opts");
         return MMOT_EINVAL;
     }
-    if (opts && opts->kernel == MMOT_KERNEL_STABLE) return create_stable(l, N, batch, eta_host, grid, dt, opts, cuda_stream, out);
+    if (l > mmot::kMaxL && (dt != MMOT_F64 || (opts && opts->kernel != MMOT_KERNEL_AUTO && opts->kernel != MMOT_KERNEL_STABLE))) {
+        set_err(nullptr, "l=%d > %d runs on the stabilised family only (MMOT_F64, MMOT_KERNEL_AUTO or _STABLE)", l, mmot::kMaxL);
+        return MMOT_EUNSUPPORTED;
+    }
+    if ((opts && opts->kernel == MMOT_KERNEL_STABLE) || l > mmot::kMaxL) return create_stable(l, N, batch, eta_host, grid, dt, opts, cuda_stream, out);
     if (l > 5) { set_err(nullptr, "batched contexts support l <= 5 in this build"); return MMOT_EUNSUPPORTED; }
     mmot_ctx *c = new mmot_ctx();
     c->l = l;
@@ -2185,7 +2200,7 @@ mmot_status mmot_sinkhorn(mmot_ctx *c, const void *const *marginals, int iters, 
     if (rep) { rep->iters_done = 0; rep->residual = NAN; rep->converged = 0; rep->status = 0; rep->fail_iter = -1; }
     if (!c || !marginals || !u) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
     if (iters < 0 || isnan(tol)) { set_err(c, "iters must be >= 0"); return MMOT_EINVAL; }
-    const double *mu[mmot::kMaxL];
+    const double *mu[mmot::kStMaxL];
     for (int q = 0; q < c->l; ++q) {
         if (!marginals[q] || !u[q]) { set_err(c, "marginals[%d] or u[%d] is NULL", q, q); return MMOT_EINVAL; }
         mu[q] = static_cast<const double *>(marginals[q]);
@@ -2225,8 +2240,8 @@ mmot_status mmot_sinkhorn_host(mmot_ctx *c, const void *const *marginals_host, i
         }
         CK(c, cudaMemcpyAsync(c->stage_u[q], u_host[q], bytes, cudaMemcpyHostToDevice, c->stream));
     }
-    const double *mu[mmot::kMaxL];
-    void *ud[mmot::kMaxL];
+    const double *mu[mmot::kStMaxL];
+    void *ud[mmot::kStMaxL];
     for (int q = 0; q < c->l; ++q) {
         mu[q] = c->stage_mu[q];
         ud[q] = c->stage_u[q];

@@ -225,14 +225,16 @@ struct VPtrs {
 };
 cudaError_t launch_vreduce(const VPtrs &src, int world, int n, int op, void *out, cudaStream_t s, int64_t *launches);
 
-// Stabilised family (stable.cu): log-domain subset recurrence, one warp per instance.
+// Stabilised family (stable.cu): log-domain subset recurrence, one warp per instance.  The only
+// family for l = 7, 8 (2^(l-1) = 64 / 128 subset states: 2 / 4 per lane).
+constexpr int kStMaxL = 8;
 struct SPlan {
     int l;
     int64_t N, batch;
     double h;                    // grid spacing
     const double *eta;           // device [batch]
-    double *g[kMaxL];            // device [batch][N] log scalings (in/out)
-    const double *mu[kMaxL];     // device [batch][N] marginals (linear)
+    double *g[kStMaxL];          // device [batch][N] log scalings (in/out)
+    const double *mu[kStMaxL];   // device [batch][N] marginals (linear)
     double *scratch;             // device [slots][scratch_per_warp]
     int64_t scratch_per_warp;    // 2 N 2^(l-1) doubles
     int64_t slots;               // resident warps (scratch slots)

@@ -13,7 +13,8 @@
 // tangent hatJ = sum E lambda^E prod phi is carried as the log of the E-weighted sums
 // (d/dlog lambda of w_a is e_a w_a).
 //
-// Layout / parallelism: one warp per instance, lane S = subset state S (2^(l-1) <= 32 lanes), the
+// Layout / parallelism: one warp per instance, lane S = subset state S (2^(l-1) <= 32 lanes; for
+// l = 7, 8 each lane holds 2 / 4 states, S = lane | r << 5), the
 // grid walked sequentially (prefix walk storing every prefix state, then the suffix walk with the
 // combine).  O(N) work like the plain families but O(N) latency per product and ~50 fp64
 // instructions per logaddexp: this is the robust family the plain ones fall back to when a product
@@ -51,62 +52,105 @@ __device__ __forceinline__ double warp_sum(double v) {
 //   MARG: out[x] = exp(g_k[x] + log J_k[x])
 //   RES : returns sum_x |exp(g_k + log J_k) - mu_k|
 //   COST: returns sum_x exp(g_k + log hatJ_k)  (times hc by the caller)
-template <bool TAN>
+// R states per lane: state S = lane | r << 5 (R = 1 for l <= 6; R = 2, 4 for l = 7, 8, where the
+// bound marginals j >= 5 pair registers of the same lane instead of lanes).
+template <int R, bool TAN>
 __device__ double st_product(const SPlan &sp, int64_t b, int k, int mode, bool &bad, int lane) {
     const int l = sp.l, NB = l - 1, M = 1 << NB;
+    const int NBL = NB < 5 ? NB : 5;  // bound marginals on lane bits
     const int64_t N = sp.N;
     const double eta = sp.eta[b];
-    double lw[kMaxL + 2], le[kMaxL + 2];
+    double lw[kStMaxL + 2], le[kStMaxL + 2];
 #pragma unroll
-    for (int a = 0; a <= kMaxL + 1; ++a) {
+    for (int a = 0; a <= kStMaxL + 1; ++a) {
         const double e = a <= l ? (double)(a * (l - a)) : 0.0;
         lw[a] = a <= l ? -e * sp.h / eta : -INFINITY;
         le[a] = e > 0 ? log(e) : -INFINITY;
     }
-    const double *gq[kMaxL];
+    const double *gq[kStMaxL];
     for (int j = 0; j < NB; ++j) gq[j] = sp.g[(k + 1 + j) % l] + b * N;
     double *gk = sp.g[k] + b * N;
     const double *muk = sp.mu[k] ? sp.mu[k] + b * N : nullptr;
     // this warp's slot of prefix-state storage ([2][N][M]: states, tangents)
     double *pre = sp.scratch + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * sp.scratch_per_warp;
-    const bool act = lane < M;
-    const int S = lane & (M - 1);
-    const int pcS = __popc(S);
+    const bool act = R > 1 || lane < M;
+    const int SL = R > 1 ? lane : lane & (M - 1);  // lane part of the state index
+    const int pcL = __popc(SL);
     // prefix walk: store F (and hatF) of every point
-    double F = S == 0 ? 0.0 : -INFINITY, Fh = -INFINITY;
+    double F[R], Fh[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        F[r] = (SL == 0 && r == 0) ? 0.0 : -INFINITY;
+        Fh[r] = -INFINITY;
+    }
     for (int64_t x = 0; x < N; ++x) {
-        const double a = lw[pcS];
-        if (TAN) Fh = lae(Fh + a, F + a + le[pcS]);
-        F += a;
-        for (int j = 0; j < NB; ++j) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int pc = pcL + __popc(r);
+            const double a = lw[pc];
+            if (TAN) Fh[r] = lae(Fh[r] + a, F[r] + a + le[pc]);
+            F[r] += a;
+        }
+        for (int j = 0; j < NBL; ++j) {
             const double gx = gq[j][x];  // plain load: g is rewritten inside the launch
-            const double o = __shfl_xor_sync(0xffffffffu, F, 1 << j);
-            const double oh = TAN ? __shfl_xor_sync(0xffffffffu, Fh, 1 << j) : 0.0;
-            if ((S >> j) & 1) {
-                F = lae(F, gx + o);
-                if (TAN) Fh = lae(Fh, gx + oh);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double o = __shfl_xor_sync(0xffffffffu, F[r], 1 << j);
+                const double oh = TAN ? __shfl_xor_sync(0xffffffffu, Fh[r], 1 << j) : 0.0;
+                if ((SL >> j) & 1) {
+                    F[r] = lae(F[r], gx + o);
+                    if (TAN) Fh[r] = lae(Fh[r], gx + oh);
+                }
+            }
+        }
+        if (R > 1) {
+#pragma unroll
+            for (int jb = 0; jb < 2; ++jb) {
+                if ((1 << jb) < R) {
+                    const double gx = gq[5 + jb][x];
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if ((r >> jb) & 1) {
+                            F[r] = lae(F[r], gx + F[r ^ (1 << jb)]);
+                            if (TAN) Fh[r] = lae(Fh[r], gx + Fh[r ^ (1 << jb)]);
+                        }
+                }
             }
         }
         if (act) {
-            pre[x * M + S] = F;
-            if (TAN) pre[(N + x) * M + S] = Fh;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                pre[x * M + SL + 32 * r] = F[r];
+                if (TAN) pre[(N + x) * M + SL + 32 * r] = Fh[r];
+            }
         }
     }
     __syncwarp();
     // suffix walk with the combine at every point
-    double B = S == 0 ? 0.0 : -INFINITY, Bh = -INFINITY;
+    double B[R], Bh[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        B[r] = (SL == 0 && r == 0) ? 0.0 : -INFINITY;
+        Bh[r] = -INFINITY;
+    }
     double acc = 0.0;
-    const int full = M - 1;
+    const int cl = (R > 1 ? 31 : M - 1) & ~SL;  // lane holding the complement's lane part
     for (int64_t x = N - 1; x >= 0; --x) {
         // B holds B_{x+1}; combine J_x = sum_S F_x[S] w_{|S|+1} B_{x+1}[S^c]
-        const double Bc = __shfl_sync(0xffffffffu, B, full & ~S);
-        const double Fx = act ? pre[x * M + S] : -INFINITY;
-        double term = act ? Fx + lw[pcS + 1] + Bc : -INFINITY;
-        if (TAN) {
-            const double Bhc = __shfl_sync(0xffffffffu, Bh, full & ~S);
-            const double Fhx = act ? pre[(N + x) * M + S] : -INFINITY;
-            term = act ? lae(lae(Fhx + lw[pcS + 1] + Bc, Fx + lw[pcS + 1] + le[pcS + 1] + Bc), Fx + lw[pcS + 1] + Bhc)
-                       : -INFINITY;
+        double term = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int pc = pcL + __popc(r);
+            const double Bc = __shfl_sync(0xffffffffu, B[R - 1 - r], cl);
+            const double Fx = act ? pre[x * M + SL + 32 * r] : -INFINITY;
+            double t = act ? Fx + lw[pc + 1] + Bc : -INFINITY;
+            if (TAN) {
+                const double Bhc = __shfl_sync(0xffffffffu, Bh[R - 1 - r], cl);
+                const double Fhx = act ? pre[(N + x) * M + SL + 32 * r] : -INFINITY;
+                t = act ? lae(lae(Fhx + lw[pc + 1] + Bc, Fx + lw[pc + 1] + le[pc + 1] + Bc), Fx + lw[pc + 1] + Bhc)
+                        : -INFINITY;
+            }
+            term = R > 1 ? lae(term, t) : t;
         }
         const double lj = warp_lse(term);
         if (lane == 0) {
@@ -124,16 +168,37 @@ __device__ double st_product(const SPlan &sp, int64_t b, int k, int mode, bool &
             }
         }
         // B_x = place_x(diag B_{x+1})
-        const double a = lw[pcS];
-        if (TAN) Bh = lae(Bh + a, B + a + le[pcS]);
-        B += a;
-        for (int j = 0; j < NB; ++j) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int pc = pcL + __popc(r);
+            const double a = lw[pc];
+            if (TAN) Bh[r] = lae(Bh[r] + a, B[r] + a + le[pc]);
+            B[r] += a;
+        }
+        for (int j = 0; j < NBL; ++j) {
             const double gx = gq[j][x];  // plain load: g is rewritten inside the launch
-            const double o = __shfl_xor_sync(0xffffffffu, B, 1 << j);
-            const double oh = TAN ? __shfl_xor_sync(0xffffffffu, Bh, 1 << j) : 0.0;
-            if ((S >> j) & 1) {
-                B = lae(B, gx + o);
-                if (TAN) Bh = lae(Bh, gx + oh);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double o = __shfl_xor_sync(0xffffffffu, B[r], 1 << j);
+                const double oh = TAN ? __shfl_xor_sync(0xffffffffu, Bh[r], 1 << j) : 0.0;
+                if ((SL >> j) & 1) {
+                    B[r] = lae(B[r], gx + o);
+                    if (TAN) Bh[r] = lae(Bh[r], gx + oh);
+                }
+            }
+        }
+        if (R > 1) {
+#pragma unroll
+            for (int jb = 0; jb < 2; ++jb) {
+                if ((1 << jb) < R) {
+                    const double gx = gq[5 + jb][x];
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if ((r >> jb) & 1) {
+                            B[r] = lae(B[r], gx + B[r ^ (1 << jb)]);
+                            if (TAN) Bh[r] = lae(Bh[r], gx + Bh[r ^ (1 << jb)]);
+                        }
+                }
             }
         }
     }
@@ -142,6 +207,7 @@ __device__ double st_product(const SPlan &sp, int64_t b, int k, int mode, bool &
 }
 
 // what: 0 Sinkhorn, 1 marginal k -> out, 2 cost -> wout.  One warp per instance (grid-stride).
+template <int R>
 __global__ void __launch_bounds__(128) k_stable(SPlan sp, int what) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -150,11 +216,11 @@ __global__ void __launch_bounds__(128) k_stable(SPlan sp, int what) {
         if (sp.status[b] || (sp.sel && !sp.sel[b])) continue;
         bool bad = false;
         if (what == 1) {
-            st_product<false>(sp, b, sp.k, MODE_MARG, bad, lane);
+            st_product<R, false>(sp, b, sp.k, MODE_MARG, bad, lane);
             continue;
         }
         if (what == 2) {
-            const double acc = st_product<true>(sp, b, sp.l - 1, MODE_COST, bad, lane);
+            const double acc = st_product<R, true>(sp, b, sp.l - 1, MODE_COST, bad, lane);
             if (lane == 0) sp.wout[b] = sp.hc * acc;
             continue;
         }
@@ -163,12 +229,12 @@ __global__ void __launch_bounds__(128) k_stable(SPlan sp, int what) {
         bool conv = false;
         while (t < sp.iters) {
             ++t;
-            for (int k = 0; k < sp.l && !bad; ++k) st_product<false>(sp, b, k, MODE_UPD, bad, lane);
+            for (int k = 0; k < sp.l && !bad; ++k) st_product<R, false>(sp, b, k, MODE_UPD, bad, lane);
             bad = __any_sync(0xffffffffu, bad);
             if (bad) break;
             if (sp.tol > 0 && (t % sp.check_every == 0 || t == sp.iters)) {
                 double r = 0.0;
-                for (int k = 0; k + 1 < sp.l; ++k) r += st_product<false>(sp, b, k, MODE_RES, bad, lane);
+                for (int k = 0; k + 1 < sp.l; ++k) r += st_product<R, false>(sp, b, k, MODE_RES, bad, lane);
                 res = r;
                 if (r <= sp.tol) {
                     conv = true;
@@ -218,7 +284,9 @@ cudaError_t launch_st_convert(const double *in, double *out, int64_t batch, int6
 cudaError_t launch_stable(const SPlan &sp, int what, cudaStream_t s, int64_t *launches) {
     const int64_t warps = std::min<int64_t>(sp.batch, sp.slots);
     const unsigned blocks = (unsigned)((warps + 3) / 4);
-    k_stable<<<blocks, 128, 0, s>>>(sp, what);
+    if (sp.l <= 6) k_stable<1><<<blocks, 128, 0, s>>>(sp, what);
+    else if (sp.l == 7) k_stable<2><<<blocks, 128, 0, s>>>(sp, what);
+    else k_stable<4><<<blocks, 128, 0, s>>>(sp, what);
     ++*launches;
     return cudaGetLastError();
 }

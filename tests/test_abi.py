@@ -53,7 +53,8 @@ def test_argument_errors_before_any_launch(lib):
     assert lib.mmot_create(3, 10, -1.0, g, 0, None, None, ctypes.byref(ctx)) == 1      # eta <= 0
     assert lib.mmot_create(3, 10, float("nan"), g, 0, None, None, ctypes.byref(ctx)) == 1
     assert lib.mmot_create(3, 10, 0.1, mm._Grid(1.0, 0.0), 0, None, None, ctypes.byref(ctx)) == 1
-    assert lib.mmot_create(7, 10, 0.1, g, 0, None, None, ctypes.byref(ctx)) == 10      # l > MMOT_MAX_L
+    assert lib.mmot_create(9, 10, 0.1, g, 0, None, None, ctypes.byref(ctx)) == 1       # l > MMOT_MAX_L = 8
+    assert lib.mmot_create(7, 10, 0.1, g, 1, None, None, ctypes.byref(ctx)) == 10      # l = 7, 8: MMOT_F64 only
     assert ctx.value is None
     assert lib.mmot_marginal(None, 0, None, None) == 1
     assert lib.mmot_sinkhorn(None, None, 1, 0.0, None, None) == 1

@@ -140,3 +140,79 @@ def test_stable_batched_explicit():
     for b in range(B):
         g_ref, _, _ = osk.sinkhorn(mus[b], h, etas[b], T, domain="log", engine="subset")
         assert _gclose(g[:, b, :], g_ref), b
+
+
+# ---- l = 7, 8 (include/mmot.h MMOT_MAX_L = 8; SURVEY §8(b) l in [2, 8]): 64 / 128 subset states, 2 / 4
+# per lane of the instance's warp, bound marginals 5, 6 pairing registers instead of lanes.  The
+# oracle is O4 (oracle/subset.c, pinned against the dense definition at l = 7, 8 in
+# tests/test_oracle_subset.py); the region-chain oracle would need l! = 5040 / 40320 chains.
+
+def _subset_cost(phis, h, eta):
+    l = len(phis)
+    w = regions.edge_weights(l, h, eta)
+    _, jh = subset.marginal_product(list(phis), l - 1, w, want_hat=True)
+    return float(h * np.dot(phis[l - 1], jh))
+
+
+@pytest.mark.parametrize("l", [7, 8])
+@pytest.mark.parametrize("N", [1, 7, 130])
+def test_l78_marginal_and_cost_parity(l, N):
+    h = mmot_inputs.grid_h(N)
+    eta = 0.05
+    phis = mmot_inputs.random_positive(4100 + 10 * l + N, l, N)
+    ctx = mm.Context(l, N, eta, repr="linear")  # AUTO: l > 6 takes the stabilised family
+    assert ctx.info["kernel"] == "stable"
+    u = _dev(phis)
+    w = regions.edge_weights(l, h, eta)
+    for k in range(l):
+        got = ctx.marginal(k, u).cpu().numpy()
+        want = phis[k] * subset.marginal_product(list(phis), k, w)
+        assert np.max(np.abs(got - want) / want) <= RTOL, (l, N, k)
+    W = ctx.cost(u)
+    ctx.close()
+    W_ref = _subset_cost(phis, h, eta)
+    assert abs(W - W_ref) <= RTOL * abs(W_ref) + 1e-300, (W, W_ref)
+
+
+@pytest.mark.parametrize("l,N,eta,T", [(7, 96, 0.02, 4), (8, 64, 0.05, 3), (7, 200, 1e-3, 3)])
+def test_l78_sinkhorn_lockstep(l, N, eta, T):
+    h = mmot_inputs.grid_h(N)
+    mus = np.stack(mmot_inputs.c2_marginals(2, N, l))
+    ctx = mm.Context(l, N, eta, repr="log", kernel="stable", check_every=1)
+    u = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in range(l)]
+    ctx.init_uniform(u)
+    rep = ctx.sinkhorn(_dev(mus), T, 1e-300, u)
+    assert rep["status"] == 0 and rep["iters_done"] == T
+    g = np.stack([x.cpu().numpy() for x in u])
+    # after the last update of a sweep the l-th marginal of the plan is mu_l
+    m_last = ctx.marginal(l - 1, u).cpu().numpy()
+    ctx.close()
+    g_ref, _, res_ref = osk.sinkhorn(mus, h, eta, T, tol=1e-300, domain="log", engine="subset")
+    assert _gclose(g, g_ref)
+    assert rep["residual"] == pytest.approx(res_ref, rel=1e-8)
+    assert np.abs(m_last - mus[l - 1]).sum() <= 1e-12
+
+
+def test_l78_batched_and_host_buffers():
+    l, N, B, T = 7, 60, 3, 3
+    h = mmot_inputs.grid_h(N)
+    etas = [0.01, 0.05, 0.2]
+    mus = [np.stack(mmot_inputs.c2_marginals(b + 11, N, l)) for b in range(B)]
+    ctx = mm.Context(l, N, etas, batch=B, repr="log")
+    assert ctx.info["kernel"] == "stable"
+    mh = [torch.from_numpy(np.stack([mus[b][q] for b in range(B)])).pin_memory() for q in range(l)]
+    uh = [torch.full((B, N), -np.log(N), dtype=torch.float64).pin_memory() for _ in range(l)]
+    rep = ctx.sinkhorn_host(mh, T, 0.0, uh)
+    assert rep["status"] == 0
+    g = np.stack([x.numpy() for x in uh])
+    ctx.close()
+    for b in range(B):
+        g_ref, _, _ = osk.sinkhorn(mus[b], h, etas[b], T, domain="log", engine="subset")
+        assert _gclose(g[:, b, :], g_ref), b
+
+
+def test_l78_unsupported_requests():
+    with pytest.raises(mm.MMOTError):
+        mm.Context(7, 50, 0.05, kernel="two_walk")
+    with pytest.raises(mm.MMOTError):
+        mm.Context(8, 50, 0.05, dtype="f32")

@@ -13,7 +13,7 @@ def _phis(seed, l, N, lo=0.1, hi=1.0):
     return np.random.default_rng(seed).uniform(lo, hi, (l, N))
 
 
-@pytest.mark.parametrize("l,N", [(2, 7), (3, 6), (4, 5), (5, 4), (6, 3)])
+@pytest.mark.parametrize("l,N", [(2, 7), (3, 6), (4, 5), (5, 4), (6, 3), (7, 4), (8, 3)])
 @pytest.mark.parametrize("lam", [0.3, 0.8])
 def test_subset_equals_dense_definition(l, N, lam):
     phis = _phis(10 * l + N, l, N)
@@ -39,10 +39,10 @@ def test_subset_equals_region_chains(l):
         np.testing.assert_allclose(gh, wh, rtol=1e-12)
 
 
-@pytest.mark.parametrize("l", [3, 4])
+@pytest.mark.parametrize("l", [3, 4, 7, 8])
 def test_subset_tangent_equals_cost_weighted_dense(l):
     """Jhat_k = sum_i E(i) lambda^E(i) prod phi: the dense (E . K) contraction."""
-    N = 5
+    N = 5 if l <= 4 else 3
     phis = _phis(5 + l, l, N)
     h, eta = 1.0 / (N - 1), 0.3
     w = regions.edge_weights(l, h, eta)
@@ -68,7 +68,7 @@ def test_subset_closed_forms():
     assert one[0] == 10.0
 
 
-@pytest.mark.parametrize("l", [3, 5])
+@pytest.mark.parametrize("l", [3, 5, 7, 8])
 def test_subset_log_equals_plain_and_handles_zeros(l):
     N = 120
     phis = _phis(9 + l, l, N)
