@@ -260,6 +260,12 @@ MMOT_API mmot_status mmot_sinkhorn_host(mmot_ctx *ctx, const void *const *margin
  * as the tangent of the same scans.  W: host pointer.  Synchronises. */
 MMOT_API mmot_status mmot_cost(mmot_ctx *ctx, const void *const *u, double *W);
 
+/* mmot_cost of the scalings the last mmot_sinkhorn_host left in the context's device staging
+ * buffers (the host-buffer counterpart of mmot_cost: no further host<->device copy of u).
+ * MMOT_EINVAL before the first mmot_sinkhorn_host of the context.  W: host pointer ([batch] for
+ * batched contexts).  Synchronises. */
+MMOT_API mmot_status mmot_cost_staged(mmot_ctx *ctx, double *W);
+
 /* u_q <- the paper's initial scalings phi_q = 1/N: log phi = -log N (MMOT_LOG)
  * or 1/N (MMOT_LINEAR).  u: host array of l device pointers.  Asynchronous. */
 MMOT_API mmot_status mmot_init_uniform(mmot_ctx *ctx, void *const *u);

@@ -114,6 +114,8 @@ def load_library():
     lib.mmot_sinkhorn_host.restype = ctypes.c_int
     lib.mmot_cost.argtypes = [vp, vpp, ctypes.POINTER(ctypes.c_double)]
     lib.mmot_cost.restype = ctypes.c_int
+    lib.mmot_cost_staged.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
+    lib.mmot_cost_staged.restype = ctypes.c_int
     lib.mmot_init_uniform.argtypes = [vp, vpp]
     lib.mmot_init_uniform.restype = ctypes.c_int
     lib.mmot_destroy.argtypes = [vp]
@@ -458,6 +460,12 @@ class Context:
         W = ctypes.c_double()
         self._check(self._lib.mmot_cost(self._ctx, self._ptrs(u), ctypes.byref(W)))
         return W.value
+
+    def cost_staged(self):
+        """W of the scalings the last sinkhorn_host left on the device (mmot_cost_staged)."""
+        Wb = (ctypes.c_double * (self.batch or 1))()
+        self._check(self._lib.mmot_cost_staged(self._ctx, Wb))
+        return list(Wb) if self.batch is not None else Wb[0]
 
     def profile(self, enable: bool = True) -> None:
         self._check(self._lib.mmot_profile_enable(self._ctx, 1 if enable else 0))

@@ -2337,6 +2337,16 @@ mmot_status mmot_profile_read(mmot_ctx *c, double *ms, double *ms_mode, int64_t 
     return MMOT_OK;
 }
 
+mmot_status mmot_cost_staged(mmot_ctx *c, double *W) {
+    if (!c || !W) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
+    const void *u[mmot::kStMaxL];
+    for (int q = 0; q < c->l; ++q) {
+        if (!c->stage_u[q]) { set_err(c, "mmot_cost_staged before mmot_sinkhorn_host"); return MMOT_EINVAL; }
+        u[q] = c->stage_u[q];
+    }
+    return mmot_cost(c, u, W);
+}
+
 mmot_status mmot_init_uniform(mmot_ctx *c, void *const *u) {
     if (!c || !u) { set_err(c, "NULL argument"); return MMOT_EINVAL; }
     cudaSetDevice(c->device);

@@ -136,10 +136,15 @@ def test_linear_repr_and_host_entry_agree():
     rep_b, g_b, _, _ = _run_gpu(mus, 0.02, 15, repr_="linear")
     np.testing.assert_allclose(g_b, g_a, atol=1e-11)
     ctx = mm.Context(l, N, 0.02)
+    with pytest.raises(mm.MMOTError):
+        ctx.cost_staged()  # nothing staged yet
     u = [np.full(N, -math.log(N)) for _ in range(l)]
     rep = ctx.sinkhorn_host([np.ascontiguousarray(m) for m in mus], 15, 0.0, u)
+    W = ctx.cost_staged()  # mmot_cost of the scalings the host call left on the device
     ctx.close()
     np.testing.assert_allclose(np.stack(u), g_a, atol=1e-11)
+    W_ref = osk.cost(np.exp(np.stack(u)), mmot_inputs.grid_h(N), 0.02)
+    assert abs(W - W_ref) <= 1e-10 * abs(W_ref)
 
 
 def test_residual_cadence():
