@@ -128,7 +128,8 @@ MMOT_API mmot_status mmot_create(int l, int64_t N, double eta, mmot_grid grid, m
 
 /* Create a context for `batch` independent instances of (l, N) on the same grid, instance b
  * with its own eta_host[b] (BASELINE C5: 8192 x (l=5, N=4096), eta ~ logU[1e-3, 1e-1]).
- *   l in [2, 5] in this build (EUNSUPPORTED above), N >= 1, batch >= 1, every eta finite > 0;
+ *   l in [2, MMOT_MAX_L]: the persistent / pair / CTA families for l <= 5; l = 6..8 on the stabilised
+ *   family (MMOT_F64, MMOT_KERNEL_AUTO or _STABLE; EUNSUPPORTED otherwise); N >= 1, batch >= 1, every eta finite > 0;
  *   dt: MMOT_F64 or MMOT_F32 (fp32 I/O, as for mmot_create).  eta_host is copied.
  * Layouts for the compute calls on a batched context: every array argument is a plane of
  * `batch` consecutive N-vectors ([batch][N], instance-major); mmot_cost fills W[batch] (host);

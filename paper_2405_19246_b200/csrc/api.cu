@@ -755,7 +755,13 @@ mmot_status mmot_create_batched(int l, int64_t N, int64_t batch, const double *e
         return MMOT_EUNSUPPORTED;
     }
     if ((opts && opts->kernel == MMOT_KERNEL_STABLE) || l > mmot::kMaxL) return create_stable(l, N, batch, eta_host, grid, dt, opts, cuda_stream, out);
-    if (l > 5) { set_err(nullptr, "batched contexts support l <= 5 in this build"); return MMOT_EUNSUPPORTED; }
+    if (l > 5) {
+        // l = 6 batches: the stabilised family (warp per instance, lane = subset state) under AUTO
+        if (dt == MMOT_F64 && (!opts || opts->kernel == MMOT_KERNEL_AUTO))
+            return create_stable(l, N, batch, eta_host, grid, dt, opts, cuda_stream, out);
+        set_err(nullptr, "batched contexts with l > 5 run on the stabilised family only (MMOT_F64, MMOT_KERNEL_AUTO or _STABLE)");
+        return MMOT_EUNSUPPORTED;
+    }
     mmot_ctx *c = new mmot_ctx();
     c->l = l;
     c->N = N;

@@ -68,7 +68,7 @@ def test_batched_and_sharded_argument_errors(lib):
     assert lib.mmot_create_batched(4, 100, 2, etas, g, 0, None, None, ctypes.byref(ctx)) == 1   # eta <= 0
     etas_ok = (ctypes.c_double * 2)(0.1, 0.2)
     assert lib.mmot_create_batched(4, 0, 2, etas_ok, g, 0, None, None, ctypes.byref(ctx)) == 1  # N < 1
-    assert lib.mmot_create_batched(6, 100, 2, etas_ok, g, 0, None, None, ctypes.byref(ctx)) == 10  # l > 5
+    assert lib.mmot_create_batched(6, 100, 2, etas_ok, g, 1, None, None, ctypes.byref(ctx)) == 10  # l > 5: MMOT_F64 only
     uid = ctypes.create_string_buffer(128)
     assert lib.mmot_create_sharded(4, 100, 0.1, g, 0, uid, 2, 2, None, None, ctypes.byref(ctx)) == 1  # rank >= world
     assert lib.mmot_create_sharded(4, 100, 0.1, g, 0, None, 0, 1, None, None, ctypes.byref(ctx)) == 1  # no id

@@ -149,8 +149,11 @@ def test_batched_argument_errors():
         mm.Context(4, 100, [0.1, -1.0], batch=2)
     assert e.value.name == "MMOT_EINVAL"
     with pytest.raises(mm.MMOTError) as e:
-        mm.Context(6, 100, [0.1], batch=1)
+        mm.Context(6, 100, [0.1], batch=1, kernel="persistent")  # l = 6 batches: stabilised family only
     assert e.value.name == "MMOT_EUNSUPPORTED"
+    ctx = mm.Context(6, 100, [0.1], batch=1)
+    assert ctx.info["kernel"] == "stable"
+    ctx.close()
 
 
 
