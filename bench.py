@@ -215,7 +215,7 @@ def run_reference(args, cfg):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    _emit(line)
 
 
 # ------------------------------------------------------------------------------------------
@@ -356,7 +356,7 @@ def run_batched(args, cfg):
             "gpu_launches": int(launches), "iters_per_s": cfg.batch * T / (ms / 1e3),
             "W_first": state["W"][0], "impl": "mmot",
         }
-        print(json.dumps(line), flush=True)
+        _emit(line)
     ctx.close()
     if ws > 1:
         dist.destroy_process_group()
@@ -535,14 +535,34 @@ def run_mmot(args, cfg):
             "W": state["W"],
             "impl": "mmot",
         }
-        print(json.dumps(line), flush=True)
+        _emit(line)
     ctx.close()
     if ws > 1:
         dist.destroy_process_group()
 
 
+_JSON_OUT = None
+
+
+def _guard_stdout():
+    """The contract is ONE JSON line on stdout: native libraries (NCCL's version banner under
+    NCCL_DEBUG) write to fd 1 too, so fd 1 is pointed at stderr and the line goes to a duplicate of
+    the original stdout."""
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+def _emit(line):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
     args = _args()
+    _guard_stdout()
     cfg = mmot_inputs.CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

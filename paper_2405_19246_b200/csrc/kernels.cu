@@ -1590,6 +1590,103 @@ __global__ void __launch_bounds__(128) k_rx_down_w(const double *el_f, const dou
     }
 }
 
+// The top of the restricted scan in ONE launch (single-process contexts with >= 3 levels): the
+// reduce of level top-1 (<= 1024 elements) into the <= 32 top elements, the down-sweep of the top
+// level (zero new part entering it) and the down-sweep of level top-1, the top level's elements and
+// carries staying in shared memory.  One CTA per direction; replaces three dependent launches of
+// ~5 us each per update (C4: 74 -> 3 elements).  Same arithmetic, same order as k_rx_reduce_w /
+// k_rx_down_w (bit-identical carries).
+template <int NB>
+__global__ void __launch_bounds__(128) k_rx_top(const double *e1_f, const double *e1_b, double *car1_f, double *car1_b,
+                                               int64_t n1, const int *stop) {
+    constexpr int SZE = Rx<NB>::SZE;
+    constexpr int MO = Rx<NB>::MO;
+    __shared__ double s_el[32][SZE];
+    __shared__ double s_car[32][MO];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int dir = blockIdx.x;
+    if (*stop) return;
+    const int ng = (int)((n1 + 31) / 32);  // groups of level top-1 = elements of the top level (<= 32)
+    const double *e1 = dir == 0 ? e1_f : e1_b;
+    double A[SZE], Bv[SZE], C[SZE];
+    for (int g = warp; g < ng; g += 4) {  // reduce: one top element per group
+        rx_load<NB>(A, e1, (int64_t)g * 32 + lane, n1);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            rx_shfl<NB>(Bv, A, d, 2);
+            if (dir == 0) rx_compose<NB>(A, Bv, C);
+            else rx_compose<NB>(Bv, A, C);
+            if ((lane & (2 * d - 1)) == 0) {
+#pragma unroll
+                for (int q = 0; q < SZE; ++q) A[q] = C[q];
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int q = 0; q < SZE; ++q) s_el[g][q] = A[q];
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {  // down-sweep of the top level: carries entering each group
+        if (lane < ng) {
+#pragma unroll
+            for (int q = 0; q < SZE; ++q) A[q] = s_el[lane][q];
+        } else {
+            rx_identity<NB>(A);
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            rx_shfl<NB>(Bv, A, d, dir == 0 ? 1 : 2);
+            rx_compose<NB>(Bv, A, C);
+            const bool take = dir == 0 ? lane >= d : lane + d < 32;
+            if (take) {
+#pragma unroll
+                for (int q = 0; q < SZE; ++q) A[q] = C[q];
+            }
+        }
+        double cin[MO], out[MO], nb[MO];
+#pragma unroll
+        for (int U = 0; U < MO; ++U) cin[U] = 0.0;
+        rx_apply<NB>(A, cin, out);
+#pragma unroll
+        for (int U = 0; U < MO; ++U)
+            nb[U] = dir == 0 ? __shfl_up_sync(0xffffffffu, out[U], 1) : __shfl_down_sync(0xffffffffu, out[U], 1);
+        const bool edge = dir == 0 ? lane == 0 : lane == 31;
+        if (lane < ng) {
+#pragma unroll
+            for (int U = 0; U < MO; ++U) s_car[lane][U] = edge ? cin[U] : nb[U];
+        }
+    }
+    __syncthreads();
+    for (int g = warp; g < ng; g += 4) {  // down-sweep of level top-1
+        const int64_t i = (int64_t)g * 32 + lane;
+        rx_load<NB>(A, e1, i, n1);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            rx_shfl<NB>(Bv, A, d, dir == 0 ? 1 : 2);
+            rx_compose<NB>(Bv, A, C);
+            const bool take = dir == 0 ? lane >= d : lane + d < 32;
+            if (take) {
+#pragma unroll
+                for (int q = 0; q < SZE; ++q) A[q] = C[q];
+            }
+        }
+        double cin[MO], out[MO], nb[MO];
+#pragma unroll
+        for (int U = 0; U < MO; ++U) cin[U] = s_car[g][U];
+        rx_apply<NB>(A, cin, out);
+#pragma unroll
+        for (int U = 0; U < MO; ++U)
+            nb[U] = dir == 0 ? __shfl_up_sync(0xffffffffu, out[U], 1) : __shfl_down_sync(0xffffffffu, out[U], 1);
+        const bool edge = dir == 0 ? lane == 0 : lane == 31;
+        if (i < n1) {
+            double *dst = (dir == 0 ? car1_f : car1_b) + i * MO;
+#pragma unroll
+            for (int U = 0; U < MO; ++U) dst[U] = edge ? cin[U] : nb[U];
+        }
+    }
+}
+
 // Levels >= 1 (level 0 is fused into the update kernels: reduce at the end of update k, down at
 // the start of update k+1).
 template <int NB>
@@ -1599,7 +1696,10 @@ __global__ void k_rx_compose(const double *all, int world, int rank, double *car
 
 template <int NB>
 static void launch_rx_scan(const Plan &p, cudaStream_t s, int64_t *launches) {
-    for (int i = 1; i + 1 < p.nlev; ++i) {
+    static const bool no_top = getenv("MMOT_NO_RXTOP") != nullptr;
+    const bool fuse_top = !p.exch && p.nlev >= 3 && !no_top;  // top two levels in one launch (k_rx_top)
+    const int nred = fuse_top ? p.nlev - 2 : p.nlev - 1;
+    for (int i = 1; i < nred; ++i) {
         const int64_t ng = p.nlev_n[i + 1];
         k_rx_reduce_w<NB><<<dim3((unsigned)((ng + 3) / 4), 2), 128, 0, s>>>(
             static_cast<const double *>(p.rxe_f[i]), static_cast<const double *>(p.rxe_b[i]),
@@ -1619,7 +1719,14 @@ static void launch_rx_scan(const Plan &p, cudaStream_t s, int64_t *launches) {
                                         static_cast<double *>(p.rank_car));
         ++*launches;
     }
-    for (int i = p.nlev - 1; i >= 1; --i) {
+    if (fuse_top) {
+        const int t1 = p.nlev - 2;
+        k_rx_top<NB><<<2, 128, 0, s>>>(static_cast<const double *>(p.rxe_f[t1]), static_cast<const double *>(p.rxe_b[t1]),
+                                       static_cast<double *>(p.rcar_f[t1]), static_cast<double *>(p.rcar_b[t1]),
+                                       p.nlev_n[t1], p.stop);
+        ++*launches;
+    }
+    for (int i = fuse_top ? p.nlev - 3 : p.nlev - 1; i >= 1; --i) {
         const int64_t ng = (p.nlev_n[i] + 31) / 32;
         const double *gf = i + 1 < p.nlev ? static_cast<const double *>(p.rcar_f[i + 1])
                                           : (p.exch ? static_cast<const double *>(p.rank_car) : nullptr);
