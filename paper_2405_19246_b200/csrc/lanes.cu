@@ -263,6 +263,7 @@ struct LsLevel {
     double *agg[2];
     int64_t n;
     int rev1;  // direction 1 reads `in` reversed (level 0: chain order)
+    double *car[2];  // top level only (k_ls_prefix_red): carries = excl applied to e_empty; else null
 };
 
 // Kogge-Stone over the kLsB items of a block (log2 kLsB = 4 dependent compositions instead of the
@@ -424,6 +425,9 @@ __global__ void __launch_bounds__(kLsB * 32, 2) k_ls_prefix_red(LsLevel L, const
     if (wi == 0) {
         if (j < L.n) ls_store_op((dir ? L.excl[1] : L.excl[0]) + j * kLsSZ, 0, lane);
         else ls_store_op((dir ? L.agg[1] : L.agg[0]) + (j - L.n) * kLsSZ, 0, lane);
+        // top level: the state entering item j is its exclusive prefix applied to e_empty, i.e. the
+        // operator's slice c = 0 (the top level's k_ls_down, fused)
+        if (j < L.n && L.car[0]) (dir ? L.car[1] : L.car[0])[j * kLsM + lane] = ls_sm[lane];
     }
 }
 
@@ -446,7 +450,7 @@ __global__ void __launch_bounds__(128) k_ls_down(const double *excl0, const doub
 // Apply: warp per chain.  MODE_UPD: phi_k <- mu_k / J_k; MODE_MARG: out = phi_k J_k; MODE_RES:
 // partial[c] = sum |phi_k J_k - mu_k|.  Points beyond N (the last chain's padding) hold phi = 0.
 template <int MODE>
-__global__ void __launch_bounds__(128) k_ls_apply(Plan p, LsWork w) {
+__global__ void __launch_bounds__(128) k_ls_apply(Plan p, LsWork w, int fuse1) {
     constexpr int NB = kLsNB, M = kLsM;
     constexpr int Q = 8;              // checkpoint block
     constexpr int NQ = kLsP / Q;
@@ -464,8 +468,17 @@ __global__ void __launch_bounds__(128) k_ls_apply(Plan p, LsWork w) {
     // (level 0 of the down pass, fused here: the chain's exclusive in-block prefix applied to the
     // state entering its block; e_empty when the scan has a single level)
     const int64_t rb = w.C - 1 - c;
-    const double pf0 = w.nlev > 1 ? w.lv_car[1][0][(c / kLsB) * M + lane] : (lane == 0 ? 1.0 : 0.0);
-    const double pb0 = w.nlev > 1 ? w.lv_car[1][1][(rb / kLsB) * M + lane] : (lane == 0 ? 1.0 : 0.0);
+    double pf0, pb0;
+    if (fuse1) {
+        // level 1 of the down pass fused here too (scans of >= 3 levels): the block's exclusive
+        // prefix at level 1 applied to the state entering its level-2 parent
+        const int64_t i1f = c / kLsB, i1b = rb / kLsB;
+        pf0 = ls_apply(w.lv_excl[1][0] + i1f * kLsSZ, w.lv_car[2][0][(i1f / kLsB) * M + lane], lane);
+        pb0 = ls_apply(w.lv_excl[1][1] + i1b * kLsSZ, w.lv_car[2][1][(i1b / kLsB) * M + lane], lane);
+    } else {
+        pf0 = w.nlev > 1 ? w.lv_car[1][0][(c / kLsB) * M + lane] : (lane == 0 ? 1.0 : 0.0);
+        pb0 = w.nlev > 1 ? w.lv_car[1][1][(rb / kLsB) * M + lane] : (lane == 0 ? 1.0 : 0.0);
+    }
     double F = ls_apply(w.lv_excl[0][0] + c * kLsSZ, pf0, lane);
     double B = ls_apply(w.lv_excl[0][1] + rb * kLsSZ, pb0, lane);
     // the chain's bound values (lane j: point x0 + j), padded with zeros beyond N, staged in shared
@@ -584,6 +597,11 @@ cudaError_t launch_ls_product(const Plan &p, const LsWork &w, int mode, cudaStre
     smem_attr((const void *)k_ls_prefix_red, smb);
     static const int tree0 = getenv("MMOT_LS_KS0") ? 0 : 1;  // level 0: tree (default) or Kogge-Stone
     static const int red_up = getenv("MMOT_LS_KS_UP") ? 0 : 1;  // upper levels: per-output trees
+    // down pass: the top level inside its k_ls_prefix_red, level 1 inside k_ls_apply (no k_ls_down
+    // launches for scans of <= 3 levels)
+    static const int fuse_down = getenv("MMOT_LS_NO_FUSE_DOWN") ? 0 : 1;
+    const bool top_fused = fuse_down && red_up && w.nlev >= 2;
+    const int fuse1 = fuse_down && w.nlev >= 3 ? 1 : 0;
     // up: level 0 = chains (direction 1 reversed), then block aggregates until one block remains
     for (int lv = 0; lv < w.nlev; ++lv) {
         LsLevel L{};
@@ -595,6 +613,8 @@ cudaError_t launch_ls_product(const Plan &p, const LsWork &w, int mode, cudaStre
         L.excl[1] = w.lv_excl[lv][1];
         L.agg[0] = lv + 1 < w.nlev ? w.lv_agg[lv][0] : nullptr;
         L.agg[1] = lv + 1 < w.nlev ? w.lv_agg[lv][1] : nullptr;
+        L.car[0] = top_fused && lv == w.nlev - 1 ? w.lv_car[lv][0] : nullptr;
+        L.car[1] = top_fused && lv == w.nlev - 1 ? w.lv_car[lv][1] : nullptr;
         const dim3 g((unsigned)((L.n + kLsB - 1) / kLsB), 2);
         if (lv == 0 && tree0) k_ls_blockscan<true><<<g, kLsB * 32, smb, s>>>(L, p.stop);
         else if (lv == 0 || !red_up) k_ls_blockscan<false><<<g, kLsB * 32, smb, s>>>(L, p.stop);
@@ -603,6 +623,7 @@ cudaError_t launch_ls_product(const Plan &p, const LsWork &w, int mode, cudaStre
     }
     // down: carries of every level from the top; level 0's are the chain carries (scan order)
     for (int lv = w.nlev - 1; lv >= 1; --lv) {  // level 0: inside k_ls_apply
+        if ((top_fused && lv == w.nlev - 1) || (fuse1 && lv == 1)) continue;
         const int64_t n = w.lv_n[lv];
         const double *par0 = lv + 1 < w.nlev ? w.lv_car[lv + 1][0] : nullptr;
         const double *par1 = lv + 1 < w.nlev ? w.lv_car[lv + 1][1] : nullptr;
@@ -611,9 +632,9 @@ cudaError_t launch_ls_product(const Plan &p, const LsWork &w, int mode, cudaStre
         ++nl;
     }
     switch (mode) {
-        case MODE_UPD: k_ls_apply<MODE_UPD><<<wb, 128, 0, s>>>(p, w); break;
-        case MODE_MARG: k_ls_apply<MODE_MARG><<<wb, 128, 0, s>>>(p, w); break;
-        default: k_ls_apply<MODE_RES><<<wb, 128, 0, s>>>(p, w); break;
+        case MODE_UPD: k_ls_apply<MODE_UPD><<<wb, 128, 0, s>>>(p, w, fuse1); break;
+        case MODE_MARG: k_ls_apply<MODE_MARG><<<wb, 128, 0, s>>>(p, w, fuse1); break;
+        default: k_ls_apply<MODE_RES><<<wb, 128, 0, s>>>(p, w, fuse1); break;
     }
     *launches += 2 + nl;
     return cudaGetLastError();
