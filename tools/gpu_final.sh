@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round evidence: GPU tests, smoke, every config's bench line, reference arm, C4 launch list + ncu of
-# the update kernel, C5 ncu of the persistent kernel (reduced probe), C3 launch list.
+# the update kernel, C5 ncu of the pair kernel (full batch, 10 sweeps), C3 launch list.
 O=${OUT:-gpurun_out/final}
 mkdir -p $O
 if [ "${SKIP_TESTS:-0}" != "1" ]; then
@@ -18,8 +18,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sw_apply -s 20 -c 1 -o $O/prof_c4 $CMD > $O/ncu_c4.log 2>&1
 CMD3="python bench.py --config C3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_c3.csv $CMD3 > $O/ncu_launch3.log 2>&1
-timeout 300 python tools/c5_probe.py 1184 30 > $O/c5probe.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bat_sinkhorn -c 1 -o $O/prof_c5 python tools/c5_probe.py 1184 30 > $O/ncu_c5.log 2>&1
+# C5: the pair family's whole-solve kernel on the full batch, 10 sweeps (the bench's 300 would replay for minutes)
+timeout 300 python tools/c5_f32_probe.py 10 > $O/c5probe.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pair_sinkhorn -c 1 -o $O/prof_c5 python tools/c5_f32_probe.py 10 > $O/ncu_c5.log 2>&1
 python tools/prof_summary.py $O/launches_c4.csv $O/prof_c4.ncu-rep > $O/summary_c4.txt 2>&1
 python tools/prof_summary.py $O/launches_c3.csv > $O/summary_c3.txt 2>&1
 python tools/prof_summary.py $O/prof_c5.ncu-rep > $O/summary_c5.txt 2>&1
