@@ -213,3 +213,50 @@ def test_vshard_error_reported_by_every_rank():
 
     names = _run_ranks(G, rank)
     assert names == ["MMOT_ENONFINITE"] * G, names
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_vshard_c4_full_size_matches_single_context(G):
+    """The bench's multi-GPU C4 configuration (N = 1e8 sharded by grid chunks, AUTO kernels: exact
+    chain tiling per shard, restricted-scan exchange from the second update on) on G virtual shards
+    against the single-context solve of the same inputs (itself compared with the oracle at full
+    size in test_gpu_single_walk.py): scalings to 1e-9, W to 1e-10, and the plan's last marginal
+    equal to mu_l after the last update."""
+    cfg = mmot_inputs.CONFIGS["C4"]
+    l, N, eta, T = cfg.l, cfg.N, cfg.eta, 2
+    mus = mmot_inputs.make_marginals("C4", 0)
+    mu_d = [torch.from_numpy(np.ascontiguousarray(m)).to(DEV) for m in mus]
+    ctx = mm.Context(l, N, eta)
+    u0 = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in range(l)]
+    ctx.init_uniform(u0)
+    rep = ctx.sinkhorn(mu_d, T, 0.0, u0)
+    assert rep["status"] == 0
+    W0 = ctx.cost(u0)
+    ctx.close()
+    sl = _slices(N, G)
+
+    def rank(r, group):
+        lo, hi = sl[r]
+        c = mm.Context(l, N, eta, shard=(r, G, group))
+        u = [torch.empty(hi - lo, dtype=torch.float64, device=DEV) for _ in range(l)]
+        c.init_uniform(u)
+        rp = c.sinkhorn([m[lo:hi] for m in mu_d], T, 0.0, u)
+        W = c.cost(u)
+        m_last = c.marginal(l - 1, u)
+        torch.cuda.synchronize()
+        kern = c.info["kernel"]
+        c.close()
+        return rp, u, W, m_last, kern
+
+    res = _run_ranks(G, rank)
+    for r, (rp, u, W, m_last, kern) in enumerate(res):
+        lo, hi = sl[r]
+        assert rp["status"] == 0 and rp["iters_done"] == T
+        assert abs(W - W0) <= 1e-10 * abs(W0), (r, W, W0)
+        for q in range(l):
+            ref = u0[q][lo:hi]
+            d = torch.max(torch.abs(u[q] - ref) / torch.clamp(torch.abs(ref), min=1.0)).item()
+            assert d <= 1e-9, (r, q, d, kern)
+        dm = (torch.abs(m_last - mu_d[l - 1][lo:hi]).sum() / mu_d[l - 1][lo:hi].sum()).item()
+        assert dm <= 1e-10, (r, dm)
+    print(f"G={G}: shard kernels {[x[4] for x in res]}")
