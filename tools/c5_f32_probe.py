@@ -1,6 +1,6 @@
 """C5 in an MMOT_F32 context (pair family, fp32 arithmetic): how many instances leave the fp32 range
 (MMOT_DEBUG_FAIL=1 prints them; MMOT_NO_STABLE=1 skips the stabilised redo).  Usage:
-  python tools/c5_f32_probe.py [T]"""
+  python tools/c5_f32_probe.py [T] [B]      (B: the first B instances, e.g. 1024 = one rank of 8)"""
 import os
 import sys
 import time
@@ -15,7 +15,8 @@ import paper_2405_19246_b200 as mm  # noqa: E402
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 cfg = mmot_inputs.CONFIGS["C5"]
 l, N, B = cfg.l, cfg.N, cfg.batch
-etas = [float(e) for e in mmot_inputs.c5_etas(B)]
+B = int(sys.argv[2]) if len(sys.argv) > 2 else B
+etas = [float(e) for e in mmot_inputs.c5_etas(cfg.batch)[:B]]
 mus = mmot_inputs.c5_batch_marginals(0, B, N, l).astype(np.float32)
 dev = torch.device("cuda:0")
 mu_d = [torch.from_numpy(np.ascontiguousarray(mus[q])).to(dev) for q in range(l)]
@@ -27,4 +28,4 @@ t0 = time.perf_counter()
 rep = ctx.sinkhorn(mu_d, T, 0.0, u)
 torch.cuda.synchronize()
 print(f"T={T} status={rep['status']} {time.perf_counter() - t0:.3f} s pair={ctx.pair_solves} f32={ctx.pair_f32_solves} "
-      f"stable_redo={ctx.stable_fallbacks}", flush=True)
+      f"stable_redo={ctx.stable_fallbacks} B={B} kernel={ctx.info['kernel']}", flush=True)
